@@ -1,0 +1,120 @@
+/* gc.h -- C ABI of the B200 grid min-cut library (libgc.so).
+ *
+ * Operation (§4):
+ *   For each frame, the graph of P:331-357 -- one vertex per pixel, a source s and a
+ *   sink t, t-links c(s,v) = cap_s (the cost of label 0) and c(v,t) = cap_t
+ *   (the cost of label 1), and for every pixel p and direction k an n-link
+ *   p -> p+d_k of capacity cap_nb[k] (the "pair of mutually connected directed edges"
+ *   of footnote P:336-338; the two directions may differ).  The library computes the
+ *   maximum s-t flow value F* (= the minimum cut capacity) and the canonical minimum
+ *   cut: mask[v] = 1 iff v is reachable from s in the residual graph of a maximum
+ *   flow.  "The minimum cut ... provides the MAP configuration": mask = 1 is
+ *   label 1 (object, source side), mask = 0 is label 0 (background); among several
+ *   minimum cuts the mask is the inclusion-minimal one, i.e. ties go to label 0
+ *   (readings c1, c2).  Both outputs are unique functions of the input, so
+ *   they are compared bit-exactly with the CPU oracle.
+ *
+ * Direction order (k, (dy,dx)):  0 E(0,+1) 1 W(0,-1) 2 S(+1,0) 3 N(-1,0)
+ *                                4 SE(+1,+1) 5 NW(-1,-1) 6 SW(+1,-1) 7 NE(-1,+1);
+ *   opp(k) = k ^ 1.  4-neighbour frames use k = 0..3, 8-neighbour frames k = 0..7.
+ *   "Forward" directions (warm-start flow planes) are the even k: E, S[, SE, SW].
+ *
+ * Layout: every plane is row-major [H][W] (x fastest), int32 unless noted; a batch is
+ *   n frames back to back.  No alignment beyond the element size is required.
+ *
+ * Ownership: all I/O buffers belong to the caller.  gc_solve_batch takes CUDA DEVICE
+ *   pointers (e.g. torch tensors on the context's device); gc_solve_batch_host takes
+ *   HOST pointers (pinned memory recommended) and copies through the context's
+ *   staging buffers.  The context owns all scratch.  One context serves one device and
+ *   one caller at a time (not thread-safe); distinct contexts may run concurrently.
+ *
+ * Errors: host-checkable argument errors (NULL required pointer, n/H/W <= 0 or
+ *   H > max_h or W > max_w, bad neighbourhood) return GC_ERR_ARG before any launch.
+ *   Capacities are checked on the device: any in-grid capacity < 0 or > GC_CAP_MAX
+ *   makes that frame's flow_out = -1, its mask all 0, its stats status GC_ERR_RANGE,
+ *   and the call returns GC_ERR_RANGE (other frames are still solved).  n-link entries
+ *   that point off the grid are IGNORED (any value, reading c7).  If the solve needs
+ *   more than max_launches kernel launches the unfinished frames get flow_out = -1 and
+ *   the call returns GC_ERR_NOCONV.  CUDA failures return GC_ERR_CUDA; the message is
+ *   available from gc_last_error().  Calls return after all work on `stream` for this
+ *   call has completed.
+ */
+#ifndef GC_H
+#define GC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gc_ctx gc_ctx;
+
+typedef enum {
+  GC_OK = 0,
+  GC_ERR_ARG = 1,
+  GC_ERR_RANGE = 2,
+  GC_ERR_OOM = 3,
+  GC_ERR_CUDA = 4,
+  GC_ERR_NOCONV = 5
+} gc_status;
+
+#define GC_CAP_MAX ((1 << 26) - 1)
+
+/* 0 in any field selects the default. */
+typedef struct {
+  int device;            /* CUDA device ordinal (default: current device)                */
+  int neighborhood;      /* 4 or 8 (default 4)                                            */
+  int max_h, max_w;      /* largest frame the context will accept (default 1080 x 1920)  */
+  int max_batch;         /* frames solved concurrently per device pass (default: sized to
+                            keep the working set inside L2, at least 1)                  */
+  int rounds_per_launch; /* push/relabel rounds inside a tile per launch (default 16)    */
+  int relabel_period;    /* push launches between global relabels (default 4)            */
+  long long max_launches;/* per chunk; exceeded -> GC_ERR_NOCONV (default 1,000,000)     */
+} gc_config;
+
+/* Allocates the context and its device scratch.  *out is NULL on failure. */
+gc_status gc_create(const gc_config* cfg, gc_ctx** out);
+
+/* Frees the context and its scratch.  NULL is a no-op. */
+void gc_destroy(gc_ctx* ctx);
+
+typedef struct {
+  int n, H, W;
+  const int32_t* cap_s;      /* [n][H][W]   c(s->v): cost of label 0            */
+  const int32_t* cap_t;      /* [n][H][W]   c(v->t): cost of label 1            */
+  const int32_t* cap_nb;     /* [n][K][H][W] c(p -> p+d_k); off-grid entries ignored        */
+  const int32_t* warm_flow;  /* NULL, or [n][K/2][H][W]: net flow on the forward arcs
+                                (E, S[, SE, SW]) from any earlier solve (Kohli-Torr-style
+                                reuse); it is clamped to the new capacities, so
+                                any int32 values are accepted and the result is unchanged */
+  int64_t* flow_out;         /* [n] max-flow value of the graph as given                   */
+  uint8_t* mask_out;         /* [n][H][W] 1 iff reachable from s in the final residual     */
+  int32_t* flow_state_out;   /* NULL, or [n][K/2][H][W]: this solve's forward-arc flows    */
+  int32_t* stats_out;        /* NULL, or [n][4]: push launches, global relabels, BFS sweeps,
+                                status (gc_status of the frame)                            */
+} gc_batch;
+
+/* Device-pointer entry point.  `stream` is a cudaStream_t (NULL = legacy default). */
+gc_status gc_solve_batch(gc_ctx* ctx, const gc_batch* batch, void* stream);
+
+/* Host-pointer entry point: same semantics; the library copies inputs to the device and
+ * results back, in chunks, on `stream`.  All pointers in *batch are host pointers. */
+gc_status gc_solve_batch_host(gc_ctx* ctx, const gc_batch* batch, void* stream);
+
+/* Message for the last failing call on this context ("" if none).  Never NULL. */
+const char* gc_last_error(const gc_ctx* ctx);
+
+/* Number of kernel launches the last solve issued (for the bench's gpu_launches). */
+long long gc_last_launches(const gc_ctx* ctx);
+
+/* Profiling: when enabled, the library brackets every launch of each kernel class with
+ * CUDA events on the launching stream and accumulates device time.  Classes: 0 init,
+ * 1 bfs (seed+relax), 2 push, 3 status, 4 closure, 5 finalize.  Off by default. */
+void gc_set_profiling(gc_ctx* ctx, int enable);
+/* Fills launches[6] and ms[6] accumulated since the last reset; resets if reset != 0. */
+void gc_get_profile(gc_ctx* ctx, long long* launches, double* ms, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GC_H */

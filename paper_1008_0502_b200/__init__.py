@@ -1,0 +1,211 @@
+"""B200-native batched grid min-cut (the hot path of arXiv 1008.0502, §4 / §7.3).
+
+Thin ctypes binding over ``libgc.so`` (include/gc.h).  Argument marshalling only:
+every step of the solve runs in the library's sm_100a kernels.  There is no CPU or
+PyTorch fallback -- importing this package raises if the library is missing.
+
+Functions carry the C names (``gc_create``, ``gc_solve_batch``, ``gc_solve_batch_host``,
+``gc_destroy``, ``gc_last_error``, ...); :class:`GridCut` is a convenience wrapper
+that allocates outputs as torch tensors (device path) or numpy arrays (host path).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host",
+           "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "CAP_MAX",
+           "STATUS", "lib_path"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libgc.so")
+CAP_MAX = (1 << 26) - 1
+STATUS = {0: "GC_OK", 1: "GC_ERR_ARG", 2: "GC_ERR_RANGE", 3: "GC_ERR_OOM", 4: "GC_ERR_CUDA", 5: "GC_ERR_NOCONV"}
+PROFILE_CLASSES = ("init", "bfs", "push", "status", "closure", "finalize")
+
+if not os.path.exists(lib_path):
+    raise ImportError(f"{lib_path} is missing: build it with __graft_entry__.build() (make). "
+                      "There is no fallback implementation.")
+_lib = ctypes.CDLL(lib_path)
+
+
+class gc_config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("neighborhood", ctypes.c_int), ("max_h", ctypes.c_int),
+                ("max_w", ctypes.c_int), ("max_batch", ctypes.c_int), ("rounds_per_launch", ctypes.c_int),
+                ("relabel_period", ctypes.c_int), ("max_launches", ctypes.c_longlong)]
+
+
+class gc_batch(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int),
+                ("cap_s", ctypes.c_void_p), ("cap_t", ctypes.c_void_p), ("cap_nb", ctypes.c_void_p),
+                ("warm_flow", ctypes.c_void_p), ("flow_out", ctypes.c_void_p), ("mask_out", ctypes.c_void_p),
+                ("flow_state_out", ctypes.c_void_p), ("stats_out", ctypes.c_void_p)]
+
+
+_lib.gc_create.argtypes = [ctypes.POINTER(gc_config), ctypes.POINTER(ctypes.c_void_p)]
+_lib.gc_create.restype = ctypes.c_int
+_lib.gc_destroy.argtypes = [ctypes.c_void_p]
+_lib.gc_destroy.restype = None
+_lib.gc_solve_batch.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_batch), ctypes.c_void_p]
+_lib.gc_solve_batch.restype = ctypes.c_int
+_lib.gc_solve_batch_host.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_batch), ctypes.c_void_p]
+_lib.gc_solve_batch_host.restype = ctypes.c_int
+_lib.gc_last_error.argtypes = [ctypes.c_void_p]
+_lib.gc_last_error.restype = ctypes.c_char_p
+_lib.gc_last_launches.argtypes = [ctypes.c_void_p]
+_lib.gc_last_launches.restype = ctypes.c_longlong
+_lib.gc_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int]
+_lib.gc_set_profiling.restype = None
+_lib.gc_get_profile.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong),
+                                ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+_lib.gc_get_profile.restype = None
+
+EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
+            "gc_last_launches", "gc_set_profiling", "gc_get_profile")
+
+
+class GcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def gc_create(cfg: gc_config) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    st = _lib.gc_create(ctypes.byref(cfg), ctypes.byref(h))
+    if st != 0:
+        raise GcError(st, "gc_create failed")
+    return h
+
+
+def gc_destroy(ctx) -> None:
+    _lib.gc_destroy(ctx)
+
+
+def gc_solve_batch(ctx, batch: gc_batch, stream: int) -> int:
+    return _lib.gc_solve_batch(ctx, ctypes.byref(batch), ctypes.c_void_p(stream))
+
+
+def gc_solve_batch_host(ctx, batch: gc_batch, stream: int) -> int:
+    return _lib.gc_solve_batch_host(ctx, ctypes.byref(batch), ctypes.c_void_p(stream))
+
+
+def gc_last_error(ctx) -> str:
+    return _lib.gc_last_error(ctx).decode()
+
+
+def gc_last_launches(ctx) -> int:
+    return int(_lib.gc_last_launches(ctx))
+
+
+def gc_set_profiling(ctx, enable: bool) -> None:
+    _lib.gc_set_profiling(ctx, int(bool(enable)))
+
+
+def gc_get_profile(ctx, reset: bool = False):
+    n = (ctypes.c_longlong * 6)()
+    ms = (ctypes.c_double * 6)()
+    _lib.gc_get_profile(ctx, n, ms, int(bool(reset)))
+    return {c: (int(n[i]), float(ms[i])) for i, c in enumerate(PROFILE_CLASSES)}
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+class GridCut:
+    """One solver context (one device, one caller at a time).
+
+    ``solve`` takes torch int32 CUDA tensors cap_s [n,H,W], cap_t [n,H,W], cap_nb [n,K,H,W]
+    (and optionally warm_flow [n,K/2,H,W]) and returns int64 flow [n] and uint8 mask [n,H,W]
+    on the device.  ``solve_host`` does the same with numpy arrays (host buffers).
+    """
+
+    def __init__(self, neighborhood: int = 4, max_h: int = 1080, max_w: int = 1920, max_batch: int = 0,
+                 rounds_per_launch: int = 0, relabel_period: int = 0, max_launches: int = 0, device: int = 0):
+        self.K = neighborhood
+        cfg = gc_config(device, neighborhood, max_h, max_w, max_batch, rounds_per_launch, relabel_period,
+                        max_launches)
+        self.ctx = gc_create(cfg)
+
+    def close(self):
+        if self.ctx:
+            gc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int, allow=()):
+        if st != 0 and st not in allow:
+            raise GcError(st, gc_last_error(self.ctx))
+        return st
+
+    def solve(self, cap_s, cap_t, cap_nb, warm_flow=None, flow_state=False, stats=False, stream=None,
+              allow=(), out=None):
+        import torch
+        n, H, W = cap_s.shape
+        K = self.K
+        assert cap_nb.shape == (n, K, H, W), cap_nb.shape
+        for t in (cap_s, cap_t, cap_nb) + ((warm_flow,) if warm_flow is not None else ()):
+            assert t.dtype == torch.int32 and t.is_cuda and t.is_contiguous()
+        dev = cap_s.device
+        if out is None:
+            flow = torch.empty(n, dtype=torch.int64, device=dev)
+            mask = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
+        else:
+            flow, mask = out
+        fs = torch.empty((n, K // 2, H, W), dtype=torch.int32, device=dev) if flow_state else None
+        stt = torch.empty((n, 4), dtype=torch.int32, device=dev) if stats else None
+        b = gc_batch(n, H, W, _ptr(cap_s), _ptr(cap_t), _ptr(cap_nb), _ptr(warm_flow), _ptr(flow), _ptr(mask),
+                     _ptr(fs), _ptr(stt))
+        s = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
+        self.last_status = self._check(gc_solve_batch(self.ctx, b, s), allow)
+        res = [flow, mask]
+        if flow_state:
+            res.append(fs)
+        if stats:
+            res.append(stt)
+        return tuple(res)
+
+    def solve_host(self, cap_s, cap_t, cap_nb, warm_flow=None, flow_state=False, stats=False, stream=0,
+                   allow=(), out=None):
+        n, H, W = cap_s.shape
+        K = self.K
+        assert cap_nb.shape == (n, K, H, W)
+        for a in (cap_s, cap_t, cap_nb) + ((warm_flow,) if warm_flow is not None else ()):
+            assert a.dtype == np.int32 and a.flags["C_CONTIGUOUS"]
+        if out is None:
+            flow = np.empty(n, np.int64)
+            mask = np.empty((n, H, W), np.uint8)
+        else:
+            flow, mask = out
+        fs = np.empty((n, K // 2, H, W), np.int32) if flow_state else None
+        stt = np.empty((n, 4), np.int32) if stats else None
+        b = gc_batch(n, H, W, _ptr(cap_s), _ptr(cap_t), _ptr(cap_nb), _ptr(warm_flow), _ptr(flow), _ptr(mask),
+                     _ptr(fs), _ptr(stt))
+        self.last_status = self._check(gc_solve_batch_host(self.ctx, b, stream), allow)
+        res = [flow, mask]
+        if flow_state:
+            res.append(fs)
+        if stats:
+            res.append(stt)
+        return tuple(res)
+
+    def launches(self) -> int:
+        return gc_last_launches(self.ctx)
+
+    def set_profiling(self, on: bool):
+        gc_set_profiling(self.ctx, on)
+
+    def profile(self, reset=False):
+        return gc_get_profile(self.ctx, reset)

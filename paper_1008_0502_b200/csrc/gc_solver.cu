@@ -1,0 +1,422 @@
+// gc_solver.cu -- host driver and C ABI (include/gc.h) of the B200 grid min-cut library.
+//
+// Per chunk of frames (all frames of a chunk share H, W, K):
+//   init (a1 / a1w) -> loop { global relabel: seed sweep + relax sweeps until no border
+//   change (a2); status: frames with no active node are done; R push launches (a3) }
+//   -> closure seed + relax sweeps (a4) -> finalize (mask, F, flow export a5).
+// The loop polls two device flags per iteration through pinned host memory.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "gc.h"
+#include "gc_kernels.cuh"
+
+using namespace gcb;
+
+struct gc_ctx {
+  int dev = 0, K = 4, max_h = 0, max_w = 0, max_batch = 0, rounds = 16, period = 4;
+  long long max_launches = 1000000;
+  size_t pool_bytes = 0;
+  char* pool = nullptr;
+  int32_t* hpin = nullptr;  // pinned host words for polling
+  std::string err;
+  long long last_launches = 0;
+  bool prof = false;
+  long long prof_n[6] = {0, 0, 0, 0, 0, 0};
+  double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<cudaEvent_t> evpool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  size_t evnext = 0;
+  // host-API staging (device)
+  char* stage = nullptr;
+  size_t stage_bytes = 0;
+};
+
+namespace {
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bytes of scratch per frame with T tiles.
+size_t frame_bytes(int K, size_t T) {
+  size_t b = 0;
+  b += 2 * T * TPX * 4;           // e, h
+  b += (size_t)K * T * TPX * 4;   // r
+  b += T * 128 * 4;               // hedge
+  b += 2 * T * K * 64 * 4;        // inbox
+  b += T * K * 64;                // reach
+  b += 2 * T * TPX;               // m, open
+  b += 7 * T * 4;                 // tile flags
+  b += 64;                        // frame words
+  return b + 4096;
+}
+
+int tiles_of(int H, int W) { return ((H + TS - 1) / TS) * ((W + TS - 1) / TS); }
+
+// Carve the pool for nslot frames of geometry H x W.
+Dev carve(gc_ctx* c, int nslot, int H, int W) {
+  Dev d;
+  memset(&d, 0, sizeof(d));
+  d.H = H; d.W = W;
+  d.TY = (H + TS - 1) / TS; d.TX = (W + TS - 1) / TS; d.T = d.TY * d.TX;
+  d.nslot = nslot;
+  d.hmax = d.T * TPX + 2;
+  const size_t T = d.T, ns = (size_t)nslot * T, K = c->K;
+  char* p = c->pool;
+  auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
+  d.e = (int32_t*)take(ns * TPX * 4);
+  d.h = (int32_t*)take(ns * TPX * 4);
+  d.r = (int32_t*)take(ns * K * TPX * 4);
+  d.hedge = (int32_t*)take(ns * 128 * 4);
+  d.inbox = (int32_t*)take(2 * ns * K * 64 * 4);
+  d.reach = (uint8_t*)take(ns * K * 64);
+  d.m = (uint8_t*)take(ns * TPX);
+  d.open = (uint8_t*)take(ns * TPX);
+  d.tact = (int32_t*)take(ns * 4);
+  d.bchg = (int32_t*)take(2 * ns * 4);
+  d.recv = (int32_t*)take(2 * ns * 4);
+  d.crecv = (int32_t*)take(2 * ns * 4);
+  // per-frame words: contiguous so one memset clears them
+  char* fw = take((size_t)nslot * (4 + 4 + 16 + 8 + 8) + 64 * 4 + 8 * 4 + 64);
+  d.fdone = (int32_t*)fw;
+  d.ferr = d.fdone + nslot;
+  d.fstat = d.ferr + nslot;
+  d.sumct = (unsigned long long*)align_up((size_t)(d.fstat + 4 * nslot), 8);
+  d.sumneg = d.sumct + nslot;
+  d.ring = (int32_t*)(d.sumneg + nslot);
+  d.ctr = d.ring + 64;
+  return d;
+}
+
+size_t frame_words_bytes(const Dev& d) { return (char*)(d.ctr + 8) - (char*)d.fdone; }
+
+bool ck(gc_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return true;
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+  c->err = buf;
+  return false;
+}
+
+struct Launcher {
+  gc_ctx* c;
+  cudaStream_t st;
+  long long n = 0;
+  void pre(int cls) {
+    if (!c->prof) return;
+    if (c->evnext + 2 > c->evpool.size()) {
+      for (int i = 0; i < 256; ++i) {
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        c->evpool.push_back(ev);
+      }
+    }
+    cudaEvent_t a = c->evpool[c->evnext++], b = c->evpool[c->evnext++];
+    cudaEventRecord(a, st);
+    c->pending.push_back({cls, {a, b}});
+  }
+  void post() {
+    ++n;
+    if (!c->prof) return;
+    cudaEventRecord(c->pending.back().second.second, st);
+  }
+};
+
+void resolve_profile(gc_ctx* c) {
+  for (auto& p : c->pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+    c->prof_n[p.first] += 1;
+    c->prof_ms[p.first] += ms;
+  }
+  c->pending.clear();
+  c->evnext = 0;
+}
+
+template <int K>
+gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStream_t st, Launcher& L) {
+  Dev d = carve(c, nslot, H, W);
+  const dim3 grid(d.T, nslot), blk(NTH);
+  if (!ck(c, cudaMemsetAsync(d.fdone, 0, frame_words_bytes(d), st), "memset")) return GC_ERR_CUDA;
+  L.pre(0);
+  if (io.wf) k_init<K, true><<<grid, blk, 0, st>>>(d, io);
+  else k_init<K, false><<<grid, blk, 0, st>>>(d, io);
+  L.post();
+  if (!ck(c, cudaGetLastError(), "k_init")) return GC_ERR_CUDA;
+
+  int push_launches = 0, relabels = 0, sweeps = 0, last_par = -1, sw = 0;
+  const int BATCH = 4;
+  gc_status status = GC_OK;
+  auto poll = [&](const int32_t* dptr) -> int {
+    cudaMemcpyAsync(c->hpin, dptr, 4, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return c->hpin[0];
+  };
+  for (;;) {
+    // ---- a2: exact global relabel
+    L.pre(1);
+    k_bfs_seed<K><<<grid, blk, 0, st>>>(d, last_par, sw);
+    L.post();
+    last_par = -1;
+    ++sw; ++sweeps; ++relabels;
+    for (;;) {
+      for (int b = 0; b < BATCH; ++b) {
+        L.pre(1);
+        k_bfs_relax<K><<<grid, blk, 0, st>>>(d, sw);
+        L.post();
+        ++sw; ++sweeps;
+      }
+      if (!ck(c, cudaGetLastError(), "k_bfs_relax")) return GC_ERR_CUDA;
+      if (!poll(d.ring + ((sw - 1) & 63))) break;
+      if (L.n > c->max_launches) { status = GC_ERR_NOCONV; break; }
+    }
+    if (status == GC_ERR_NOCONV) break;  // labels not final: leave unfinished frames not-done
+    // ---- status: done frames have no active node reaching the sink
+    cudaMemsetAsync(d.ctr, 0, 4, st);
+    L.pre(3);
+    k_status<<<nslot, NTH, 0, st>>>(d, push_launches, relabels, sweeps);
+    L.post();
+    if (!poll(d.ctr)) break;
+    if (L.n > c->max_launches) { status = GC_ERR_NOCONV; break; }
+    // ---- a3: push launches
+    for (int j = 0; j < c->period; ++j) {
+      const int par_out = push_launches & 1;
+      const int par_in = (j == 0) ? -1 : (par_out ^ 1);
+      L.pre(2);
+      k_push<K><<<grid, blk, 0, st>>>(d, par_in, par_out, c->rounds);
+      L.post();
+      ++push_launches;
+      last_par = par_out;
+    }
+    if (!ck(c, cudaGetLastError(), "k_push")) return GC_ERR_CUDA;
+  }
+  // ---- a4: canonical mask
+  L.pre(4);
+  k_closure_seed<K><<<grid, blk, 0, st>>>(d, sw);
+  L.post();
+  ++sw;
+  if (poll(d.ring + ((sw - 1) & 63))) {
+    for (;;) {
+      for (int b = 0; b < BATCH; ++b) {
+        L.pre(4);
+        k_closure_relax<K><<<grid, blk, 0, st>>>(d, sw);
+        L.post();
+        ++sw;
+      }
+      if (!ck(c, cudaGetLastError(), "k_closure_relax")) return GC_ERR_CUDA;
+      if (!poll(d.ring + ((sw - 1) & 63))) break;
+    }
+  }
+  L.pre(5);
+  k_finalize<K><<<grid, blk, 0, st>>>(d, io);
+  L.post();
+  cudaMemsetAsync(d.ctr, 0, 16, st);
+  k_flow<<<(nslot + 127) / 128, 128, 0, st>>>(d, io);
+  ++L.n;
+  if (!ck(c, cudaGetLastError(), "k_finalize")) return GC_ERR_CUDA;
+  cudaMemcpyAsync(c->hpin, d.ctr, 12, cudaMemcpyDeviceToHost, st);
+  if (!ck(c, cudaStreamSynchronize(st), "solve")) return GC_ERR_CUDA;
+  if (c->hpin[1]) return GC_ERR_RANGE;
+  if (c->hpin[2] || status == GC_ERR_NOCONV) return GC_ERR_NOCONV;
+  return GC_OK;
+}
+
+gc_status check_batch(gc_ctx* c, const gc_batch* b) {
+  if (!c) return GC_ERR_ARG;
+  if (!b) { c->err = "batch is NULL"; return GC_ERR_ARG; }
+  if (b->n < 0 || b->H <= 0 || b->W <= 0 || b->H > c->max_h || b->W > c->max_w) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "bad dims n=%d H=%d W=%d (max %dx%d)", b->n, b->H, b->W, c->max_h, c->max_w);
+    c->err = buf;
+    return GC_ERR_ARG;
+  }
+  if (b->n > 0 && (!b->cap_s || !b->cap_t || !b->cap_nb || !b->flow_out || !b->mask_out)) {
+    c->err = "NULL required pointer";
+    return GC_ERR_ARG;
+  }
+  return GC_OK;
+}
+
+int chunk_frames(gc_ctx* c, int H, int W) {
+  const size_t fb = frame_bytes(c->K, tiles_of(H, W));
+  size_t n = c->pool_bytes / fb;
+  if (n < 1) n = 1;
+  if (c->max_batch > 0 && n > (size_t)c->max_batch) n = c->max_batch;
+  const char* env = getenv("GC_CHUNK");
+  if (env && atoi(env) > 0 && (size_t)atoi(env) < n) n = atoi(env);
+  return (int)n;
+}
+
+gc_status worst(gc_status a, gc_status b) {
+  if (a == GC_ERR_CUDA || b == GC_ERR_CUDA) return GC_ERR_CUDA;
+  if (a == GC_ERR_RANGE || b == GC_ERR_RANGE) return GC_ERR_RANGE;
+  if (a == GC_ERR_NOCONV || b == GC_ERR_NOCONV) return GC_ERR_NOCONV;
+  return a != GC_OK ? a : b;
+}
+
+}  // namespace
+
+extern "C" {
+
+gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
+  if (!out) return GC_ERR_ARG;
+  *out = nullptr;
+  gc_config z;
+  memset(&z, 0, sizeof(z));
+  const gc_config& g = cfg ? *cfg : z;
+  gc_ctx* c = new gc_ctx();
+  if (cudaGetDevice(&c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
+  if (g.device > 0) c->dev = g.device;
+  c->K = g.neighborhood ? g.neighborhood : 4;
+  if (c->K != 4 && c->K != 8) { delete c; return GC_ERR_ARG; }
+  c->max_h = g.max_h > 0 ? g.max_h : 1080;
+  c->max_w = g.max_w > 0 ? g.max_w : 1920;
+  c->rounds = g.rounds_per_launch > 0 ? g.rounds_per_launch : 16;
+  c->period = g.relabel_period > 0 ? g.relabel_period : 4;
+  c->max_launches = g.max_launches > 0 ? g.max_launches : 1000000;
+  c->max_batch = g.max_batch > 0 ? g.max_batch : 0;
+  if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
+  if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
+  const size_t fb = frame_bytes(c->K, tiles_of(c->max_h, c->max_w));
+  size_t nf;
+  if (c->max_batch > 0) {
+    nf = c->max_batch;
+  } else {
+    // default: keep one chunk's working set inside L2 (126 MB on B200), at least 1 frame
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->dev);
+    size_t budget = l2 > 0 ? (size_t)l2 * 3 / 4 : ((size_t)96 << 20);
+    nf = budget / fb;
+    if (nf < 1) nf = 1;
+  }
+  c->pool_bytes = nf * fb;
+  if (cudaMalloc(&c->pool, c->pool_bytes) != cudaSuccess) { cudaGetLastError(); delete c; return GC_ERR_OOM; }
+  if (cudaMallocHost(&c->hpin, 64) != cudaSuccess) { cudaFree(c->pool); delete c; return GC_ERR_OOM; }
+  *out = c;
+  return GC_OK;
+}
+
+void gc_destroy(gc_ctx* c) {
+  if (!c) return;
+  for (auto ev : c->evpool) cudaEventDestroy(ev);
+  if (c->pool) cudaFree(c->pool);
+  if (c->stage) cudaFree(c->stage);
+  if (c->hpin) cudaFreeHost(c->hpin);
+  delete c;
+}
+
+const char* gc_last_error(const gc_ctx* c) { return c ? c->err.c_str() : "NULL context"; }
+
+long long gc_last_launches(const gc_ctx* c) { return c ? c->last_launches : 0; }
+
+void gc_set_profiling(gc_ctx* c, int enable) {
+  if (c) c->prof = enable != 0;
+}
+
+void gc_get_profile(gc_ctx* c, long long* launches, double* ms, int reset) {
+  if (!c) return;
+  for (int i = 0; i < 6; ++i) {
+    if (launches) launches[i] = c->prof_n[i];
+    if (ms) ms[i] = c->prof_ms[i];
+  }
+  if (reset)
+    for (int i = 0; i < 6; ++i) { c->prof_n[i] = 0; c->prof_ms[i] = 0; }
+}
+
+gc_status gc_solve_batch(gc_ctx* c, const gc_batch* b, void* stream) {
+  gc_status s0 = check_batch(c, b);
+  if (s0 != GC_OK) return s0;
+  c->err.clear();
+  cudaSetDevice(c->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int H = b->H, W = b->W, K = c->K;
+  const size_t plane = (size_t)H * W;
+  const int chunk = chunk_frames(c, H, W);
+  Launcher L{c, st};
+  gc_status res = GC_OK;
+  for (int f0 = 0; f0 < b->n; f0 += chunk) {
+    const int m = b->n - f0 < chunk ? b->n - f0 : chunk;
+    IO io;
+    io.cs = b->cap_s + f0 * plane;
+    io.ct = b->cap_t + f0 * plane;
+    io.nb = b->cap_nb + f0 * plane * K;
+    io.wf = b->warm_flow ? b->warm_flow + f0 * plane * (K / 2) : nullptr;
+    io.flow = b->flow_out + f0;
+    io.mask = b->mask_out + f0 * plane;
+    io.fstate = b->flow_state_out ? b->flow_state_out + f0 * plane * (K / 2) : nullptr;
+    io.stats = b->stats_out ? b->stats_out + f0 * 4 : nullptr;
+    gc_status r = (K == 8) ? solve_chunk<8>(c, io, m, H, W, st, L) : solve_chunk<4>(c, io, m, H, W, st, L);
+    res = worst(res, r);
+    if (r == GC_ERR_CUDA) break;
+  }
+  c->last_launches = L.n;
+  if (c->prof) resolve_profile(c);
+  if (res == GC_ERR_RANGE && c->err.empty()) c->err = "capacity out of range [0, GC_CAP_MAX] in some frame";
+  if (res == GC_ERR_NOCONV && c->err.empty()) c->err = "max_launches exceeded before convergence";
+  return res;
+}
+
+gc_status gc_solve_batch_host(gc_ctx* c, const gc_batch* b, void* stream) {
+  gc_status s0 = check_batch(c, b);
+  if (s0 != GC_OK) return s0;
+  c->err.clear();
+  cudaSetDevice(c->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int H = b->H, W = b->W, K = c->K;
+  const size_t plane = (size_t)H * W;
+  int chunk = chunk_frames(c, H, W);
+  // staging: caps (2+K planes), warm (K/2), flow state (K/2), mask (1 B), flow (8 B), stats
+  const size_t per = plane * 4 * (2 + K) + (b->warm_flow ? plane * 4 * (K / 2) : 0) +
+                     (b->flow_state_out ? plane * 4 * (K / 2) : 0) + plane + 8 + 16 + 4 * 256;
+  const size_t need = per * chunk;
+  if (need > c->stage_bytes) {
+    if (c->stage) cudaFree(c->stage);
+    c->stage = nullptr;
+    c->stage_bytes = 0;
+    if (cudaMalloc(&c->stage, need) != cudaSuccess) { cudaGetLastError(); c->err = "staging alloc"; return GC_ERR_OOM; }
+    c->stage_bytes = need;
+  }
+  gc_status res = GC_OK;
+  Launcher L{c, st};
+  for (int f0 = 0; f0 < b->n; f0 += chunk) {
+    const int m = b->n - f0 < chunk ? b->n - f0 : chunk;
+    char* p = c->stage;
+    auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
+    int32_t* dcs = (int32_t*)take(m * plane * 4);
+    int32_t* dct = (int32_t*)take(m * plane * 4);
+    int32_t* dnb = (int32_t*)take(m * plane * 4 * K);
+    int32_t* dwf = b->warm_flow ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
+    int32_t* dfs = b->flow_state_out ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
+    uint8_t* dmask = (uint8_t*)take(m * plane);
+    int64_t* dflow = (int64_t*)take(m * 8);
+    int32_t* dstats = (int32_t*)take(m * 16);
+    cudaMemcpyAsync(dcs, b->cap_s + f0 * plane, m * plane * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dct, b->cap_t + f0 * plane, m * plane * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dnb, b->cap_nb + f0 * plane * K, m * plane * 4 * K, cudaMemcpyHostToDevice, st);
+    if (dwf)
+      cudaMemcpyAsync(dwf, b->warm_flow + f0 * plane * (K / 2), m * plane * 4 * (K / 2), cudaMemcpyHostToDevice, st);
+    IO io{dcs, dct, dnb, dwf, dflow, dmask, dfs, dstats};
+    gc_status r = (K == 8) ? solve_chunk<8>(c, io, m, H, W, st, L) : solve_chunk<4>(c, io, m, H, W, st, L);
+    res = worst(res, r);
+    if (r == GC_ERR_CUDA) break;
+    cudaMemcpyAsync(b->mask_out + f0 * plane, dmask, m * plane, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(b->flow_out + f0, dflow, m * 8, cudaMemcpyDeviceToHost, st);
+    if (b->stats_out) cudaMemcpyAsync(b->stats_out + f0 * 4, dstats, m * 16, cudaMemcpyDeviceToHost, st);
+    if (dfs)
+      cudaMemcpyAsync(b->flow_state_out + f0 * plane * (K / 2), dfs, m * plane * 4 * (K / 2), cudaMemcpyDeviceToHost,
+                      st);
+  }
+  if (!ck(c, cudaStreamSynchronize(st), "host solve")) res = GC_ERR_CUDA;
+  c->last_launches = L.n;
+  if (c->prof) resolve_profile(c);
+  if (res == GC_ERR_RANGE && c->err.empty()) c->err = "capacity out of range [0, GC_CAP_MAX] in some frame";
+  if (res == GC_ERR_NOCONV && c->err.empty()) c->err = "max_launches exceeded before convergence";
+  return res;
+}
+
+}  // extern "C"

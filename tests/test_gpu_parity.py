@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact in both
+the flow value (int64) and the canonical mask (uint8) -- SURVEY.md §8(c)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DY = [0, 0, 1, -1, 1, -1, 1, -1]
+DX = [1, -1, 0, 0, 1, -1, -1, 1]
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as _t
+    assert _t.cuda.is_available(), "GPU tests need a CUDA device"
+    return _t
+
+
+@pytest.fixture(scope="module")
+def gc():
+    import paper_1008_0502_b200 as _gc
+    return _gc
+
+
+_SOLVERS = {}
+
+
+def solver(gc, K, max_h=1080, max_w=1920, **kw):
+    key = (K, max_h, max_w, tuple(sorted(kw.items())))
+    if key not in _SOLVERS:
+        _SOLVERS[key] = gc.GridCut(neighborhood=K, max_h=max_h, max_w=max_w, **kw)
+    return _SOLVERS[key]
+
+
+def to_dev(torch, *arrs):
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrs]
+
+
+def check_against_oracle(cs, ct, nb, F, mask, algo="dinic", frames=None):
+    n = cs.shape[0]
+    idx = range(n) if frames is None else frames
+    for i in idx:
+        Fo, mo = oracle.solve(cs[i], ct[i], nb[i], algo)
+        assert int(F[i]) == Fo, f"frame {i}: F gpu {int(F[i])} oracle {Fo}"
+        if not np.array_equal(mask[i], mo):
+            bad = np.argwhere(mask[i] != mo)
+            raise AssertionError(f"frame {i}: {len(bad)} mask mismatches, first {bad[:5].tolist()}")
+
+
+def cut_cert(cs, ct, nb, f):
+    """Oracle-free certificate: e from caps and the exported forward flow;
+    F(f) = sum ct - sum max(0,-e); returns (feasible, F(f))."""
+    K, H, W = nb.shape
+    e = cs.astype(np.int64) - ct.astype(np.int64)
+    ok = True
+    for j in range(K // 2):
+        k = 2 * j
+        fj = f[j].astype(np.int64)
+        y0, y1 = max(0, -DY[k]), H - max(0, DY[k])
+        x0, x1 = max(0, -DX[k]), W - max(0, DX[k])
+        src = fj[y0:y1, x0:x1]
+        cfw = nb[k, y0:y1, x0:x1].astype(np.int64)
+        crv = nb[k ^ 1, y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]].astype(np.int64)
+        ok &= bool(np.all(src <= cfw) and np.all(-src <= crv))
+        e[y0:y1, x0:x1] -= src
+        e[y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]] += src
+        # off-grid flows must be zero
+        full = np.zeros_like(fj, bool)
+        full[y0:y1, x0:x1] = True
+        ok &= bool(np.all(fj[~full] == 0))
+    return ok, int(ct.astype(np.int64).sum() - np.maximum(0, -e).sum())
+
+
+# ----------------------------------------------------------------------------- generator twin
+@pytest.mark.parametrize("kind,H,W,K", [("blob", 48, 64, 4), ("blob", 240, 320, 8), ("serpentine", 100, 130, 4),
+                                        ("random", 33, 47, 8)])
+def test_generator_twins_bit_identical(torch, kind, H, W, K):
+    a = synth.gen_host(kind, 99, 4, 3, H, W, K)
+    b = synth.gen_torch(kind, 99, 4, 3, H, W, K)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y.cpu().numpy())
+
+
+# ----------------------------------------------------------------------------- small random
+SIZES = [(1, 1), (1, 7), (5, 1), (2, 2), (3, 5), (8, 8), (13, 31), (31, 33), (32, 32), (33, 32), (32, 65),
+         (47, 29), (64, 64), (70, 97)]
+
+
+@pytest.mark.parametrize("K", [4, 8])
+def test_random_grids_parity(torch, gc, K):
+    rng = np.random.default_rng(500 + K)
+    g = solver(gc, K, 128, 128)
+    for (H, W) in SIZES:
+        for tmax, nmax in [(3, 3), (20, 20), (1000, 50), (50, 1000)]:
+            cs, ct, nb = synth.random_caps(rng, H, W, K, tmax=tmax, nmax=nmax, zero_frac=0.3, garbage=True, n=3)
+            F, mask = g.solve(*to_dev(torch, cs, ct, nb))
+            check_against_oracle(cs, ct, nb, F.cpu().numpy(), mask.cpu().numpy())
+
+
+@pytest.mark.parametrize("K", [4, 8])
+def test_extreme_caps(torch, gc, K):
+    """CAP_MAX-edge capacities (int32 headroom of e and r) and all-zero frames."""
+    rng = np.random.default_rng(77)
+    g = solver(gc, K, 128, 128)
+    H, W = 40, 50
+    cs = rng.choice([0, gc.CAP_MAX, gc.CAP_MAX - 1, 1], size=(2, H, W)).astype(np.int32)
+    ct = rng.choice([0, gc.CAP_MAX, 2], size=(2, H, W)).astype(np.int32)
+    nb = rng.choice([0, gc.CAP_MAX, 5], size=(2, K, H, W)).astype(np.int32)
+    cs[1] = 0; ct[1] = 0; nb[1] = 0
+    F, mask = g.solve(*to_dev(torch, cs, ct, nb))
+    check_against_oracle(cs, ct, nb, F.cpu().numpy(), mask.cpu().numpy())
+
+
+# ----------------------------------------------------------------------------- configs
+@pytest.mark.parametrize("K", [4, 8])
+def test_c1_blob_64x48(torch, gc, K):
+    cs, ct, nb = synth.gen_host("blob", synth.BASE_SEED + 0, 0, 1, 48, 64, K)
+    g = solver(gc, K)
+    F, mask, fs = g.solve(*to_dev(torch, cs, ct, nb), flow_state=True)
+    F, mask, fs = F.cpu().numpy(), mask.cpu().numpy(), fs.cpu().numpy()
+    check_against_oracle(cs, ct, nb, F, mask, "dinic")
+    check_against_oracle(cs, ct, nb, F, mask, "bk")
+    ok, Ff = cut_cert(cs[0], ct[0], nb[0], fs[0])
+    assert ok and Ff == int(F[0]) == oracle.cut_value(cs[0], ct[0], nb[0], mask[0])
+
+
+def test_c2_qvga_clip_sample(torch, gc):
+    """C2 shape: 320x240 4-nbr blob frames, independent cold solves (40 of the 300)."""
+    n = 40
+    cs, ct, nb = synth.gen_torch("blob", synth.BASE_SEED + 1, 0, n, 240, 320, 4)
+    g = solver(gc, 4)
+    F, mask, st = g.solve(cs, ct, nb, stats=True)
+    torch.cuda.synchronize()
+    hc, ht, hn = synth.gen_host("blob", synth.BASE_SEED + 1, 0, n, 240, 320, 4)
+    Fo, mo = oracle.solve_batch(hc, ht, hn, "bk")
+    np.testing.assert_array_equal(F.cpu().numpy(), Fo)
+    np.testing.assert_array_equal(mask.cpu().numpy(), mo)
+    assert np.all(st.cpu().numpy()[:, 3] == 0)
+
+
+def test_c3_vga_warm_start(torch, gc):
+    """C3: 640x480 sequence; frame t>=1 warm-started from t-1's exported flows.
+    warm == cold == oracle on every frame."""
+    n = 6
+    cs, ct, nb = synth.gen_torch("blob", synth.BASE_SEED + 2, 0, n, 480, 640, 4, seq_len=120)
+    g = solver(gc, 4)
+    Fc, mc, fc = g.solve(cs, ct, nb, flow_state=True)
+    prev = fc[0:1]
+    Fw, mw = [Fc[0:1]], [mc[0:1]]
+    for t in range(1, n):
+        F1, m1, f1 = g.solve(cs[t:t + 1], ct[t:t + 1], nb[t:t + 1], warm_flow=prev.contiguous(), flow_state=True)
+        Fw.append(F1); mw.append(m1); prev = f1
+    Fw, mw = torch.cat(Fw), torch.cat(mw)
+    np.testing.assert_array_equal(Fw.cpu().numpy(), Fc.cpu().numpy())
+    np.testing.assert_array_equal(mw.cpu().numpy(), mc.cpu().numpy())
+    hc, ht, hn = synth.gen_host("blob", synth.BASE_SEED + 2, 0, n, 480, 640, 4, seq_len=120)
+    Fo, mo = oracle.solve_batch(hc, ht, hn, "bk")
+    np.testing.assert_array_equal(Fc.cpu().numpy(), Fo)
+    np.testing.assert_array_equal(mc.cpu().numpy(), mo)
+
+
+def test_warm_start_from_garbage_flow(torch, gc):
+    """Any int32 warm flow is clamped, so the result equals the cold solve."""
+    rng = np.random.default_rng(5)
+    cs, ct, nb = synth.gen_host("blob", 3, 1, 2, 60, 70, 8)
+    wf = rng.integers(-(1 << 31), (1 << 31) - 1, size=(2, 4, 60, 70), dtype=np.int64).astype(np.int32)
+    g = solver(gc, 8)
+    F, m = g.solve(*to_dev(torch, cs, ct, nb, wf)[:3], warm_flow=to_dev(torch, wf)[0])
+    check_against_oracle(cs, ct, nb, F.cpu().numpy(), m.cpu().numpy())
+
+
+def test_c4_1080p_8nbr_sample(torch, gc):
+    """C4 shape: 1920x1080 8-neighbour frames (2 of the 1024), full-size parity."""
+    n = 2
+    cs, ct, nb = synth.gen_torch("blob", synth.BASE_SEED + 3, 0, n, 1080, 1920, 8)
+    g = solver(gc, 8)
+    F, mask, fs = g.solve(cs, ct, nb, flow_state=True)
+    torch.cuda.synchronize()
+    hc, ht, hn = synth.gen_host("blob", synth.BASE_SEED + 3, 0, n, 1080, 1920, 8)
+    Fo, mo = oracle.solve_batch(hc, ht, hn, "bk")
+    np.testing.assert_array_equal(F.cpu().numpy(), Fo)
+    np.testing.assert_array_equal(mask.cpu().numpy(), mo)
+    fsn = fs.cpu().numpy()
+    for i in range(n):
+        ok, Ff = cut_cert(hc[i], ht[i], hn[i], fsn[i])
+        assert ok and Ff == Fo[i]
+
+
+def test_serpentine_adversarial_small(torch, gc):
+    """C5 shape at reduced size: long snaking augmenting paths."""
+    synth.set_serpentine_params(lane=16, big=1 << 20)
+    try:
+        cs, ct, nb = synth.gen_host("serpentine", synth.BASE_SEED + 4, 0, 2, 256, 384, 4)
+    finally:
+        synth.set_serpentine_params()
+    g = solver(gc, 4)
+    F, mask = g.solve(*to_dev(torch, cs, ct, nb))
+    check_against_oracle(cs, ct, nb, F.cpu().numpy(), mask.cpu().numpy(), "bk")
+
+
+# ----------------------------------------------------------------------------- ABI behaviour
+def test_host_entry_point_matches_device(torch, gc):
+    cs, ct, nb = synth.gen_host("blob", 8, 0, 5, 120, 160, 4)
+    g = solver(gc, 4)
+    Fd, md = g.solve(*to_dev(torch, cs, ct, nb))
+    Fh, mh = g.solve_host(cs, ct, nb)
+    np.testing.assert_array_equal(Fh, Fd.cpu().numpy())
+    np.testing.assert_array_equal(mh, md.cpu().numpy())
+    assert g.launches() > 0
+
+
+def test_range_error(torch, gc):
+    cs, ct, nb = synth.gen_host("blob", 9, 0, 3, 40, 40, 4, garbage=True)
+    cs[1, 5, 5] = -1
+    nb[2, 0, 10, 10] = gc.CAP_MAX + 1
+    g = solver(gc, 4)
+    F, m = g.solve(*to_dev(torch, cs, ct, nb), allow=(2,))
+    assert g.last_status == 2
+    F = F.cpu().numpy()
+    assert F[1] == -1 and F[2] == -1 and F[0] >= 0
+    assert m.cpu().numpy()[1].sum() == 0
+    check_against_oracle(cs, ct, nb, F, m.cpu().numpy(), frames=[0])
+
+
+def test_arg_errors(torch, gc):
+    g = solver(gc, 4, 64, 64)
+    cs, ct, nb = to_dev(torch, *synth.gen_host("blob", 1, 0, 1, 70, 70, 4))
+    with pytest.raises(gc.GcError) as ei:
+        g.solve(cs, ct, nb)
+    assert ei.value.status == 1
+    b = gc.gc_batch(1, 10, 10, None, None, None, None, None, None, None, None)
+    assert gc.gc_solve_batch(g.ctx, b, 0) == 1
+
+
+def test_noconv(torch, gc):
+    synth.set_serpentine_params(lane=4, big=1 << 20)
+    try:
+        cs, ct, nb = synth.gen_host("serpentine", 5, 0, 1, 128, 128, 4)
+    finally:
+        synth.set_serpentine_params()
+    g = gc.GridCut(neighborhood=4, max_h=128, max_w=128, max_launches=3)
+    F, m = g.solve(*to_dev(torch, cs, ct, nb), allow=(5,))
+    assert g.last_status == 5 and int(F[0]) == -1
+    g.close()
+
+
+def test_two_contexts_interleaved(torch, gc):
+    a = gc.GridCut(neighborhood=4, max_h=100, max_w=100)
+    b = gc.GridCut(neighborhood=8, max_h=100, max_w=100)
+    c4 = synth.gen_host("blob", 2, 0, 2, 90, 100, 4)
+    c8 = synth.gen_host("blob", 2, 0, 2, 90, 100, 8)
+    Fa, ma = a.solve(*to_dev(torch, *c4))
+    Fb, mb = b.solve(*to_dev(torch, *c8))
+    check_against_oracle(*c4, Fa.cpu().numpy(), ma.cpu().numpy())
+    check_against_oracle(*c8, Fb.cpu().numpy(), mb.cpu().numpy())
+    a.close(); b.close()
