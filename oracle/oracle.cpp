@@ -142,50 +142,61 @@ int64_t dinic(Graph& g) {
 }
 
 // ---------------------------------------------------------------- Boykov-Kolmogorov
-// Trees: tree[v] = 0 free, 1 source tree S, 2 sink tree T.  parent[v] = arc from the
-// parent to v in S (residual > 0), arc from v to the parent in T (residual > 0).  The
-// roots s and t carry parent = ROOT.  Adoption uses the published timestamp/distance
-// rule to test whether a candidate parent is still connected to its root.
+// As published (Boykov & Kolmogorov, PAMI 2004): terminal arcs are not scanned as
+// adjacency -- every pixel starts as a child of s or t through its t-link (after pushing
+// min(c(s,v), c(v,t)) straight s -> v -> t), then search trees S and T grow along
+// n-links, an S-T meeting arc gives an augmenting path, saturated tree arcs create
+// orphans, and orphans are re-adopted (timestamp/distance validity test) or freed.
+// tree[v]: 0 free, 1 S, 2 T.  parent[v]: TERM (child of its terminal), NONE, or the
+// n-link arc from the parent to v (S) / from v to the parent (T).
+// Build order of build(): arcs 4v, 4v+1 = (s->v, v->s); 4v+2, 4v+3 = (v->t, t->v).
 int64_t boykov_kolmogorov(Graph& g) {
-  const int n = g.n;
-  const int NONE = -1, ROOT = -2;
-  std::vector<int> tree(n, 0), parent(n, NONE), ts(n, 0), dist(n, 0);
-  std::vector<char> in_active(n, 0);
+  const int N = g.n - 2;
+  const int NONE = -1, TERM = -2;
+  std::vector<int> tree(N, 0), parent(N, NONE), ts(N, 0), dist(N, 0);
+  std::vector<char> in_active(N, 0);
   std::vector<int> active;  // FIFO with head index
   size_t ahead = 0;
   std::vector<int> orphans;
   int64_t flow = 0;
   int TIME = 0;
-  tree[g.s] = 1; parent[g.s] = ROOT;
-  tree[g.t] = 2; parent[g.t] = ROOT;
-  active.push_back(g.s); in_active[g.s] = 1;
-  active.push_back(g.t); in_active[g.t] = 1;
+  auto aS = [](int v) { return 4 * v; };      // s -> v
+  auto aT = [](int v) { return 4 * v + 2; };  // v -> t
+  auto push_arc = [&](int a, int64_t d) { g.res[a] -= d; g.res[a ^ 1] += d; };
 
-  auto pnode = [&](int v) -> int {  // parent vertex of a tree vertex
+  for (int v = 0; v < N; ++v) {
+    int64_t d = std::min(g.res[aS(v)], g.res[aT(v)]);
+    if (d > 0) { push_arc(aS(v), d); push_arc(aT(v), d); flow += d; }
+    if (g.res[aS(v)] > 0) tree[v] = 1;
+    else if (g.res[aT(v)] > 0) tree[v] = 2;
+    if (tree[v]) { parent[v] = TERM; dist[v] = 1; active.push_back(v); in_active[v] = 1; }
+  }
+  auto pnode = [&](int v) -> int {  // parent pixel of a non-root tree pixel
     int a = parent[v];
     return tree[v] == 1 ? g.tail(a) : g.head[a];
   };
+  auto is_term = [&](int v) { return v >= N; };
 
   for (;;) {
-    // ---- growth: find an arc connecting S and T
-    int meet = -1;  // arc p -> q with p in S, q in T, residual > 0
+    // ---- growth
+    int meet = -1;  // n-link arc p -> q with p in S, q in T, residual > 0
     while (ahead < active.size() && meet < 0) {
       int p = active[ahead];
       if (tree[p] == 0) { ++ahead; in_active[p] = 0; continue; }
       int tr = tree[p];
       for (int a = g.first[p]; a != -1; a = g.next[a]) {
-        // S grows along p -> q with res(p->q) > 0; T grows along q -> p with res(q->p) > 0
         int q = g.head[a];
+        if (is_term(q)) continue;
         int64_t c = (tr == 1) ? g.res[a] : g.res[a ^ 1];
         if (c <= 0) continue;
         if (tree[q] == 0) {
           tree[q] = tr;
-          parent[q] = (tr == 1) ? a : (a ^ 1);  // S: arc p->q ; T: arc q->p
+          parent[q] = (tr == 1) ? a : (a ^ 1);
           ts[q] = ts[p];
           dist[q] = dist[p] + 1;
           if (!in_active[q]) { active.push_back(q); in_active[q] = 1; }
         } else if (tree[q] != tr) {
-          meet = (tr == 1) ? a : (a ^ 1);  // orient from the S side to the T side
+          meet = (tr == 1) ? a : (a ^ 1);
           break;
         }
       }
@@ -193,70 +204,74 @@ int64_t boykov_kolmogorov(Graph& g) {
     }
     if (meet < 0) break;
 
-    // ---- augmentation along s ~> p -> q ~> t by the bottleneck residual
+    // ---- augmentation along s -> ... -> p -> q -> ... -> t
     ++TIME;
     int p = g.tail(meet), q = g.head[meet];
     int64_t d = g.res[meet];
-    for (int u = p; parent[u] != ROOT; u = g.tail(parent[u])) d = std::min(d, g.res[parent[u]]);
-    for (int u = q; parent[u] != ROOT; u = g.head[parent[u]]) d = std::min(d, g.res[parent[u]]);
-    g.res[meet] -= d; g.res[meet ^ 1] += d;
-    for (int u = p; parent[u] != ROOT;) {
+    int u;
+    for (u = p; parent[u] != TERM; u = g.tail(parent[u])) d = std::min(d, g.res[parent[u]]);
+    d = std::min(d, g.res[aS(u)]);
+    for (u = q; parent[u] != TERM; u = g.head[parent[u]]) d = std::min(d, g.res[parent[u]]);
+    d = std::min(d, g.res[aT(u)]);
+    push_arc(meet, d);
+    for (u = p; parent[u] != TERM;) {
       int a = parent[u];
-      g.res[a] -= d; g.res[a ^ 1] += d;
+      push_arc(a, d);
       int pu = g.tail(a);
       if (g.res[a] == 0) { parent[u] = NONE; orphans.push_back(u); }
       u = pu;
     }
-    for (int u = q; parent[u] != ROOT;) {
+    push_arc(aS(u), d);
+    if (g.res[aS(u)] == 0) { parent[u] = NONE; orphans.push_back(u); }
+    for (u = q; parent[u] != TERM;) {
       int a = parent[u];
-      g.res[a] -= d; g.res[a ^ 1] += d;
+      push_arc(a, d);
       int pu = g.head[a];
       if (g.res[a] == 0) { parent[u] = NONE; orphans.push_back(u); }
       u = pu;
     }
+    push_arc(aT(u), d);
+    if (g.res[aT(u)] == 0) { parent[u] = NONE; orphans.push_back(u); }
     flow += d;
 
     // ---- adoption
     while (!orphans.empty()) {
       int o = orphans.back(); orphans.pop_back();
       int tr = tree[o];
+      if ((tr == 1 && g.res[aS(o)] > 0) || (tr == 2 && g.res[aT(o)] > 0)) {
+        parent[o] = TERM; ts[o] = TIME; dist[o] = 1;
+        continue;
+      }
       int best = NONE, dmin = INT32_MAX;
       for (int a = g.first[o]; a != -1; a = g.next[a]) {
-        int u = g.head[a];
-        if (tree[u] != tr) continue;
-        // candidate parent u: S needs res(u->o) > 0 (arc a^1); T needs res(o->u) > 0 (arc a)
-        int pa = (tr == 1) ? (a ^ 1) : a;
+        int v = g.head[a];
+        if (is_term(v) || tree[v] != tr) continue;
+        int pa = (tr == 1) ? (a ^ 1) : a;  // S: arc v -> o ; T: arc o -> v
         if (g.res[pa] <= 0) continue;
-        // is u connected to its root?  walk up until a root or a node already
-        // verified in this stage (ts == TIME)
-        int dd = 0, j = u;
+        int dd = 0, j = v;
         bool ok;
         for (;;) {
           if (ts[j] == TIME) { dd += dist[j]; ok = true; break; }
-          if (parent[j] == ROOT) { ts[j] = TIME; dist[j] = 0; ok = true; break; }
           if (parent[j] == NONE) { ok = false; break; }
           ++dd;
+          if (parent[j] == TERM) { ts[j] = TIME; dist[j] = 1; ok = true; break; }
           j = pnode(j);
         }
         if (!ok) continue;
         if (dd < dmin) { dmin = dd; best = pa; }
-        for (j = u; ts[j] != TIME; j = pnode(j)) { ts[j] = TIME; dist[j] = dd--; }
+        for (j = v; ts[j] != TIME; j = pnode(j)) { ts[j] = TIME; dist[j] = dd--; }
       }
       if (best != NONE) {
-        parent[o] = best;
-        ts[o] = TIME;
-        dist[o] = dmin + 1;
+        parent[o] = best; ts[o] = TIME; dist[o] = dmin + 1;
         continue;
       }
-      // no valid parent: o becomes free; its children become orphans; same-tree
-      // neighbours that could re-grow into o become active
       for (int a = g.first[o]; a != -1; a = g.next[a]) {
-        int u = g.head[a];
-        if (tree[u] != tr) continue;
+        int v = g.head[a];
+        if (is_term(v) || tree[v] != tr) continue;
         int pa = (tr == 1) ? (a ^ 1) : a;
-        if (g.res[pa] > 0 && !in_active[u]) { active.push_back(u); in_active[u] = 1; }
-        int child_arc = (tr == 1) ? a : (a ^ 1);  // S: o->u ; T: u->o
-        if (parent[u] == child_arc) { parent[u] = NONE; orphans.push_back(u); }
+        if (g.res[pa] > 0 && !in_active[v]) { active.push_back(v); in_active[v] = 1; }
+        int child_arc = (tr == 1) ? a : (a ^ 1);  // S: o -> v ; T: v -> o
+        if (parent[v] == child_arc) { parent[v] = NONE; orphans.push_back(v); }
       }
       tree[o] = 0;
       parent[o] = NONE;
