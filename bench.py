@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py -- batched exact grid min-cut (hot path of arXiv 1008.0502 §4/§7.3) on B200.
+
+One "step" = one pass of the whole hot path (init, global relabels, push launches,
+closure, flow value) over one batch of synthetic frames resident in HBM, through the
+C ABI (gc_solve_batch).  Default workload: C4 of BASELINE.json -- 1920x1080 8-neighbour
+saliency-blob frames, 1024 frames per GPU, frames sharded across ranks (weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+Rank 0 prints ONE JSON line.  The reference arm (--impl reference) is the CPU oracle
+(Boykov-Kolmogorov, oracle/) on the host cores, as the tier framing prescribes.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mpixel/s and frames/s min-cut solve (VGA, 1080p) at 1/2/4/8 B200; % HBM peak"
+CONFIGS = {
+    "c1": dict(workload="C1 64x48 blob, 4-nbr", kind="blob", H=48, W=64, K=4, frames=1, seed_off=0),
+    "c2": dict(workload="C2 320x240 QVGA blob clip, 4-nbr, 300 frames", kind="blob", H=240, W=320, K=4,
+               frames=300, seed_off=1),
+    "c3": dict(workload="C3 640x480 VGA blob sequences, 4-nbr", kind="blob", H=480, W=640, K=4, frames=120,
+               seed_off=2),
+    "c4": dict(workload="C4 1920x1080 blob batch, 8-nbr, 1024 frames per GPU", kind="blob", H=1080, W=1920, K=8,
+               frames=1024, seed_off=3),
+    "c5": dict(workload="C5 3840x2160 serpentine adversarial, 4-nbr", kind="serpentine", H=2160, W=3840, K=4,
+               frames=8, seed_off=4),
+}
+# algorithmic bytes per processed 32x32 tile and kernel class
+
+
+def tile_bytes(cls: str, K: int) -> int:
+    px = 1024
+    if cls == "push":      # read + write e, h, r[K]
+        return 2 * 4 * (2 + K) * px
+    if cls == "bfs":       # read e, h, r[K]; write h
+        return (4 * (2 + K) + 4) * px
+    if cls == "init":      # read cs, ct, c[K]; write e, r[K]
+        return (4 * (2 + K) + 4 * (1 + K)) * px
+    if cls == "closure":   # read e, r[K] (seed) ; write m, open
+        return (4 * (1 + K) + 2) * px
+    if cls == "finalize":  # read e, m; write mask
+        return (4 + 1 + 1) * px
+    return 0
+
+
+def compulsory_bytes_per_px(K: int, warm: bool = False) -> int:
+    """read cs, ct, K n-links, write the mask (+ warm flows in/out)."""
+    b = 4 * (2 + K) + 1
+    if warm:
+        b += 2 * 4 * (K // 2)
+    return b
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_id: str | None):
+        self.proc = None
+        self.path = None
+        self.dev_id = dev_id
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+            os.close(fd)
+            cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"]
+            if self.dev_id:
+                cmd += ["-i", self.dev_id]
+            self.proc = subprocess.Popen(cmd, stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9 and f[1].isdigit():
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [int(r[1]) for r in rows]
+        mx = max(int(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": int(statistics.median(loaded)), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_sample(cfg, n_frames: int, threads: int, seed: int):
+    """Bounded sample of the workload solved by the CPU oracle (BK) on `threads` host threads."""
+    import oracle  # test infrastructure: only the cpu_baseline / reference legs use it
+    import synth
+    cs, ct, nb = synth.gen_host(cfg["kind"], seed, 0, n_frames, cfg["H"], cfg["W"], cfg["K"])
+    t0 = time.perf_counter()
+    F, m = oracle.solve_batch(cs, ct, nb, "bk", threads=threads)
+    dt = time.perf_counter() - t0
+    return dt, F
+
+
+def cpu_baseline(cfg, seed: int):
+    cores = host_cores()
+    n = max(8, min(cores, 24))
+    threads = min(cores, n)
+    dt, _ = oracle_sample(cfg, n, threads, seed)
+    px = n * cfg["H"] * cfg["W"]
+    return {"value": round(px / dt / 1e6, 3), "unit": "Mpixel/s", "cores": threads, "kind": "oracle",
+            "sample": f"{n} frames of {cfg['workload'].split(',')[0]} solved by the CPU oracle "
+                      f"(Boykov-Kolmogorov, oracle/oracle.cpp), one frame per thread, {cpu_model()}",
+            "seconds": round(dt, 3), "fps": round(n / dt, 3)}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the CPU oracle as it stands, on the host cores (tier framing ④)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    cores = host_cores()
+    n = max(8, min(cores, 24))
+    threads = min(cores, n)
+    seed = synth.BASE_SEED + cfg["seed_off"]
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, _ = oracle_sample(cfg, n, threads, seed)
+        if i >= args.warmup:
+            times.append(dt)
+    px = n * cfg["H"] * cfg["W"]
+    tot = sum(times)
+    val = px * len(times) / tot / 1e6
+    out = {"metric": METRIC, "value": round(val, 3), "unit": "Mpixel/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic", "impl": "reference",
+           "config": {"workload": cfg["workload"], "H": cfg["H"], "W": cfg["W"], "K": cfg["K"],
+                      "frames_per_step": n, "note": "bounded sample per step (CPU oracle)"},
+           "fps": round(n * len(times) / tot, 3),
+           "cpu_baseline": {"value": round(val, 3), "unit": "Mpixel/s", "cores": threads, "kind": "oracle",
+                            "sample": f"{n} frames per step, Boykov-Kolmogorov, one frame per thread, {cpu_model()}"},
+           "e2e": {"value": round(val, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-frames", type=int, default=32)
+    ap.add_argument("--profile-steps", type=int, default=1)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.frames:
+        cfg["frames"] = args.frames
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1008_0502_b200 as gc
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    H, W, K, n = cfg["H"], cfg["W"], cfg["K"], cfg["frames"]
+    seed = synth.BASE_SEED + cfg["seed_off"]
+    if cfg["kind"] == "serpentine":
+        synth.set_serpentine_params(lane=64, big=1 << 20)
+
+    # ---- inputs: this rank's frame shard, generated on the device (CUDA twin of synth/)
+    t_first = rank * n
+    cs, ct, nb = synth.gen_torch(cfg["kind"], seed, t_first, n, H, W, K, device=dev)
+    flow = torch.empty(n, dtype=torch.int64, device=dev)
+    mask = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    g = gc.GridCut(neighborhood=K, max_h=H, max_w=W)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        g.solve(cs, ct, nb, out=(flow, mask))
+        return g.launches()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    uuid = None
+    try:
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        pass
+    clk = ClockSampler(uuid)
+    clk.start()
+    time.sleep(0.4)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        launches += step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    px_total = world * n * H * W * args.steps
+    value = px_total / (ms_max * 1e-3) / 1e6
+    fps = world * n * args.steps / (ms_max * 1e-3)
+
+    # ---- final statistics over NCCL (the only collective: SURVEY.md §8(a) a6)
+    pop = mask.view(n, -1).sum(dim=1, dtype=torch.int64)
+    stats = torch.stack([flow.sum(), pop.sum(), (flow < 0).sum().to(torch.int64)])
+    per_frame = torch.stack([flow, pop], dim=1)
+    if world > 1:
+        dist.all_reduce(stats)
+        gathered = [torch.empty_like(per_frame) for _ in range(world)]
+        dist.all_gather(gathered, per_frame)
+        per_frame = torch.cat(gathered)
+    bad_frames = int(stats[2].item())
+
+    # ---- profiled replica steps: per-kernel-class device time and tiles processed
+    g.set_profiling(True)
+    g.profile(reset=True)
+    for _ in range(args.profile_steps):
+        g.solve(cs, ct, nb, out=(flow, mask))
+    torch.cuda.synchronize()
+    prof = g.profile(reset=True)
+    g.set_profiling(False)
+    peak, peak_src = load_peak()
+    dom = max(prof, key=lambda c: prof[c][1])
+    nl, pms, ptiles = prof[dom]
+    avg_ms = pms / max(nl, 1)
+    bytes_launch = tile_bytes(dom, K) * ptiles / max(nl, 1)
+    achieved = bytes_launch / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    tot_prof_ms = sum(v[1] for v in prof.values())
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": f"k_{dom}",
+                "bytes_per_launch": int(bytes_launch), "avg_launch_ms": round(avg_ms, 5),
+                "tiles_per_launch": round(ptiles / max(nl, 1), 1), "share_of_step": round(pms / tot_prof_ms, 3),
+                "peak_source": peak_src,
+                "classes": {c: {"launches": v[0], "ms": round(v[1], 3), "tiles": v[2]} for c, v in prof.items()}}
+    comp = compulsory_bytes_per_px(K) * n * H * W * world * args.steps / (ms_max * 1e-3) / 1e9
+
+    # ---- end to end through the public API with HOST buffers (pinned), copies inside timing
+    e2e = None
+    if not args.no_e2e:
+        ne = min(args.e2e_frames, n)
+        hcs = torch.empty((ne, H, W), dtype=torch.int32, pin_memory=True)
+        hct = torch.empty((ne, H, W), dtype=torch.int32, pin_memory=True)
+        hnb = torch.empty((ne, K, H, W), dtype=torch.int32, pin_memory=True)
+        hcs.copy_(cs[:ne]); hct.copy_(ct[:ne]); hnb.copy_(nb[:ne])
+        hflow = torch.empty(ne, dtype=torch.int64, pin_memory=True)
+        hmask = torch.empty((ne, H, W), dtype=torch.uint8, pin_memory=True)
+        hargs = (hcs.numpy(), hct.numpy(), hnb.numpy())
+        hout = (hflow.numpy(), hmask.numpy())
+        g.solve_host(*hargs, out=hout, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        for _ in range(args.steps):
+            g.solve_host(*hargs, out=hout, stream=stream.cuda_stream)
+        e3.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e2.elapsed_time(e3)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        ems = float(et.item())
+        e2e = {"value": round(world * ne * H * W * args.steps / (ems * 1e-3) / 1e6, 1), "unit": "Mpixel/s",
+               "h2d_bytes_per_step": int(ne * H * W * 4 * (2 + K)),
+               "d2h_bytes_per_step": int(ne * H * W + ne * 8), "frames_per_step": ne,
+               "fps": round(world * ne * args.steps / (ems * 1e-3), 1),
+               "note": "gc_solve_batch_host on pinned host buffers; H2D caps + D2H mask/flow inside the timed region"}
+        # results through the host path must equal the device path
+        assert np.array_equal(hflow.numpy(), flow[:ne].cpu().numpy())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, seed)
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 1), "unit": "Mpixel/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+               "data": "synthetic (seeded saliency-blob frames, synth/; generated on device before timing)",
+               "config": {"workload": cfg["workload"], "H": H, "W": W, "K": K, "frames_per_rank": n,
+                          "frames_total": n * world, "parallelism": f"frame-sharded dp{world}",
+                          "l2": f"inputs {n * H * W * 4 * (2 + K) / 1e9:.1f} GB per rank >> 126 MB L2 (no flush needed)"},
+               "fps": round(fps, 1),
+               "roofline": roofline,
+               "hbm_frac_compulsory": round(comp / peak, 5),
+               "cpu_baseline": cpu,
+               "e2e": e2e,
+               "gpu_launches": int(launches),
+               "clocks": clocks,
+               "frames_failed": bad_frames,
+               "checksum": {"sum_F": int(stats[0].item()), "sum_mask": int(stats[1].item())},
+               "paper_context": "graph-cut stage 1.47 / 6.65 / 1.41 Mpx/s on a GeForce 9800GT (P:757-762)"}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -108,11 +108,14 @@ const char* gc_last_error(const gc_ctx* ctx);
 long long gc_last_launches(const gc_ctx* ctx);
 
 /* Profiling: when enabled, the library brackets every launch of each kernel class with
- * CUDA events on the launching stream and accumulates device time.  Classes: 0 init,
- * 1 bfs (seed+relax), 2 push, 3 status, 4 closure, 5 finalize.  Off by default. */
+ * CUDA events on the launching stream, accumulates device time, and counts the 32x32
+ * tiles each class actually processed (tiles skipped as inactive are not counted).
+ * Classes: 0 init, 1 bfs (seed+relax), 2 push, 3 status, 4 closure, 5 finalize.
+ * Off by default (the events add host overhead to every launch). */
 void gc_set_profiling(gc_ctx* ctx, int enable);
-/* Fills launches[6] and ms[6] accumulated since the last reset; resets if reset != 0. */
-void gc_get_profile(gc_ctx* ctx, long long* launches, double* ms, int reset);
+/* Fills launches[6], ms[6] and tiles[6] (any may be NULL) accumulated since the last
+ * reset; resets the counters if reset != 0. */
+void gc_get_profile(gc_ctx* ctx, long long* launches, double* ms, long long* tiles, int reset);
 
 #ifdef __cplusplus
 }

@@ -59,7 +59,7 @@ _lib.gc_last_launches.restype = ctypes.c_longlong
 _lib.gc_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.gc_set_profiling.restype = None
 _lib.gc_get_profile.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong),
-                                ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 _lib.gc_get_profile.restype = None
 
 EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
@@ -107,8 +107,9 @@ def gc_set_profiling(ctx, enable: bool) -> None:
 def gc_get_profile(ctx, reset: bool = False):
     n = (ctypes.c_longlong * 6)()
     ms = (ctypes.c_double * 6)()
-    _lib.gc_get_profile(ctx, n, ms, int(bool(reset)))
-    return {c: (int(n[i]), float(ms[i])) for i, c in enumerate(PROFILE_CLASSES)}
+    tl = (ctypes.c_longlong * 6)()
+    _lib.gc_get_profile(ctx, n, ms, tl, int(bool(reset)))
+    return {c: (int(n[i]), float(ms[i]), int(tl[i])) for i, c in enumerate(PROFILE_CLASSES)}
 
 
 def _ptr(x):

@@ -62,7 +62,12 @@ struct Dev {
   unsigned long long* sumneg;  // [nslot]
   int32_t* ring;   // [64] per-sweep "something changed" flags
   int32_t* ctr;    // [8]
+  unsigned long long* ptiles;  // [6] tiles processed per kernel class (profiling only, else NULL)
 };
+
+__device__ __forceinline__ void count_tile(const Dev& d, int cls) {
+  if (d.ptiles && threadIdx.x == 0) atomicAdd(&d.ptiles[cls], 1ULL);
+}
 
 struct IO {
   const int32_t* cs;
@@ -189,6 +194,7 @@ __global__ void __launch_bounds__(NTH) k_init(Dev d, IO io) {
   const int32_t* nb = io.nb + s * plane * K;
   const int32_t* wf = WARM ? io.wf + s * plane * (K / 2) : nullptr;
   const size_t gt = (size_t)s * d.T + tile;
+  count_tile(d, 0);
   int bad = 0;
   long long sct = 0;
 #pragma unroll
@@ -293,6 +299,7 @@ __global__ void __launch_bounds__(NTH) k_bfs_seed(Dev d, int par_in, int sw) {
   const int tile = blockIdx.x, s = blockIdx.y;
   if (tile == 0 && s == 0 && threadIdx.x == 0) d.ring[(sw + 1) & 63] = 0;
   if (d.fdone[s]) return;
+  count_tile(d, 1);
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const size_t gt = (size_t)s * d.T + tile;
   const size_t ns = NS(d);
@@ -364,6 +371,7 @@ __global__ void __launch_bounds__(NTH) k_bfs_relax(Dev d, int sw) {
     if (t == 0) d.bchg[cur * ns + gt] = 0;
     return;
   }
+  count_tile(d, 1);
   __shared__ int hs[HS * HS];
   int e[4], r[4][K], h[4], h0[4];
 #pragma unroll
@@ -408,6 +416,7 @@ __global__ void __launch_bounds__(NTH) k_bfs_relax(Dev d, int sw) {
 __global__ void __launch_bounds__(NTH) k_status(Dev d, int pushes, int relabels, int sweeps) {
   const int s = blockIdx.x, t = threadIdx.x;
   if (d.fdone[s]) return;
+  count_tile(d, 3);
   int any = 0;
   for (int i = t; i < d.T; i += NTH) any |= d.tact[(size_t)s * d.T + i];
   any = __syncthreads_or(any);
@@ -438,6 +447,7 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, int par_in, int par_out, in
   const size_t ns = NS(d);
   const int rcv = (par_in >= 0) ? d.recv[par_in * ns + gt] : 0;
   if (!d.tact[gt] && !rcv) return;
+  count_tile(d, 2);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   __shared__ int hs[HS * HS];
   __shared__ int ps[K][TPX];
@@ -628,6 +638,7 @@ __global__ void __launch_bounds__(NTH) k_closure_seed(Dev d, int sw) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   if (tile == 0 && s == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
   if (d.ferr[s]) return;
+  count_tile(d, 4);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const size_t gt = (size_t)s * d.T + tile;
   __shared__ uint8_t ms[TPX];
@@ -664,6 +675,7 @@ __global__ void __launch_bounds__(NTH) k_closure_relax(Dev d, int sw) {
   const size_t ns = NS(d);
   const int cur = sw & 1, prv = cur ^ 1;
   if (!d.crecv[prv * ns + gt]) return;
+  count_tile(d, 4);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   __shared__ uint8_t ms[TPX];
   __shared__ uint8_t os[TPX];
@@ -713,6 +725,7 @@ __global__ void __launch_bounds__(NTH) k_finalize(Dev d, IO io) {
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const size_t gt = (size_t)s * d.T + tile;
+  count_tile(d, 5);
   const int err = d.ferr[s];
   long long neg = 0;
 #pragma unroll

@@ -29,6 +29,8 @@ struct gc_ctx {
   long long last_launches = 0;
   bool prof = false;
   long long prof_n[6] = {0, 0, 0, 0, 0, 0};
+  long long prof_tiles[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long* dtiles = nullptr;  // device counters [6]
   double prof_ms[6] = {0, 0, 0, 0, 0, 0};
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -90,6 +92,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W) {
   d.sumneg = d.sumct + nslot;
   d.ring = (int32_t*)(d.sumneg + nslot);
   d.ctr = d.ring + 64;
+  d.ptiles = c->prof ? c->dtiles : nullptr;
   return d;
 }
 
@@ -128,6 +131,11 @@ struct Launcher {
 };
 
 void resolve_profile(gc_ctx* c) {
+  unsigned long long t[6];
+  if (cudaMemcpy(t, c->dtiles, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
+    for (int i = 0; i < 6; ++i) c->prof_tiles[i] += (long long)t[i];
+    cudaMemset(c->dtiles, 0, sizeof(t));
+  }
   for (auto& p : c->pending) {
     float ms = 0;
     cudaEventElapsedTime(&ms, p.second.first, p.second.second);
@@ -297,6 +305,8 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   c->pool_bytes = nf * fb;
   if (cudaMalloc(&c->pool, c->pool_bytes) != cudaSuccess) { cudaGetLastError(); delete c; return GC_ERR_OOM; }
   if (cudaMallocHost(&c->hpin, 64) != cudaSuccess) { cudaFree(c->pool); delete c; return GC_ERR_OOM; }
+  if (cudaMalloc(&c->dtiles, 64) != cudaSuccess) { cudaFree(c->pool); cudaFreeHost(c->hpin); delete c; return GC_ERR_OOM; }
+  cudaMemset(c->dtiles, 0, 64);
   *out = c;
   return GC_OK;
 }
@@ -307,6 +317,7 @@ void gc_destroy(gc_ctx* c) {
   if (c->pool) cudaFree(c->pool);
   if (c->stage) cudaFree(c->stage);
   if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->dtiles) cudaFree(c->dtiles);
   delete c;
 }
 
@@ -318,14 +329,15 @@ void gc_set_profiling(gc_ctx* c, int enable) {
   if (c) c->prof = enable != 0;
 }
 
-void gc_get_profile(gc_ctx* c, long long* launches, double* ms, int reset) {
+void gc_get_profile(gc_ctx* c, long long* launches, double* ms, long long* tiles, int reset) {
   if (!c) return;
   for (int i = 0; i < 6; ++i) {
     if (launches) launches[i] = c->prof_n[i];
     if (ms) ms[i] = c->prof_ms[i];
+    if (tiles) tiles[i] = c->prof_tiles[i];
   }
   if (reset)
-    for (int i = 0; i < 6; ++i) { c->prof_n[i] = 0; c->prof_ms[i] = 0; }
+    for (int i = 0; i < 6; ++i) { c->prof_n[i] = 0; c->prof_ms[i] = 0; c->prof_tiles[i] = 0; }
 }
 
 gc_status gc_solve_batch(gc_ctx* c, const gc_batch* b, void* stream) {
