@@ -315,7 +315,7 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": f"k_{dom}",
                 "bytes_per_launch": int(bytes_launch), "avg_launch_ms": round(avg_ms, 5),
-                "tiles_per_launch": round(ptiles / max(nl, 1), 1), "share_of_step": round(pms / tot_prof_ms, 3),
+                "tiles_per_launch": round(ptiles / max(nl, 1), 1), "share_of_step": round(pms / max(tot_prof_ms, 1e-9), 3),
                 "peak_source": peak_src,
                 "classes": {c: {"launches": v[0], "ms": round(v[1], 3), "tiles": v[2]} for c, v in prof.items()}}
     comp = compulsory_bytes_per_px(K) * n * H * W * world * args.steps / (ms_max * 1e-3) / 1e9

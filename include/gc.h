@@ -65,10 +65,10 @@ typedef struct {
   int device;            /* CUDA device ordinal (default: current device)                */
   int neighborhood;      /* 4 or 8 (default 4)                                            */
   int max_h, max_w;      /* largest frame the context will accept (default 1080 x 1920)  */
-  int max_batch;         /* frames solved concurrently per device pass (default: sized to
-                            keep the working set inside L2, at least 1)                  */
-  int rounds_per_launch; /* push/relabel rounds inside a tile per launch (default 16)    */
-  int relabel_period;    /* push launches between global relabels (default 4)            */
+  int max_batch;         /* frames solved concurrently per device pass (default: as many
+                            as a scratch budget of min(8 GB, 1/16 device memory) holds) */
+  int rounds_per_launch; /* push/relabel rounds inside a tile per launch (default 8)     */
+  int relabel_period;    /* push launches between global relabels (default 2)            */
   long long max_launches;/* per chunk; exceeded -> GC_ERR_NOCONV (default 1,000,000)     */
 } gc_config;
 

@@ -529,12 +529,14 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, int par_in, int par_out, in
       }
     }
     __syncthreads();
+    int still = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       h[j] = hn[j];
       hs[hidx(iy0 + 8 * j, ix)] = hn[j];
+      still |= (e[j] > 0) & (hn[j] < HINF);
     }
-    __syncthreads();
+    if (!__syncthreads_or(still)) break;  // tile discharged: nothing left to push
   }
   // store state
   int act = 0;

@@ -20,7 +20,7 @@
 using namespace gcb;
 
 struct gc_ctx {
-  int dev = 0, K = 4, max_h = 0, max_w = 0, max_batch = 0, rounds = 16, period = 4;
+  int dev = 0, K = 4, max_h = 0, max_w = 0, max_batch = 0, rounds = 8, period = 2;
   long long max_launches = 1000000;
   size_t pool_bytes = 0;
   char* pool = nullptr;
@@ -284,8 +284,8 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (c->K != 4 && c->K != 8) { delete c; return GC_ERR_ARG; }
   c->max_h = g.max_h > 0 ? g.max_h : 1080;
   c->max_w = g.max_w > 0 ? g.max_w : 1920;
-  c->rounds = g.rounds_per_launch > 0 ? g.rounds_per_launch : 16;
-  c->period = g.relabel_period > 0 ? g.relabel_period : 4;
+  c->rounds = g.rounds_per_launch > 0 ? g.rounds_per_launch : 8;
+  c->period = g.relabel_period > 0 ? g.relabel_period : 2;
   c->max_launches = g.max_launches > 0 ? g.max_launches : 1000000;
   c->max_batch = g.max_batch > 0 ? g.max_batch : 0;
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
@@ -295,10 +295,13 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (c->max_batch > 0) {
     nf = c->max_batch;
   } else {
-    // default: keep one chunk's working set inside L2 (126 MB on B200), at least 1 frame
-    int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->dev);
-    size_t budget = l2 > 0 ? (size_t)l2 * 3 / 4 : ((size_t)96 << 20);
+    // default: enough frames per pass to fill 148 SMs with active tiles (only a small
+    // fraction of a realistic frame's tiles is active after the first global relabel),
+    // bounded by a scratch budget of min(8 GB, 1/16 of device memory)
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    size_t budget = (size_t)8 << 30;
+    if (tot > 0 && tot / 16 < budget) budget = tot / 16;
     nf = budget / fb;
     if (nf < 1) nf = 1;
   }
