@@ -16,7 +16,7 @@ def launches(path):
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("void ", "")
         agg[name][0] += 1
         agg[name][1] += v
