@@ -42,17 +42,18 @@ CONFIGS = {
 
 
 def tile_bytes(cls: str, K: int) -> int:
+    """Algorithmic bytes one kernel class moves per processed 32x32 tile."""
     px = 1024
-    if cls == "push":      # read + write e, h, r[K]
-        return 2 * 4 * (2 + K) * px
-    if cls == "bfs":       # read e, h, r[K]; write h
-        return (4 * (2 + K) + 4) * px
-    if cls == "init":      # read cs, ct, c[K]; write e, r[K]
-        return (4 * (2 + K) + 4 * (1 + K)) * px
-    if cls == "closure":   # read e, r[K] (seed) ; write m, open
-        return (4 * (1 + K) + 2) * px
-    if cls == "finalize":  # read e, m; write mask
-        return (4 + 1 + 1) * px
+    if cls == "push":      # read e, r[K], h; write e, r[K], h, fl
+        return (4 * (2 + K) + 4 * (2 + K) + 2) * px
+    if cls == "bfs":       # read fl, h; write h (relax sweeps; the seed sweep moves less)
+        return (2 + 4 + 4) * px
+    if cls == "init":      # read cs, ct, c[K]; write fl, h
+        return (4 * (2 + K) + 2 + 4) * px
+    if cls == "closure":   # read fl; write m and the caller's mask
+        return (2 + 1 + 1) * px
+    if cls == "export":    # read r[K/2] (or caps) ; write f[K/2]
+        return (4 * (K // 2) * 2) * px
     return 0
 
 

@@ -110,7 +110,8 @@ long long gc_last_launches(const gc_ctx* ctx);
 /* Profiling: when enabled, the library brackets every launch of each kernel class with
  * CUDA events on the launching stream, accumulates device time, and counts the 32x32
  * tiles each class actually processed (tiles skipped as inactive are not counted).
- * Classes: 0 init, 1 bfs (seed+relax), 2 push, 3 status, 4 closure, 5 finalize.
+ * Classes: 0 init (+ first BFS seed), 1 bfs (seed+relax), 2 push, 3 status, 4 closure,
+ * 5 export (flow_state_out).
  * Off by default (the events add host overhead to every launch). */
 void gc_set_profiling(gc_ctx* ctx, int enable);
 /* Fills launches[6], ms[6] and tiles[6] (any may be NULL) accumulated since the last

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libgc.so")
 CAP_MAX = (1 << 26) - 1
 STATUS = {0: "GC_OK", 1: "GC_ERR_ARG", 2: "GC_ERR_RANGE", 3: "GC_ERR_OOM", 4: "GC_ERR_CUDA", 5: "GC_ERR_NOCONV"}
-PROFILE_CLASSES = ("init", "bfs", "push", "status", "closure", "finalize")
+PROFILE_CLASSES = ("init", "bfs", "push", "status", "closure", "export")
 
 if not os.path.exists(lib_path):
     raise ImportError(f"{lib_path} is missing: build it with __graft_entry__.build() (make). "

@@ -7,19 +7,22 @@
 // this is a fresh B200 design, not a translation of it.
 //
 // State (tile-major, 32x32 tiles, frame padded to whole tiles):
-//   e  [slot][tile][1024]     signed net excess: e = cs - ct + inflow - outflow.  e > 0 is
-//                             excess (an "active" node), e < 0 is remaining residual
-//                             capacity v -> t.  The terminal pair is pre-cancelled (a1).
-//   h  [slot][tile][1024]     height / distance label (HINF = unreachable)
-//   r  [slot][k][tile][1024]  residual capacity of arc v -> v + d_k
-//   hedge [slot][tile][4][32] copy of the tile's boundary heights (top,bottom,left,right)
-//   inbox [2][slot][tile][k][64]  flow pushed INTO the tile across its border, by arc
-//                             direction and receiver edge slot; double-buffered by launch
-//                             parity, written by the unique sender, zeroed by the receiver
-//   reach [slot][tile][k][64] sticky min-cut reach bits arriving across the border
-//   m, open [slot][tile][1024] mask bit and residual-arc bits (closure phase)
-// No kernel uses global atomics on the push path; the only atomics are per-tile int64
-// partial sums of the flow value.
+//   fl [slot][tile][1024] u16  bit k: r_k > 0 (arc open), bit 8: e > 0, bit 9: e < 0.
+//                              Everything the BFS and closure phases need (2 B/px).
+//   h  [slot][tile][1024]      height / distance label (HINF = cannot reach the sink)
+//   e  [slot][tile][1024]      signed net excess e = cs - ct + inflow - outflow      } only for
+//   r  [slot][k][tile][1024]   residual capacity of arc v -> v + d_k                 } "materialised"
+//                              tiles (mat = 1): a tile's e, r are computed from the caps
+//                              (+ warm flows) the first time a push touches it, so tiles
+//                              the push phase never visits are never written.
+//   hedge [slot][tile][4][32]  copy of the tile's border heights (top, bottom, left, right)
+//   inbox [2][slot][tile][k][64] flow pushed INTO the tile across its border, by arc direction
+//                              and receiver edge slot; double-buffered by launch parity,
+//                              written by the unique sender, zeroed by the receiver
+//   reach [slot][tile][k][64]  sticky min-cut reach bits arriving across the border
+//   m  [slot][tile][1024] u8   mask bit (closure phase)
+// Sparse phases (BFS relax, push, closure relax) run as persistent grids over a worklist of
+// flagged tiles, compacted per CTA in shared memory.  No global atomics on the push path.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -32,6 +35,8 @@ constexpr int NTH = 256;     // threads per CTA; thread t owns pixels (t/32 + 8j
 constexpr int HINF = 0x3fffffff;
 constexpr int CAPMAX = (1 << 26) - 1;
 constexpr int HS = 34;       // halo'd height tile side
+constexpr int FL_POS = 1 << 8;
+constexpr int FL_NEG = 1 << 9;
 
 __host__ __device__ constexpr int DYk(int k) {
   return (k == 2 || k == 4 || k == 6) ? 1 : ((k == 3 || k == 5 || k == 7) ? -1 : 0);
@@ -46,28 +51,26 @@ struct Dev {
   int32_t* e;
   int32_t* h;
   int32_t* r;
+  uint16_t* fl;
   int32_t* hedge;
   int32_t* inbox;
   uint8_t* reach;
   uint8_t* m;
-  uint8_t* open;
-  int32_t* tact;   // [NS]   tile has an active node (e > 0, h < HINF)
-  int32_t* bchg;   // [2][NS] tile boundary heights changed in the sweep of that parity
-  int32_t* recv;   // [2][NS] tile has inbound flow in inbox of that parity
-  int32_t* crecv;  // [2][NS] tile received new reach bits in the sweep of that parity
-  int32_t* fdone;  // [nslot]
-  int32_t* ferr;   // [nslot]
-  int32_t* fstat;  // [nslot][4]
+  long long* neg0;  // [NS] sum max(0,-e) of the tile as initialised (for never-materialised tiles)
+  int32_t* mat;     // [NS]   e, r of the tile are materialised
+  int32_t* tact;    // [NS]   tile has an active node (e > 0, h < HINF)
+  int32_t* dirty;   // [2][NS] tile must be re-relaxed in the next BFS sweep of that parity
+  int32_t* recv;    // [2][NS] tile has inbound flow in inbox of that parity
+  int32_t* crecv;   // [2][NS] tile received new reach bits in the closure sweep of that parity
+  int32_t* fdone;   // [nslot]
+  int32_t* ferr;    // [nslot]
+  int32_t* fstat;   // [nslot][4]
   unsigned long long* sumct;   // [nslot]
   unsigned long long* sumneg;  // [nslot]
-  int32_t* ring;   // [64] per-sweep "something changed" flags
-  int32_t* ctr;    // [8]
+  int32_t* ring;    // [64] per-sweep "something changed" flags
+  int32_t* ctr;     // [8]
   unsigned long long* ptiles;  // [6] tiles processed per kernel class (profiling only, else NULL)
 };
-
-__device__ __forceinline__ void count_tile(const Dev& d, int cls) {
-  if (d.ptiles && threadIdx.x == 0) atomicAdd(&d.ptiles[cls], 1ULL);
-}
 
 struct IO {
   const int32_t* cs;
@@ -80,11 +83,13 @@ struct IO {
   int32_t* stats;
 };
 
+__device__ __forceinline__ void count_tile(const Dev& d, int cls) {
+  if (d.ptiles && threadIdx.x == 0) atomicAdd(&d.ptiles[cls], 1ULL);
+}
 __device__ __forceinline__ size_t NS(const Dev& d) { return (size_t)d.nslot * d.T; }
-__device__ __forceinline__ int32_t* Ep(const Dev& d, size_t gt) { return d.e + gt * TPX; }
-__device__ __forceinline__ int32_t* Hp(const Dev& d, size_t gt) { return d.h + gt * TPX; }
-__device__ __forceinline__ int32_t* Rp(const Dev& d, int K, int s, int k, int tile) {
-  return d.r + (((size_t)s * K + k) * d.T + tile) * TPX;
+__device__ __forceinline__ int32_t* Rp(const Dev& d, int K, size_t gt, int k) {
+  const size_t s = gt / d.T, tile = gt - s * d.T;
+  return d.r + ((s * K + k) * d.T + tile) * TPX;
 }
 __device__ __forceinline__ int32_t* INBp(const Dev& d, int K, int par, size_t gt, int k) {
   return d.inbox + (((size_t)par * NS(d) + gt) * K + k) * 64;
@@ -92,7 +97,7 @@ __device__ __forceinline__ int32_t* INBp(const Dev& d, int K, int par, size_t gt
 
 // Does arc (iy,ix) -> (iy,ix)+d_k leave the tile?
 __device__ __forceinline__ bool crosses(int k, int iy, int ix) {
-  int y2 = iy + DYk(k), x2 = ix + DXk(k);
+  const int y2 = iy + DYk(k), x2 = ix + DXk(k);
   return (unsigned)y2 >= 32u || (unsigned)x2 >= 32u;
 }
 
@@ -111,13 +116,13 @@ __device__ __forceinline__ int recv_slot(int k, int uy, int ux) {
   }
 }
 
-// halo'd smem index of pixel (iy,ix) (which may be -1..32)
 __device__ __forceinline__ int hidx(int iy, int ix) { return (iy + 1) * HS + (ix + 1); }
+__device__ __forceinline__ bool on_border(int iy, int ix) { return iy == 0 || iy == 31 || ix == 0 || ix == 31; }
 
-// Load the 34x34 halo ring of heights from the neighbours' boundary copies.
+// Load the 34x34 halo ring of heights from the neighbours' border copies (HINF off-frame).
 __device__ __forceinline__ void load_halo(const Dev& d, int s, int ty, int tx, int* hs, int t) {
   if (t < 128) {
-    int side = t >> 5, i = t & 31;
+    const int side = t >> 5, i = t & 31;
     int nty = ty, ntx = tx, esd, pos;
     if (side == 0) { nty = ty - 1; esd = 1; pos = hidx(-1, i); }
     else if (side == 1) { nty = ty + 1; esd = 0; pos = hidx(32, i); }
@@ -128,14 +133,12 @@ __device__ __forceinline__ void load_halo(const Dev& d, int s, int ty, int tx, i
       v = d.hedge[(((size_t)s * d.T + nty * d.TX + ntx) * 4 + esd) * 32 + i];
     hs[pos] = v;
   } else if (t < 132) {
-    int c = t - 128;
-    int dy = (c < 2) ? -1 : 1, dx = (c & 1) ? 1 : -1;
-    int nty = ty + dy, ntx = tx + dx;
-    int esd = dy < 0 ? 1 : 0;
-    int i = dx < 0 ? 31 : 0;
+    const int c = t - 128;
+    const int dy = (c < 2) ? -1 : 1, dx = (c & 1) ? 1 : -1;
+    const int nty = ty + dy, ntx = tx + dx;
     int v = HINF;
     if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
-      v = d.hedge[(((size_t)s * d.T + nty * d.TX + ntx) * 4 + esd) * 32 + i];
+      v = d.hedge[(((size_t)s * d.T + nty * d.TX + ntx) * 4 + (dy < 0 ? 1 : 0)) * 32 + (dx < 0 ? 31 : 0)];
     hs[hidx(dy < 0 ? -1 : 32, dx < 0 ? -1 : 32)] = v;
   }
 }
@@ -152,126 +155,109 @@ __device__ __forceinline__ void store_hedge(const Dev& d, size_t gt, const int (
   }
 }
 
-__device__ __forceinline__ bool on_border(int iy, int ix) { return iy == 0 || iy == 31 || ix == 0 || ix == 31; }
-
-// Tile-local BFS fixpoint: h(v) = min(h(v), 1 + min{h(v+d_k) : r_k(v) > 0}) until stable.
-// hs holds the halo'd heights (halo fixed); updates are written in place (monotone, so
-// a racing reader sees an old or a new upper bound -- both valid).
 template <int K>
-__device__ __forceinline__ void bfs_fixpoint(volatile int* hs, const int (&r)[4][K], int (&h)[4], int t) {
-  const int ix = t & 31, iy0 = t >> 5;
-  for (;;) {
-    int changed = 0;
+__device__ __forceinline__ int make_fl(int e, const int (&r)[K]) {
+  int f = (e > 0 ? FL_POS : 0) | (e < 0 ? FL_NEG : 0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int iy = iy0 + 8 * j;
-      if (h[j] > 1) {
-        int mn = HINF;
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-          if (r[j][k] > 0) mn = min(mn, hs[hidx(iy + DYk(k), ix + DXk(k))]);
-        if (mn < HINF && mn + 1 < h[j]) {
-          h[j] = mn + 1;
-          hs[hidx(iy, ix)] = h[j];
-          changed = 1;
-        }
-      }
-    }
-    if (!__syncthreads_or(changed)) break;
-  }
+  for (int k = 0; k < K; ++k) f |= (r[k] > 0) << k;
+  return f;
 }
 
-// ------------------------------------------------------------------------------ a1 / a1w
-template <int K, bool WARM>
-__global__ void __launch_bounds__(NTH) k_init(Dev d, IO io) {
-  const int tile = blockIdx.x, s = blockIdx.y;
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+// a1 / a1w: the tile's initial e and r from the caps (and the clamped warm flows).
+// e = cs - ct pre-cancels min(cs,ct) along s -> v -> t; arcs pointing off the grid get
+// r = 0 whatever the caller stored there (reading c7).
+template <int K>
+__device__ __forceinline__ void tile_from_caps(const Dev& d, const IO& io, int s, int ty, int tx, int (&e)[4],
+                                               int (&r)[4][K], int& bad, long long& sct) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const int32_t* cs = io.cs + s * plane;
   const int32_t* ct = io.ct + s * plane;
   const int32_t* nb = io.nb + s * plane * K;
-  const int32_t* wf = WARM ? io.wf + s * plane * (K / 2) : nullptr;
-  const size_t gt = (size_t)s * d.T + tile;
-  count_tile(d, 0);
-  int bad = 0;
-  long long sct = 0;
+  const int32_t* wf = io.wf ? io.wf + s * plane * (K / 2) : nullptr;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j, y = ty * TS + iy, x = tx * TS + ix, lp = iy * TS + ix;
+    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
     int ev = 0;
-    int rk[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) rk[k] = 0;
+    for (int k = 0; k < K; ++k) r[j][k] = 0;
     if (y < H && x < W) {
       const size_t o = (size_t)y * W + x;
-      const int a = cs[o], b = ct[o];
+      const int a = __ldg(cs + o), b = __ldg(ct + o);
       bad |= (a < 0) | (a > CAPMAX) | (b < 0) | (b > CAPMAX);
-      ev = a - b;  // a1: pre-cancel min(cs,ct) straight s -> v -> t
+      ev = a - b;
       sct += b;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int y2 = y + DYk(k), x2 = x + DXk(k);
-        if (y2 < 0 || y2 >= H || x2 < 0 || x2 >= W) continue;  // off-grid: ignored
-        const int c = nb[k * plane + o];
+        if (y2 < 0 || y2 >= H || x2 < 0 || x2 >= W) continue;
+        const int c = __ldg(nb + k * plane + o);
         bad |= (c < 0) | (c > CAPMAX);
-        if (!WARM) {
-          rk[k] = c;
+        if (!wf) {
+          r[j][k] = c;
         } else {
           const size_t oq = (size_t)y2 * W + x2;
-          if ((k & 1) == 0) {  // forward arc p -> q, flow stored at p
-            const int cq = nb[(k ^ 1) * plane + oq];
-            int f = wf[(k >> 1) * plane + o];
-            f = max(-cq, min(c, f));  // a1w: clamp to the new capacities
-            rk[k] = c - f;
+          const int cq = __ldg(nb + (k ^ 1) * plane + oq);
+          if ((k & 1) == 0) {  // forward arc p -> q; its flow is stored at p
+            const int f = max(-cq, min(c, __ldg(wf + (k >> 1) * plane + o)));  // a1w clamp
+            r[j][k] = c - f;
             ev -= f;
-          } else {  // reverse arc p -> q of the forward arc q -> p, flow stored at q
-            const int cq = nb[(k ^ 1) * plane + oq];
-            int f = wf[((k ^ 1) >> 1) * plane + oq];
-            f = max(-c, min(cq, f));
-            rk[k] = c + f;
+          } else {  // reverse arc of the forward arc q -> p; its flow is stored at q
+            const int f = max(-c, min(cq, __ldg(wf + ((k ^ 1) >> 1) * plane + oq)));
+            r[j][k] = c + f;
             ev += f;
           }
         }
       }
     }
-    Ep(d, gt)[lp] = ev;
+    e[j] = ev;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void load_er(const Dev& d, size_t gt, int (&e)[4], int (&r)[4][K]) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
 #pragma unroll
-    for (int k = 0; k < K; ++k) Rp(d, K, s, k, tile)[lp] = rk[k];
-  }
-  // clear the tile's message buffers and flags
-  for (int i = t; i < 2 * K * 64; i += NTH) {
-    const int par = i / (K * 64), rest = i - par * K * 64;
-    INBp(d, K, par, gt, 0)[rest] = 0;
-  }
-  for (int i = t; i < K * 64; i += NTH) d.reach[gt * K * 64 + i] = 0;
-  if (t == 0) {
-    const size_t ns = NS(d);
-    d.tact[gt] = 0;
-    d.bchg[gt] = 0; d.bchg[ns + gt] = 0;
-    d.recv[gt] = 0; d.recv[ns + gt] = 0;
-    d.crecv[gt] = 0; d.crecv[ns + gt] = 0;
-  }
-  // frame reductions: sum of c(v,t) (for F) and the range flag
-  bad = __syncthreads_or(bad);
-  __shared__ long long red[NTH / 32];
+  for (int j = 0; j < 4; ++j) {
+    const int lp = (iy0 + 8 * j) * TS + ix;
+    e[j] = d.e[gt * TPX + lp];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sct += __shfl_xor_sync(0xffffffffu, sct, o);
-  if ((t & 31) == 0) red[t >> 5] = sct;
-  __syncthreads();
-  if (t == 0) {
-    long long tot = 0;
-    for (int i = 0; i < NTH / 32; ++i) tot += red[i];
-    if (tot) atomicAdd(&d.sumct[s], (unsigned long long)tot);
-    if (bad) { d.ferr[s] = 1; d.fdone[s] = 1; }
+    for (int k = 0; k < K; ++k) r[j][k] = Rp(d, K, gt, k)[lp];
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void store_er(const Dev& d, size_t gt, const int (&e)[4], const int (&r)[4][K]) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int lp = (iy0 + 8 * j) * TS + ix;
+    d.e[gt * TPX + lp] = e[j];
+#pragma unroll
+    for (int k = 0; k < K; ++k) Rp(d, K, gt, k)[lp] = r[j][k];
+    d.fl[gt * TPX + lp] = (uint16_t)make_fl<K>(e[j], r[j]);
+  }
+}
+
+// e, r of a tile: from the materialised state, else recomputed from the caps.
+template <int K>
+__device__ __forceinline__ void get_er(const Dev& d, const IO& io, size_t gt, int (&e)[4], int (&r)[4][K]) {
+  if (d.mat[gt]) {
+    load_er<K>(d, gt, e, r);
+  } else {
+    const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+    const int ty = tile / d.TX, tx = tile - ty * d.TX;
+    int bad = 0;
+    long long sct = 0;
+    tile_from_caps<K>(d, io, s, ty, tx, e, r, bad, sct);
   }
 }
 
 // Absorb the flow pushed into this tile in the previous launch (inbox parity `par`).
 template <int K>
-__device__ __forceinline__ void absorb(const Dev& d, int par, size_t gt, int (&e)[4], int (&r)[4][K], int t) {
-  const int ix = t & 31, iy0 = t >> 5;
+__device__ __forceinline__ void absorb(const Dev& d, int par, size_t gt, int (&e)[4], int (&r)[4][K]) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j;
@@ -291,128 +277,248 @@ __device__ __forceinline__ void absorb(const Dev& d, int par, size_t gt, int (&e
   }
 }
 
-// ------------------------------------------------------------------------------ a2 seed
-// Global relabel, sweep 0: absorb in-flight flow, seed h = 1 on nodes with residual to t
-// (e < 0), HINF elsewhere, and relax to the tile-local fixpoint with an INF halo.
+// Tile-local BFS fixpoint: h(v) = min(h(v), 1 + min{h(v+d_k) : arc k open}) until stable.
+// hs holds the halo'd heights (halo fixed); updates are written in place (monotone, so a
+// racing reader sees an old or a new upper bound -- both valid).
 template <int K>
-__global__ void __launch_bounds__(NTH) k_bfs_seed(Dev d, int par_in, int sw) {
-  const int tile = blockIdx.x, s = blockIdx.y;
-  if (tile == 0 && s == 0 && threadIdx.x == 0) d.ring[(sw + 1) & 63] = 0;
-  if (d.fdone[s]) return;
-  count_tile(d, 1);
+__device__ __forceinline__ void bfs_fixpoint(volatile int* hs, const int (&fl)[4], int (&h)[4]) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const size_t gt = (size_t)s * d.T + tile;
-  const size_t ns = NS(d);
-  __shared__ int hs[HS * HS];
-  int e[4], r[4][K], h[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int lp = (iy0 + 8 * j) * TS + ix;
-    e[j] = Ep(d, gt)[lp];
-#pragma unroll
-    for (int k = 0; k < K; ++k) r[j][k] = Rp(d, K, s, k, tile)[lp];
-  }
-  const int rcv = (par_in >= 0) ? d.recv[par_in * ns + gt] : 0;
-  if (rcv) {
-    absorb<K>(d, par_in, gt, e, r, t);
+  for (;;) {
+    int changed = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int lp = (iy0 + 8 * j) * TS + ix;
-      Ep(d, gt)[lp] = e[j];
+      const int iy = iy0 + 8 * j;
+      if (h[j] > 1) {
+        int mn = HINF;
 #pragma unroll
-      for (int k = 0; k < K; ++k) Rp(d, K, s, k, tile)[lp] = r[j][k];
+        for (int k = 0; k < K; ++k)
+          if ((fl[j] >> k) & 1) mn = min(mn, hs[hidx(iy + DYk(k), ix + DXk(k))]);
+        if (mn < HINF && mn + 1 < h[j]) {
+          h[j] = mn + 1;
+          hs[hidx(iy, ix)] = h[j];
+          changed = 1;
+        }
+      }
     }
-    if (t == 0) d.recv[par_in * ns + gt] = 0;
-  }
-  for (int i = t; i < HS * HS; i += NTH) hs[i] = HINF;
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    h[j] = e[j] < 0 ? 1 : HINF;
-    hs[hidx(iy0 + 8 * j, ix)] = h[j];
-  }
-  __syncthreads();
-  bfs_fixpoint<K>(hs, r, h, t);
-  int act = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    Hp(d, gt)[(iy0 + 8 * j) * TS + ix] = h[j];
-    act |= (e[j] > 0) & (h[j] < HINF);
-  }
-  store_hedge(d, gt, h, t);
-  act = __syncthreads_or(act);
-  if (t == 0) {
-    d.tact[gt] = act;
-    d.bchg[(sw & 1) * ns + gt] = 1;
+    if (!__syncthreads_or(changed)) break;
   }
 }
 
-// ------------------------------------------------------------------------------ a2 relax
-// Global relabel, sweep sw >= 1: re-relax tiles whose neighbours' boundary heights changed
-// in the previous sweep, until no boundary changes anywhere (exact BFS distances).
+// Seed heights from fl (h = 1 where the node still has residual capacity to t) and relax to
+// the tile-local fixpoint with an INF halo; stores h, hedge; returns "tile has an active node".
 template <int K>
-__global__ void __launch_bounds__(NTH) k_bfs_relax(Dev d, int sw) {
+__device__ __forceinline__ int bfs_seed_tile(const Dev& d, size_t gt, int* hs, const int (&fl)[4]) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  for (int i = t; i < HS * HS; i += NTH) hs[i] = HINF;
+  __syncthreads();
+  int h[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    h[j] = (fl[j] & FL_NEG) ? 1 : HINF;
+    hs[hidx(iy0 + 8 * j, ix)] = h[j];
+  }
+  __syncthreads();
+  bfs_fixpoint<K>(hs, fl, h);
+  int act = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
+    act |= (fl[j] & FL_POS) && h[j] < HINF;
+  }
+  store_hedge(d, gt, h, t);
+  return __syncthreads_or(act);
+}
+
+// ------------------------------------------------------------------------------ a1 + a2 seed
+// Init fused with the first global-relabel seed sweep: computes e, r in registers (not
+// stored: the tile stays un-materialised), writes fl, h, the frame's sum c(v,t), the
+// tile's sum max(0,-e), and the range flag.
+template <int K>
+__global__ void __launch_bounds__(NTH) k_init(Dev d, IO io) {
+  const int tile = blockIdx.x, s = blockIdx.y;
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  const size_t gt = (size_t)s * d.T + tile;
+  const size_t ns = NS(d);
+  count_tile(d, 0);
+  __shared__ int hs[HS * HS];
+  __shared__ long long red[2][NTH / 32];
+  int e[4], r[4][K], fl[4];
+  int bad = 0;
+  long long sct = 0, neg = 0;
+  tile_from_caps<K>(d, io, s, ty, tx, e, r, bad, sct);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    fl[j] = make_fl<K>(e[j], r[j]);
+    d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix] = (uint16_t)fl[j];
+    neg += e[j] < 0 ? -(long long)e[j] : 0;
+  }
+  for (int i = t; i < 2 * K * 64; i += NTH) {
+    const int par = i / (K * 64), rest = i - par * K * 64;
+    INBp(d, K, par, gt, 0)[rest] = 0;
+  }
+  for (int i = t; i < K * 64; i += NTH) d.reach[gt * K * 64 + i] = 0;
+  const int act = bfs_seed_tile<K>(d, gt, hs, fl);
+  bad = __syncthreads_or(bad);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sct += __shfl_xor_sync(0xffffffffu, sct, o);
+    neg += __shfl_xor_sync(0xffffffffu, neg, o);
+  }
+  if ((t & 31) == 0) { red[0][t >> 5] = sct; red[1][t >> 5] = neg; }
+  __syncthreads();
+  if (t == 0) {
+    long long a = 0, b = 0;
+    for (int i = 0; i < NTH / 32; ++i) { a += red[0][i]; b += red[1][i]; }
+    if (a) atomicAdd(&d.sumct[s], (unsigned long long)a);
+    d.neg0[gt] = b;
+    d.mat[gt] = 0;
+    d.tact[gt] = act;
+    d.dirty[gt] = 1; d.dirty[ns + gt] = 0;  // relax sweep 1 reads parity 0
+    d.recv[gt] = 0; d.recv[ns + gt] = 0;
+    d.crecv[gt] = 0; d.crecv[ns + gt] = 0;
+    if (bad) { d.ferr[s] = 1; d.fdone[s] = 1; }
+  }
+}
+
+// ------------------------------------------------------------------------------ a2 seed
+// Global relabel, sweep 0 (after push launches): absorb the flow still in flight, seed
+// h = 1 on nodes with residual capacity to t and relax to the tile-local fixpoint.
+template <int K>
+__global__ void __launch_bounds__(NTH) k_bfs_seed(Dev d, IO io, int par_in, int sw) {
   const int tile = blockIdx.x, s = blockIdx.y;
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   if (tile == 0 && s == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
   if (d.fdone[s]) return;
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  count_tile(d, 1);
   const size_t gt = (size_t)s * d.T + tile;
   const size_t ns = NS(d);
-  const int cur = sw & 1, prv = cur ^ 1;
-  int need = 0;
-  if (t < 9 && t != 4) {
-    const int nty = ty + t / 3 - 1, ntx = tx + t % 3 - 1;
-    if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
-      need = d.bchg[prv * ns + (size_t)s * d.T + nty * d.TX + ntx];
-  }
-  need = __syncthreads_or(need);
-  if (!need) {
-    if (t == 0) d.bchg[cur * ns + gt] = 0;
-    return;
-  }
-  count_tile(d, 1);
   __shared__ int hs[HS * HS];
-  int e[4], r[4][K], h[4], h0[4];
+  int fl[4];
+  const int rcv = (par_in >= 0) ? d.recv[par_in * ns + gt] : 0;
+  if (rcv) {
+    int e[4], r[4][K];
+    get_er<K>(d, io, gt, e, r);
+    absorb<K>(d, par_in, gt, e, r);
+    store_er<K>(d, gt, e, r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fl[j] = make_fl<K>(e[j], r[j]);
+    if (t == 0) { d.mat[gt] = 1; d.recv[par_in * ns + gt] = 0; }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
+  }
+  const int act = bfs_seed_tile<K>(d, gt, hs, fl);
+  if (t == 0) {
+    d.tact[gt] = act;
+    d.dirty[(sw & 1) * ns + gt] = 1;
+  }
+}
+
+// Mark the neighbour tiles that read a changed part of this tile's border.
+__device__ __forceinline__ void mark_neighbours(const Dev& d, int32_t* flags, size_t gt, int bits, int K) {
+  const int t = threadIdx.x;
+  if (t < 8 && ((bits >> t) & 1)) {
+    // bit: 0 N, 1 S, 2 W, 3 E, 4 NW, 5 NE, 6 SW, 7 SE
+    const int dy = (t == 0 || t == 4 || t == 5) ? -1 : ((t == 1 || t == 6 || t == 7) ? 1 : 0);
+    const int dx = (t == 2 || t == 4 || t == 6) ? -1 : ((t == 3 || t == 5 || t == 7) ? 1 : 0);
+    if (t >= 4 && K == 4) return;
+    const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+    const int ty = tile / d.TX + dy, tx = tile % d.TX + dx;
+    if (ty >= 0 && ty < d.TY && tx >= 0 && tx < d.TX) flags[(size_t)s * d.T + ty * d.TX + tx] = 1;
+  }
+}
+
+__device__ __forceinline__ int border_bits(int iy, int ix) {
+  int b = 0;
+  b |= (iy == 0) << 0;
+  b |= (iy == 31) << 1;
+  b |= (ix == 0) << 2;
+  b |= (ix == 31) << 3;
+  b |= (iy == 0 && ix == 0) << 4;
+  b |= (iy == 0 && ix == 31) << 5;
+  b |= (iy == 31 && ix == 0) << 6;
+  b |= (iy == 31 && ix == 31) << 7;
+  return b;
+}
+
+// Persistent-grid worklist: each CTA scans tiles blockIdx.x, +gridDim.x, ... 256 at a time,
+// compacts the flagged ones in shared memory and processes them one by one.
+#define GC_WORKLIST_BEGIN(PRED)                                                      \
+  __shared__ int wl_[NTH];                                                           \
+  __shared__ int wn_;                                                                \
+  const size_t ns_ = NS(d);                                                          \
+  for (size_t base_ = 0; base_ < ns_; base_ += (size_t)NTH * gridDim.x) {            \
+    const size_t id = base_ + (size_t)threadIdx.x * gridDim.x + blockIdx.x;          \
+    int want_ = 0;                                                                   \
+    if (id < ns_) want_ = (PRED);                                                    \
+    if (threadIdx.x == 0) wn_ = 0;                                                   \
+    __syncthreads();                                                                 \
+    if (want_) wl_[atomicAdd(&wn_, 1)] = (int)id;                                    \
+    __syncthreads();                                                                 \
+    const int n_ = wn_;                                                              \
+    for (int i_ = 0; i_ < n_; ++i_) {                                                \
+      const size_t gt = (size_t)wl_[i_];
+#define GC_WORKLIST_END \
+  __syncthreads();      \
+  }                     \
+  __syncthreads();      \
+  }
+
+// ------------------------------------------------------------------------------ a2 relax
+// Global relabel, sweep sw >= 1: re-relax the tiles whose neighbours' border heights
+// changed in the previous sweep, until no border changes anywhere (exact BFS distances).
+template <int K>
+__global__ void __launch_bounds__(NTH) k_bfs_relax(Dev d, int sw) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  if (blockIdx.x == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
+  const int cur = sw & 1, prv = cur ^ 1;
+  __shared__ int hs[HS * HS];
+  __shared__ int bits_s;
+  GC_WORKLIST_BEGIN(d.dirty[prv * ns_ + id] && !d.fdone[id / d.T])
+  count_tile(d, 1);
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  if (t == 0) { d.dirty[prv * ns_ + gt] = 0; bits_s = 0; }
+  int fl[4], h[4], h0[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int lp = (iy0 + 8 * j) * TS + ix;
-    e[j] = Ep(d, gt)[lp];
-    h[j] = h0[j] = Hp(d, gt)[lp];
-#pragma unroll
-    for (int k = 0; k < K; ++k) r[j][k] = Rp(d, K, s, k, tile)[lp];
+    fl[j] = d.fl[gt * TPX + lp];
+    h[j] = h0[j] = d.h[gt * TPX + lp];
     hs[hidx(iy0 + 8 * j, ix)] = h[j];
   }
   load_halo(d, s, ty, tx, hs, t);
   __syncthreads();
-  bfs_fixpoint<K>(hs, r, h, t);
-  int any = 0, bnd = 0, act = 0;
+  bfs_fixpoint<K>(hs, fl, h);
+  int any = 0, bits = 0, act = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j;
     const int ch = h[j] != h0[j];
     any |= ch;
-    bnd |= ch & on_border(iy, ix);
-    act |= (e[j] > 0) & (h[j] < HINF);
+    if (ch) bits |= border_bits(iy0 + 8 * j, ix);
+    act |= (fl[j] & FL_POS) && h[j] < HINF;
   }
+  if (bits) atomicOr(&bits_s, bits);
   any = __syncthreads_or(any);
+  act = __syncthreads_or(act);
   if (any) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) Hp(d, gt)[(iy0 + 8 * j) * TS + ix] = h[j];
+    for (int j = 0; j < 4; ++j) d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
     store_hedge(d, gt, h, t);
+    if (t == 0) d.tact[gt] = act;
   }
-  bnd = __syncthreads_or(bnd);
-  act = __syncthreads_or(act);
-  if (t == 0) {
-    if (any) d.tact[gt] = act;
-    d.bchg[cur * ns + gt] = bnd;
-    if (bnd) d.ring[sw & 63] = 1;
+  const int b = bits_s;
+  if (b) {
+    mark_neighbours(d, d.dirty + cur * ns_, gt, b, K);
+    if (t == 0) d.ring[sw & 63] = 1;
   }
+  GC_WORKLIST_END
 }
 
 // ------------------------------------------------------------------------------ status
-// Frame is done when no tile holds an active node that can reach the sink (after an exact
-// global relabel): that preflow is maximum (termination certificate).
+// A frame is done when no tile holds an active node that can reach the sink (after an
+// exact global relabel): that preflow is maximum (termination certificate).
 __global__ void __launch_bounds__(NTH) k_status(Dev d, int pushes, int relabels, int sweeps) {
   const int s = blockIdx.x, t = threadIdx.x;
   if (d.fdone[s]) return;
@@ -433,44 +539,37 @@ __global__ void __launch_bounds__(NTH) k_status(Dev d, int pushes, int relabels,
 }
 
 // ------------------------------------------------------------------------------ a3 push
-// One launch of `rounds` synchronous push / gather / relabel rounds inside each tile.
-// Pushes are decided by the owner (it lowers its own e and r); receivers inside the tile
-// gather them in a separate phase; pushes across the tile border go to the receiver
-// tile's inbox and are absorbed at its next launch.  Border heights are those of the
-// previous launch (stale); the exact global relabel restores valid labels.
+// One launch of up to `rounds` synchronous push / gather / relabel rounds inside each tile
+// that is active or has inbound flow.  Pushes are decided by the owner (it lowers its own
+// e and r); receivers inside the tile gather them in a separate phase; pushes across the
+// tile border go to the receiver tile's inbox and are absorbed at its next launch.  Border
+// heights are those of the previous launch (stale); the exact global relabel restores
+// valid labels and certifies termination.
 template <int K>
-__global__ void __launch_bounds__(NTH) k_push(Dev d, int par_in, int par_out, int rounds) {
-  const int tile = blockIdx.x, s = blockIdx.y;
-  if (d.fdone[s]) return;
+__global__ void __launch_bounds__(NTH) k_push(Dev d, IO io, int par_in, int par_out, int rounds) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const size_t gt = (size_t)s * d.T + tile;
-  const size_t ns = NS(d);
-  const int rcv = (par_in >= 0) ? d.recv[par_in * ns + gt] : 0;
-  if (!d.tact[gt] && !rcv) return;
-  count_tile(d, 2);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
   __shared__ int hs[HS * HS];
   __shared__ int ps[K][TPX];
   __shared__ int oacc[K][64];
+  const int hmax = d.hmax;
+  GC_WORKLIST_BEGIN(!d.fdone[id / d.T] && (d.tact[id] || (par_in >= 0 && d.recv[par_in * ns_ + id])))
+  count_tile(d, 2);
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  const int rcv = (par_in >= 0) ? d.recv[par_in * ns_ + gt] : 0;
   int e[4], r[4][K], h[4];
+  get_er<K>(d, io, gt, e, r);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int lp = (iy0 + 8 * j) * TS + ix;
-    e[j] = Ep(d, gt)[lp];
-    h[j] = Hp(d, gt)[lp];
-#pragma unroll
-    for (int k = 0; k < K; ++k) r[j][k] = Rp(d, K, s, k, tile)[lp];
-  }
+  for (int j = 0; j < 4; ++j) h[j] = d.h[gt * TPX + (iy0 + 8 * j) * TS + ix];
   if (rcv) {
-    absorb<K>(d, par_in, gt, e, r, t);
-    if (t == 0) d.recv[par_in * ns + gt] = 0;
+    absorb<K>(d, par_in, gt, e, r);
+    if (t == 0) d.recv[par_in * ns_ + gt] = 0;
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) hs[hidx(iy0 + 8 * j, ix)] = h[j];
   load_halo(d, s, ty, tx, hs, t);
   for (int i = t; i < K * 64; i += NTH) (&oacc[0][0])[i] = 0;
   __syncthreads();
-  const int hmax = d.hmax;
   for (int rd = 0; rd < rounds; ++rd) {
     // push phase (owner)
 #pragma unroll
@@ -488,10 +587,7 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, int par_in, int par_out, in
           r[j][k] -= dl;
         }
         if (crosses(k, iy, ix)) {
-          if (dl) {
-            const int uy = (iy + DYk(k)) & 31, ux = (ix + DXk(k)) & 31;
-            oacc[k][recv_slot(k, uy, ux)] += dl;
-          }
+          if (dl) oacc[k][recv_slot(k, (iy + DYk(k)) & 31, (ix + DXk(k)) & 31)] += dl;
         } else {
           ps[k][lp] = dl;
         }
@@ -540,13 +636,10 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, int par_in, int par_out, in
   }
   // store state
   int act = 0;
+  store_er<K>(d, gt, e, r);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int lp = (iy0 + 8 * j) * TS + ix;
-    Ep(d, gt)[lp] = e[j];
-    Hp(d, gt)[lp] = h[j];
-#pragma unroll
-    for (int k = 0; k < K; ++k) Rp(d, K, s, k, tile)[lp] = r[j][k];
+    d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
     act |= (e[j] > 0) & (h[j] < HINF);
   }
   store_hedge(d, gt, h, t);
@@ -559,29 +652,29 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, int par_in, int par_out, in
     for (int k = 0; k < K; ++k) {
       if (!crosses(k, iy, ix)) continue;
       const int y2 = iy + DYk(k), x2 = ix + DXk(k);
-      const int uy = y2 & 31, ux = x2 & 31;
-      const int sl = recv_slot(k, uy, ux);
+      const int sl = recv_slot(k, y2 & 31, x2 & 31);
       const int dl = oacc[k][sl];
       if (dl) {
         const int rty = ty + (y2 < 0 ? -1 : (y2 > 31 ? 1 : 0));
         const int rtx = tx + (x2 < 0 ? -1 : (x2 > 31 ? 1 : 0));
         const size_t rgt = (size_t)s * d.T + rty * d.TX + rtx;
         INBp(d, K, par_out, rgt, k)[sl] = dl;
-        d.recv[par_out * ns + rgt] = 1;
+        d.recv[par_out * ns_ + rgt] = 1;
       }
     }
   }
   act = __syncthreads_or(act);
-  if (t == 0) d.tact[gt] = act;
+  if (t == 0) { d.tact[gt] = act; d.mat[gt] = 1; }
+  GC_WORKLIST_END
 }
 
 // ------------------------------------------------------------------------------ a4 closure
 // mask = closure of {v : e(v) > 0} under arcs with positive residual: the
-// source side of the inclusion-minimal minimum cut.  Sweep 0 seeds every tile; later
-// sweeps process tiles that received new reach bits across their border.
+// source side of the inclusion-minimal minimum cut.  The seed pass covers every tile and
+// writes the caller's mask; relax passes follow reach bits across tile borders.
 template <int K>
-__device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uint8_t* os, int (&mm)[4], int t) {
-  const int ix = t & 31, iy0 = t >> 5;
+__device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uint8_t* os, int (&mm)[4]) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   for (;;) {
     int changed = 0;
 #pragma unroll
@@ -608,10 +701,12 @@ __device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uin
 }
 
 template <int K>
-__device__ __forceinline__ int closure_send(const Dev& d, int s, int ty, int tx, const int (&mm)[4],
-                                            const int (&send)[4], const uint8_t* os, int par_out, int t) {
-  const int ix = t & 31, iy0 = t >> 5;
+__device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os,
+                                            int par_out) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const size_t ns = NS(d);
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
   int sent = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -634,59 +729,88 @@ __device__ __forceinline__ int closure_send(const Dev& d, int s, int ty, int tx,
   return sent;
 }
 
-template <int K>
-__global__ void __launch_bounds__(NTH) k_closure_seed(Dev d, int sw) {
-  const int tile = blockIdx.x, s = blockIdx.y;
+__device__ __forceinline__ void write_mask(const Dev& d, const IO& io, size_t gt, const int (&mm)[4],
+                                           const int (&wr)[4]) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  if (tile == 0 && s == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
-  if (d.ferr[s]) return;
-  count_tile(d, 4);
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const size_t gt = (size_t)s * d.T + tile;
-  __shared__ uint8_t ms[TPX];
-  __shared__ uint8_t os[TPX];
-  int mm[4];
+  const size_t plane = (size_t)d.H * d.W;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int lp = (iy0 + 8 * j) * TS + ix;
-    const int ev = Ep(d, gt)[lp];
-    int ob = 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) ob |= (Rp(d, K, s, k, tile)[lp] > 0) << k;
-    mm[j] = ev > 0;
-    ms[lp] = (uint8_t)mm[j];
-    os[lp] = (uint8_t)ob;
-    d.open[gt * TPX + lp] = (uint8_t)ob;
+    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
+    if (wr[j] && y < d.H && x < d.W) io.mask[s * plane + (size_t)y * d.W + x] = (uint8_t)mm[j];
   }
-  __syncthreads();
-  closure_fixpoint<K>(ms, os, mm, t);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = (uint8_t)mm[j];
-  int sent = closure_send<K>(d, s, ty, tx, mm, mm, os, sw & 1, t);
-  sent = __syncthreads_or(sent);
-  if (t == 0 && sent) d.ring[sw & 63] = 1;
 }
 
 template <int K>
-__global__ void __launch_bounds__(NTH) k_closure_relax(Dev d, int sw) {
+__global__ void __launch_bounds__(NTH) k_closure_seed(Dev d, IO io, int sw) {
   const int tile = blockIdx.x, s = blockIdx.y;
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   if (tile == 0 && s == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
-  if (d.ferr[s]) return;
   const size_t gt = (size_t)s * d.T + tile;
-  const size_t ns = NS(d);
-  const int cur = sw & 1, prv = cur ^ 1;
-  if (!d.crecv[prv * ns + gt]) return;
+  const int all[4] = {1, 1, 1, 1};
+  if (d.ferr[s]) {
+    const int z[4] = {0, 0, 0, 0};
+    write_mask(d, io, gt, z, all);
+    return;
+  }
   count_tile(d, 4);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
   __shared__ uint8_t ms[TPX];
   __shared__ uint8_t os[TPX];
+  __shared__ long long red[NTH / 32];
+  int mm[4];
+  const int mat = d.mat[gt];
+  long long neg = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int lp = (iy0 + 8 * j) * TS + ix;
+    const int f = d.fl[gt * TPX + lp];
+    mm[j] = (f & FL_POS) ? 1 : 0;
+    ms[lp] = (uint8_t)mm[j];
+    os[lp] = (uint8_t)(f & 0xff);
+    if (mat) {
+      const int ev = d.e[gt * TPX + lp];
+      neg += ev < 0 ? -(long long)ev : 0;
+    }
+  }
+  __syncthreads();
+  closure_fixpoint<K>(ms, os, mm);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = (uint8_t)mm[j];
+  write_mask(d, io, gt, mm, all);
+  int sent = closure_send<K>(d, gt, mm, os, sw & 1);
+  sent = __syncthreads_or(sent);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
+  if ((t & 31) == 0) red[t >> 5] = neg;
+  __syncthreads();
+  if (t == 0) {
+    long long tot = 0;
+    if (mat) {
+      for (int i = 0; i < NTH / 32; ++i) tot += red[i];
+    } else {
+      tot = d.neg0[gt];
+    }
+    if (tot) atomicAdd(&d.sumneg[s], (unsigned long long)tot);
+    if (sent) d.ring[sw & 63] = 1;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(NTH) k_closure_relax(Dev d, IO io, int sw) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  if (blockIdx.x == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
+  const int cur = sw & 1, prv = cur ^ 1;
+  __shared__ uint8_t ms[TPX];
+  __shared__ uint8_t os[TPX];
+  GC_WORKLIST_BEGIN(d.crecv[prv * ns_ + id] && !d.ferr[id / d.T])
+  count_tile(d, 4);
   int mm[4], m0[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j, lp = iy * TS + ix;
     m0[j] = d.m[gt * TPX + lp];
-    os[lp] = d.open[gt * TPX + lp];
+    os[lp] = (uint8_t)(d.fl[gt * TPX + lp] & 0xff);
     int got = m0[j];
     if (!got && on_border(iy, ix)) {
 #pragma unroll
@@ -700,8 +824,8 @@ __global__ void __launch_bounds__(NTH) k_closure_relax(Dev d, int sw) {
     ms[lp] = (uint8_t)got;
   }
   __syncthreads();
-  if (t == 0) d.crecv[prv * ns + gt] = 0;
-  closure_fixpoint<K>(ms, os, mm, t);
+  if (t == 0) d.crecv[prv * ns_ + gt] = 0;
+  closure_fixpoint<K>(ms, os, mm);
   int nw[4], any = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -709,55 +833,43 @@ __global__ void __launch_bounds__(NTH) k_closure_relax(Dev d, int sw) {
     any |= nw[j];
   }
   any = __syncthreads_or(any);
-  if (!any) return;
+  if (any) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    if (nw[j]) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = 1;
-  int sent = closure_send<K>(d, s, ty, tx, mm, nw, os, cur, t);
-  sent = __syncthreads_or(sent);
-  if (t == 0 && sent) d.ring[sw & 63] = 1;
+    for (int j = 0; j < 4; ++j)
+      if (nw[j]) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = 1;
+    write_mask(d, io, gt, mm, nw);
+    int sent = closure_send<K>(d, gt, nw, os, cur);
+    sent = __syncthreads_or(sent);
+    if (t == 0 && sent) d.ring[sw & 63] = 1;
+  }
+  GC_WORKLIST_END
 }
 
-// ------------------------------------------------------------------------------ a4/a5 out
+// ------------------------------------------------------------------------------ a5 export
+// Forward-arc flows f = c - r of this solve (the next frame's warm start).
 template <int K>
-__global__ void __launch_bounds__(NTH) k_finalize(Dev d, IO io) {
+__global__ void __launch_bounds__(NTH) k_export(Dev d, IO io) {
   const int tile = blockIdx.x, s = blockIdx.y;
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const size_t gt = (size_t)s * d.T + tile;
-  count_tile(d, 5);
   const int err = d.ferr[s];
-  long long neg = 0;
+  int e[4], r[4][K];
+  get_er<K>(d, io, gt, e, r);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j, y = ty * TS + iy, x = tx * TS + ix, lp = iy * TS + ix;
+    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
     if (y >= H || x >= W) continue;
     const size_t o = (size_t)y * W + x;
-    io.mask[s * plane + o] = err ? 0 : d.m[gt * TPX + lp];
-    const int ev = Ep(d, gt)[lp];
-    neg += ev < 0 ? -(long long)ev : 0;
-    if (io.fstate) {
 #pragma unroll
-      for (int k = 0; k < K; k += 2) {
-        const int y2 = y + DYk(k), x2 = x + DXk(k);
-        int f = 0;
-        if (!err && y2 >= 0 && y2 < H && x2 >= 0 && x2 < W)
-          f = io.nb[s * plane * K + k * plane + o] - Rp(d, K, s, k, tile)[lp];  // a5: f = c - r
-        io.fstate[s * plane * (K / 2) + (k >> 1) * plane + o] = f;
-      }
+    for (int k = 0; k < K; k += 2) {
+      const int y2 = y + DYk(k), x2 = x + DXk(k);
+      int f = 0;
+      if (!err && y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = io.nb[s * plane * K + k * plane + o] - r[j][k];
+      io.fstate[s * plane * (K / 2) + (k >> 1) * plane + o] = f;
     }
-  }
-  __shared__ long long red[NTH / 32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
-  if ((t & 31) == 0) red[t >> 5] = neg;
-  __syncthreads();
-  if (t == 0) {
-    long long tot = 0;
-    for (int i = 0; i < NTH / 32; ++i) tot += red[i];
-    if (tot) atomicAdd(&d.sumneg[s], (unsigned long long)tot);
   }
 }
 

@@ -49,13 +49,14 @@ size_t frame_bytes(int K, size_t T) {
   size_t b = 0;
   b += 2 * T * TPX * 4;           // e, h
   b += (size_t)K * T * TPX * 4;   // r
+  b += T * TPX * 2;               // fl
+  b += T * TPX;                   // m
   b += T * 128 * 4;               // hedge
   b += 2 * T * K * 64 * 4;        // inbox
   b += T * K * 64;                // reach
-  b += 2 * T * TPX;               // m, open
-  b += 7 * T * 4;                 // tile flags
+  b += T * 8 + 8 * T * 4;         // neg0 + tile flags
   b += 64;                        // frame words
-  return b + 4096;
+  return b + 16 * 256;            // alignment slack
 }
 
 int tiles_of(int H, int W) { return ((H + TS - 1) / TS) * ((W + TS - 1) / TS); }
@@ -74,13 +75,15 @@ Dev carve(gc_ctx* c, int nslot, int H, int W) {
   d.e = (int32_t*)take(ns * TPX * 4);
   d.h = (int32_t*)take(ns * TPX * 4);
   d.r = (int32_t*)take(ns * K * TPX * 4);
+  d.fl = (uint16_t*)take(ns * TPX * 2);
+  d.m = (uint8_t*)take(ns * TPX);
   d.hedge = (int32_t*)take(ns * 128 * 4);
   d.inbox = (int32_t*)take(2 * ns * K * 64 * 4);
   d.reach = (uint8_t*)take(ns * K * 64);
-  d.m = (uint8_t*)take(ns * TPX);
-  d.open = (uint8_t*)take(ns * TPX);
+  d.neg0 = (long long*)take(ns * 8);
+  d.mat = (int32_t*)take(ns * 4);
   d.tact = (int32_t*)take(ns * 4);
-  d.bchg = (int32_t*)take(2 * ns * 4);
+  d.dirty = (int32_t*)take(2 * ns * 4);
   d.recv = (int32_t*)take(2 * ns * 4);
   d.crecv = (int32_t*)take(2 * ns * 4);
   // per-frame words: contiguous so one memset clears them
@@ -146,18 +149,37 @@ void resolve_profile(gc_ctx* c) {
   c->evnext = 0;
 }
 
+// Persistent grid size of a worklist kernel: resident CTAs per SM x SMs.
+template <typename F>
+int persistent_grid(gc_ctx* c, F kernel) {
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, NTH, 0);
+  if (per < 1) per = 1;
+  if (sms < 1) sms = 148;
+  return sms * per;
+}
+
 template <int K>
 gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStream_t st, Launcher& L) {
   Dev d = carve(c, nslot, H, W);
   const dim3 grid(d.T, nslot), blk(NTH);
+  static int g_relax = 0, g_push = 0, g_clos = 0;  // per-K persistent grid sizes (same device)
+  if (!g_relax) {
+    g_relax = persistent_grid(c, k_bfs_relax<K>);
+    g_push = persistent_grid(c, k_push<K>);
+    g_clos = persistent_grid(c, k_closure_relax<K>);
+  }
+  const size_t ns = (size_t)nslot * d.T;
+  auto wgrid = [&](int g) { return (int)((size_t)g < ns ? g : ns); };
   if (!ck(c, cudaMemsetAsync(d.fdone, 0, frame_words_bytes(d), st), "memset")) return GC_ERR_CUDA;
+  // ---- a1 + first a2 seed sweep
   L.pre(0);
-  if (io.wf) k_init<K, true><<<grid, blk, 0, st>>>(d, io);
-  else k_init<K, false><<<grid, blk, 0, st>>>(d, io);
+  k_init<K><<<grid, blk, 0, st>>>(d, io);
   L.post();
   if (!ck(c, cudaGetLastError(), "k_init")) return GC_ERR_CUDA;
 
-  int push_launches = 0, relabels = 0, sweeps = 0, last_par = -1, sw = 0;
+  int push_launches = 0, relabels = 1, sweeps = 1, last_par = -1, sw = 1;
   const int BATCH = 4;
   gc_status status = GC_OK;
   auto poll = [&](const int32_t* dptr) -> int {
@@ -166,16 +188,11 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStre
     return c->hpin[0];
   };
   for (;;) {
-    // ---- a2: exact global relabel
-    L.pre(1);
-    k_bfs_seed<K><<<grid, blk, 0, st>>>(d, last_par, sw);
-    L.post();
-    last_par = -1;
-    ++sw; ++sweeps; ++relabels;
+    // ---- a2: relax sweeps of the global relabel until no border height changes
     for (;;) {
       for (int b = 0; b < BATCH; ++b) {
         L.pre(1);
-        k_bfs_relax<K><<<grid, blk, 0, st>>>(d, sw);
+        k_bfs_relax<K><<<wgrid(g_relax), blk, 0, st>>>(d, sw);
         L.post();
         ++sw; ++sweeps;
       }
@@ -196,23 +213,29 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStre
       const int par_out = push_launches & 1;
       const int par_in = (j == 0) ? -1 : (par_out ^ 1);
       L.pre(2);
-      k_push<K><<<grid, blk, 0, st>>>(d, par_in, par_out, c->rounds);
+      k_push<K><<<wgrid(g_push), blk, 0, st>>>(d, io, par_in, par_out, c->rounds);
       L.post();
       ++push_launches;
       last_par = par_out;
     }
     if (!ck(c, cudaGetLastError(), "k_push")) return GC_ERR_CUDA;
+    // ---- a2: next global relabel, seed sweep
+    L.pre(1);
+    k_bfs_seed<K><<<grid, blk, 0, st>>>(d, io, last_par, sw);
+    L.post();
+    last_par = -1;
+    ++sw; ++sweeps; ++relabels;
   }
-  // ---- a4: canonical mask
+  // ---- a4: canonical mask (+ the flow value's sum over e)
   L.pre(4);
-  k_closure_seed<K><<<grid, blk, 0, st>>>(d, sw);
+  k_closure_seed<K><<<grid, blk, 0, st>>>(d, io, sw);
   L.post();
   ++sw;
   if (poll(d.ring + ((sw - 1) & 63))) {
     for (;;) {
       for (int b = 0; b < BATCH; ++b) {
         L.pre(4);
-        k_closure_relax<K><<<grid, blk, 0, st>>>(d, sw);
+        k_closure_relax<K><<<wgrid(g_clos), blk, 0, st>>>(d, io, sw);
         L.post();
         ++sw;
       }
@@ -220,13 +243,15 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStre
       if (!poll(d.ring + ((sw - 1) & 63))) break;
     }
   }
-  L.pre(5);
-  k_finalize<K><<<grid, blk, 0, st>>>(d, io);
-  L.post();
+  if (io.fstate) {
+    L.pre(5);
+    k_export<K><<<grid, blk, 0, st>>>(d, io);
+    L.post();
+  }
   cudaMemsetAsync(d.ctr, 0, 16, st);
   k_flow<<<(nslot + 127) / 128, 128, 0, st>>>(d, io);
   ++L.n;
-  if (!ck(c, cudaGetLastError(), "k_finalize")) return GC_ERR_CUDA;
+  if (!ck(c, cudaGetLastError(), "k_flow")) return GC_ERR_CUDA;
   cudaMemcpyAsync(c->hpin, d.ctr, 12, cudaMemcpyDeviceToHost, st);
   if (!ck(c, cudaStreamSynchronize(st), "solve")) return GC_ERR_CUDA;
   if (c->hpin[1]) return GC_ERR_RANGE;
