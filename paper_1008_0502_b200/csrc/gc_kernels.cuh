@@ -329,36 +329,98 @@ __device__ __forceinline__ int bfs_seed_tile(const Dev& d, size_t gt, int* hs, c
   return __syncthreads_or(act);
 }
 
-// ------------------------------------------------------------------------------ a1 + a2 seed
-// Init fused with the first global-relabel seed sweep: computes e, r in registers (not
-// stored: the tile stays un-materialised), writes fl, h, the frame's sum c(v,t), the
-// tile's sum max(0,-e), and the range flag.
-template <int K>
+// ------------------------------------------------------------------------------ a1
+// Init: a streaming pass over the caps.  Computes e and r in registers (the tile stays
+// un-materialised -- e, r are recomputed if a push ever touches it) and writes only the
+// 2-byte fl word per pixel, the frame's sum c(v,t), the tile's sum max(0,-e) and the
+// range flag.  Thread t owns 4 consecutive pixels of row t/8 (int4 loads when the caller's
+// rows are 16-byte aligned).
+template <int K, bool VEC>
 __global__ void __launch_bounds__(NTH) k_init(Dev d, IO io) {
   const int tile = blockIdx.x, s = blockIdx.y;
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
   const size_t gt = (size_t)s * d.T + tile;
   const size_t ns = NS(d);
+  const int H = d.H, W = d.W;
+  const size_t plane = (size_t)H * W;
   count_tile(d, 0);
-  __shared__ int hs[HS * HS];
   __shared__ long long red[2][NTH / 32];
-  int e[4], r[4][K], fl[4];
+  const int32_t* cs = io.cs + s * plane;
+  const int32_t* ct = io.ct + s * plane;
+  const int32_t* nb = io.nb + s * plane * K;
+  const int32_t* wf = io.wf ? io.wf + s * plane * (K / 2) : nullptr;
+  const int y = ty * TS + iy, x0 = tx * TS + ix0;
   int bad = 0;
   long long sct = 0, neg = 0;
-  tile_from_caps<K>(d, io, s, ty, tx, e, r, bad, sct);
+  int a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0}, c[K][4];
+  const size_t o0 = (size_t)y * W + x0;
+  const bool full = VEC && y < H && x0 + 3 < W;
+  if (full) {
+    const int4 va = __ldg(reinterpret_cast<const int4*>(cs + o0));
+    const int4 vb = __ldg(reinterpret_cast<const int4*>(ct + o0));
+    a[0] = va.x; a[1] = va.y; a[2] = va.z; a[3] = va.w;
+    b[0] = vb.x; b[1] = vb.y; b[2] = vb.z; b[3] = vb.w;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    fl[j] = make_fl<K>(e[j], r[j]);
-    d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix] = (uint16_t)fl[j];
-    neg += e[j] < 0 ? -(long long)e[j] : 0;
+    for (int k = 0; k < K; ++k) {
+      const int4 v = __ldg(reinterpret_cast<const int4*>(nb + k * plane + o0));
+      c[k][0] = v.x; c[k][1] = v.y; c[k][2] = v.z; c[k][3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool in = y < H && x0 + i < W;
+      a[i] = in ? __ldg(cs + o0 + i) : 0;
+      b[i] = in ? __ldg(ct + o0 + i) : 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) c[k][i] = in ? __ldg(nb + k * plane + o0 + i) : 0;
+    }
   }
+  int fl4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int x = x0 + i;
+    int f = 0;
+    if (y < H && x < W) {
+      bad |= (a[i] < 0) | (a[i] > CAPMAX) | (b[i] < 0) | (b[i] > CAPMAX);
+      int ev = a[i] - b[i];  // a1: pre-cancel min(cs,ct) straight s -> v -> t
+      sct += b[i];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int y2 = y + DYk(k), x2 = x + DXk(k);
+        if (y2 < 0 || y2 >= H || x2 < 0 || x2 >= W) continue;  // off-grid: ignored (c7)
+        const int ck = c[k][i];
+        bad |= (ck < 0) | (ck > CAPMAX);
+        int rk = ck;
+        if (wf) {  // a1w: clamp the previous flow to the new capacities
+          const size_t oq = (size_t)y2 * W + x2;
+          const int cq = __ldg(nb + (k ^ 1) * plane + oq);
+          if ((k & 1) == 0) {
+            const int fv = max(-cq, min(ck, __ldg(wf + (k >> 1) * plane + o0 + i)));
+            rk = ck - fv;
+            ev -= fv;
+          } else {
+            const int fv = max(-ck, min(cq, __ldg(wf + ((k ^ 1) >> 1) * plane + oq)));
+            rk = ck + fv;
+            ev += fv;
+          }
+        }
+        f |= (rk > 0) << k;
+      }
+      f |= (ev > 0 ? FL_POS : 0) | (ev < 0 ? FL_NEG : 0);
+      neg += ev < 0 ? -(long long)ev : 0;
+    }
+    fl4[i] = f;
+  }
+  ushort4 w;
+  w.x = (unsigned short)fl4[0]; w.y = (unsigned short)fl4[1];
+  w.z = (unsigned short)fl4[2]; w.w = (unsigned short)fl4[3];
+  *reinterpret_cast<ushort4*>(d.fl + gt * TPX + iy * TS + ix0) = w;
   for (int i = t; i < 2 * K * 64; i += NTH) {
     const int par = i / (K * 64), rest = i - par * K * 64;
     INBp(d, K, par, gt, 0)[rest] = 0;
   }
   for (int i = t; i < K * 64; i += NTH) d.reach[gt * K * 64 + i] = 0;
-  const int act = bfs_seed_tile<K>(d, gt, hs, fl);
   bad = __syncthreads_or(bad);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -368,13 +430,12 @@ __global__ void __launch_bounds__(NTH) k_init(Dev d, IO io) {
   if ((t & 31) == 0) { red[0][t >> 5] = sct; red[1][t >> 5] = neg; }
   __syncthreads();
   if (t == 0) {
-    long long a = 0, b = 0;
-    for (int i = 0; i < NTH / 32; ++i) { a += red[0][i]; b += red[1][i]; }
-    if (a) atomicAdd(&d.sumct[s], (unsigned long long)a);
-    d.neg0[gt] = b;
+    long long sa = 0, sb = 0;
+    for (int i = 0; i < NTH / 32; ++i) { sa += red[0][i]; sb += red[1][i]; }
+    if (sa) atomicAdd(&d.sumct[s], (unsigned long long)sa);
+    d.neg0[gt] = sb;
     d.mat[gt] = 0;
-    d.tact[gt] = act;
-    d.dirty[gt] = 1; d.dirty[ns + gt] = 0;  // relax sweep 1 reads parity 0
+    d.dirty[gt] = 0; d.dirty[ns + gt] = 0;
     d.recv[gt] = 0; d.recv[ns + gt] = 0;
     d.crecv[gt] = 0; d.crecv[ns + gt] = 0;
     if (bad) { d.ferr[s] = 1; d.fdone[s] = 1; }

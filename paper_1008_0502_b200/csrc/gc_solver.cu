@@ -173,11 +173,18 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStre
   const size_t ns = (size_t)nslot * d.T;
   auto wgrid = [&](int g) { return (int)((size_t)g < ns ? g : ns); };
   if (!ck(c, cudaMemsetAsync(d.fdone, 0, frame_words_bytes(d), st), "memset")) return GC_ERR_CUDA;
-  // ---- a1 + first a2 seed sweep
+  // ---- a1 (int4 loads when every caller row is 16-byte aligned)
+  const bool vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
+                   ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
   L.pre(0);
-  k_init<K><<<grid, blk, 0, st>>>(d, io);
+  if (vec) k_init<K, true><<<grid, blk, 0, st>>>(d, io);
+  else k_init<K, false><<<grid, blk, 0, st>>>(d, io);
   L.post();
   if (!ck(c, cudaGetLastError(), "k_init")) return GC_ERR_CUDA;
+  // ---- a2: first global relabel, seed sweep (reads fl only)
+  L.pre(1);
+  k_bfs_seed<K><<<grid, blk, 0, st>>>(d, io, -1, 0);
+  L.post();
 
   int push_launches = 0, relabels = 1, sweeps = 1, last_par = -1, sw = 1;
   const int BATCH = 4;
