@@ -62,15 +62,25 @@ struct Dev {
   int32_t* dirty;   // [2][NS] tile must be re-relaxed in the next BFS sweep of that parity
   int32_t* recv;    // [2][NS] tile has inbound flow in inbox of that parity
   int32_t* crecv;   // [2][NS] tile received new reach bits in the closure sweep of that parity
-  int32_t* fdone;   // [nslot]
-  int32_t* ferr;    // [nslot]
-  int32_t* fstat;   // [nslot][4]
-  unsigned long long* sumct;   // [nslot]
-  unsigned long long* sumneg;  // [nslot]
-  int32_t* ring;    // [64] per-sweep "something changed" flags
+  int32_t* tph;     // [NS]   push-phase stamp of the last push that touched the tile
+  // per frame (state machine): all zero-initialised by one memset
+  int32_t* fmode;   // [nslot] M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_DONE
+  int32_t* ferr;    // [nslot] capacity out of range
+  int32_t* fchg;    // [2][nslot] something changed in the step of that parity (BFS / closure)
+  int32_t* fph;     // [nslot] global relabels so far (push-phase id)
+  int32_t* fpush;   // [nslot] push steps in the current phase
+  int32_t* fnew;    // [nslot] tiles first touched by a push in this step
+  int32_t* fstat;   // [nslot][4] push steps, global relabels, BFS sweeps, -
+  unsigned long long* fabs_;  // [nslot] flow absorbed by sink-connected nodes in this step
+  unsigned long long* frel;   // [nslot] relabel operations in the current push phase
+  unsigned long long* sumct;  // [nslot]
+  unsigned long long* sumneg; // [nslot]
+  int32_t* ring;    // [64] frames not done, per step
   int32_t* ctr;     // [8]
   unsigned long long* ptiles;  // [6] tiles processed per kernel class (profiling only, else NULL)
 };
+
+enum { M_SEED = 0, M_BFS = 1, M_PUSH = 2, M_CSEED = 3, M_CLOS = 4, M_DONE = 5 };
 
 struct IO {
   const int32_t* cs;
@@ -438,518 +448,9 @@ __global__ void __launch_bounds__(NTH) k_init(Dev d, IO io) {
     d.dirty[gt] = 0; d.dirty[ns + gt] = 0;
     d.recv[gt] = 0; d.recv[ns + gt] = 0;
     d.crecv[gt] = 0; d.crecv[ns + gt] = 0;
-    if (bad) { d.ferr[s] = 1; d.fdone[s] = 1; }
+    d.tph[gt] = -1;
+    if (bad) d.ferr[s] = 1;
   }
-}
-
-// ------------------------------------------------------------------------------ a2 seed
-// Global relabel, sweep 0 (after push launches): absorb the flow still in flight, seed
-// h = 1 on nodes with residual capacity to t and relax to the tile-local fixpoint.
-template <int K>
-__global__ void __launch_bounds__(NTH) k_bfs_seed(Dev d, IO io, int par_in, int sw) {
-  const int tile = blockIdx.x, s = blockIdx.y;
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  if (tile == 0 && s == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
-  if (d.fdone[s]) return;
-  count_tile(d, 1);
-  const size_t gt = (size_t)s * d.T + tile;
-  const size_t ns = NS(d);
-  __shared__ int hs[HS * HS];
-  int fl[4];
-  const int rcv = (par_in >= 0) ? d.recv[par_in * ns + gt] : 0;
-  if (rcv) {
-    int e[4], r[4][K];
-    get_er<K>(d, io, gt, e, r);
-    absorb<K>(d, par_in, gt, e, r);
-    store_er<K>(d, gt, e, r);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) fl[j] = make_fl<K>(e[j], r[j]);
-    if (t == 0) { d.mat[gt] = 1; d.recv[par_in * ns + gt] = 0; }
-  } else {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
-  }
-  const int act = bfs_seed_tile<K>(d, gt, hs, fl);
-  if (t == 0) {
-    d.tact[gt] = act;
-    d.dirty[(sw & 1) * ns + gt] = 1;
-  }
-}
-
-// Mark the neighbour tiles that read a changed part of this tile's border.
-__device__ __forceinline__ void mark_neighbours(const Dev& d, int32_t* flags, size_t gt, int bits, int K) {
-  const int t = threadIdx.x;
-  if (t < 8 && ((bits >> t) & 1)) {
-    // bit: 0 N, 1 S, 2 W, 3 E, 4 NW, 5 NE, 6 SW, 7 SE
-    const int dy = (t == 0 || t == 4 || t == 5) ? -1 : ((t == 1 || t == 6 || t == 7) ? 1 : 0);
-    const int dx = (t == 2 || t == 4 || t == 6) ? -1 : ((t == 3 || t == 5 || t == 7) ? 1 : 0);
-    if (t >= 4 && K == 4) return;
-    const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-    const int ty = tile / d.TX + dy, tx = tile % d.TX + dx;
-    if (ty >= 0 && ty < d.TY && tx >= 0 && tx < d.TX) flags[(size_t)s * d.T + ty * d.TX + tx] = 1;
-  }
-}
-
-__device__ __forceinline__ int border_bits(int iy, int ix) {
-  int b = 0;
-  b |= (iy == 0) << 0;
-  b |= (iy == 31) << 1;
-  b |= (ix == 0) << 2;
-  b |= (ix == 31) << 3;
-  b |= (iy == 0 && ix == 0) << 4;
-  b |= (iy == 0 && ix == 31) << 5;
-  b |= (iy == 31 && ix == 0) << 6;
-  b |= (iy == 31 && ix == 31) << 7;
-  return b;
-}
-
-// Persistent-grid worklist: each CTA scans tiles blockIdx.x, +gridDim.x, ... 256 at a time,
-// compacts the flagged ones in shared memory and processes them one by one.
-#define GC_WORKLIST_BEGIN(PRED)                                                      \
-  __shared__ int wl_[NTH];                                                           \
-  __shared__ int wn_;                                                                \
-  const size_t ns_ = NS(d);                                                          \
-  for (size_t base_ = 0; base_ < ns_; base_ += (size_t)NTH * gridDim.x) {            \
-    const size_t id = base_ + (size_t)threadIdx.x * gridDim.x + blockIdx.x;          \
-    int want_ = 0;                                                                   \
-    if (id < ns_) want_ = (PRED);                                                    \
-    if (threadIdx.x == 0) wn_ = 0;                                                   \
-    __syncthreads();                                                                 \
-    if (want_) wl_[atomicAdd(&wn_, 1)] = (int)id;                                    \
-    __syncthreads();                                                                 \
-    const int n_ = wn_;                                                              \
-    for (int i_ = 0; i_ < n_; ++i_) {                                                \
-      const size_t gt = (size_t)wl_[i_];
-#define GC_WORKLIST_END \
-  __syncthreads();      \
-  }                     \
-  __syncthreads();      \
-  }
-
-// ------------------------------------------------------------------------------ a2 relax
-// Global relabel, sweep sw >= 1: re-relax the tiles whose neighbours' border heights
-// changed in the previous sweep, until no border changes anywhere (exact BFS distances).
-template <int K>
-__global__ void __launch_bounds__(NTH) k_bfs_relax(Dev d, int sw) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  if (blockIdx.x == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
-  const int cur = sw & 1, prv = cur ^ 1;
-  __shared__ int hs[HS * HS];
-  __shared__ int bits_s;
-  GC_WORKLIST_BEGIN(d.dirty[prv * ns_ + id] && !d.fdone[id / d.T])
-  count_tile(d, 1);
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  if (t == 0) { d.dirty[prv * ns_ + gt] = 0; bits_s = 0; }
-  int fl[4], h[4], h0[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int lp = (iy0 + 8 * j) * TS + ix;
-    fl[j] = d.fl[gt * TPX + lp];
-    h[j] = h0[j] = d.h[gt * TPX + lp];
-    hs[hidx(iy0 + 8 * j, ix)] = h[j];
-  }
-  load_halo(d, s, ty, tx, hs, t);
-  __syncthreads();
-  bfs_fixpoint<K>(hs, fl, h);
-  int any = 0, bits = 0, act = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int ch = h[j] != h0[j];
-    any |= ch;
-    if (ch) bits |= border_bits(iy0 + 8 * j, ix);
-    act |= (fl[j] & FL_POS) && h[j] < HINF;
-  }
-  if (bits) atomicOr(&bits_s, bits);
-  any = __syncthreads_or(any);
-  act = __syncthreads_or(act);
-  if (any) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
-    store_hedge(d, gt, h, t);
-    if (t == 0) d.tact[gt] = act;
-  }
-  const int b = bits_s;
-  if (b) {
-    mark_neighbours(d, d.dirty + cur * ns_, gt, b, K);
-    if (t == 0) d.ring[sw & 63] = 1;
-  }
-  GC_WORKLIST_END
-}
-
-// ------------------------------------------------------------------------------ status
-// A frame is done when no tile holds an active node that can reach the sink (after an
-// exact global relabel): that preflow is maximum (termination certificate).
-__global__ void __launch_bounds__(NTH) k_status(Dev d, int pushes, int relabels, int sweeps) {
-  const int s = blockIdx.x, t = threadIdx.x;
-  if (d.fdone[s]) return;
-  count_tile(d, 3);
-  int any = 0;
-  for (int i = t; i < d.T; i += NTH) any |= d.tact[(size_t)s * d.T + i];
-  any = __syncthreads_or(any);
-  if (t == 0) {
-    if (!any) {
-      d.fdone[s] = 1;
-      d.fstat[s * 4 + 0] = pushes;
-      d.fstat[s * 4 + 1] = relabels;
-      d.fstat[s * 4 + 2] = sweeps;
-    } else {
-      atomicAdd(&d.ctr[0], 1);
-    }
-  }
-}
-
-// ------------------------------------------------------------------------------ a3 push
-// One launch of up to `rounds` synchronous push / gather / relabel rounds inside each tile
-// that is active or has inbound flow.  Pushes are decided by the owner (it lowers its own
-// e and r); receivers inside the tile gather them in a separate phase; pushes across the
-// tile border go to the receiver tile's inbox and are absorbed at its next launch.  Border
-// heights are those of the previous launch (stale); the exact global relabel restores
-// valid labels and certifies termination.
-template <int K>
-__global__ void __launch_bounds__(NTH) k_push(Dev d, IO io, int par_in, int par_out, int rounds) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  __shared__ int hs[HS * HS];
-  __shared__ int ps[K][TPX];
-  __shared__ int oacc[K][64];
-  const int hmax = d.hmax;
-  GC_WORKLIST_BEGIN(!d.fdone[id / d.T] && (d.tact[id] || (par_in >= 0 && d.recv[par_in * ns_ + id])))
-  count_tile(d, 2);
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const int rcv = (par_in >= 0) ? d.recv[par_in * ns_ + gt] : 0;
-  int e[4], r[4][K], h[4];
-  get_er<K>(d, io, gt, e, r);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) h[j] = d.h[gt * TPX + (iy0 + 8 * j) * TS + ix];
-  if (rcv) {
-    absorb<K>(d, par_in, gt, e, r);
-    if (t == 0) d.recv[par_in * ns_ + gt] = 0;
-  }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) hs[hidx(iy0 + 8 * j, ix)] = h[j];
-  load_halo(d, s, ty, tx, hs, t);
-  for (int i = t; i < K * 64; i += NTH) (&oacc[0][0])[i] = 0;
-  __syncthreads();
-  for (int rd = 0; rd < rounds; ++rd) {
-    // push phase (owner)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int iy = iy0 + 8 * j, lp = iy * TS + ix;
-      int ee = e[j];
-      const int hv = h[j];
-      const bool act = ee > 0 && hv < HINF;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        int dl = 0;
-        if (act && ee > 0 && r[j][k] > 0 && hs[hidx(iy + DYk(k), ix + DXk(k))] == hv - 1) {
-          dl = min(ee, r[j][k]);
-          ee -= dl;
-          r[j][k] -= dl;
-        }
-        if (crosses(k, iy, ix)) {
-          if (dl) oacc[k][recv_slot(k, (iy + DYk(k)) & 31, (ix + DXk(k)) & 31)] += dl;
-        } else {
-          ps[k][lp] = dl;
-        }
-      }
-      e[j] = ee;
-    }
-    __syncthreads();
-    // gather phase (receiver) + relabel decision
-    int hn[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int iy = iy0 + 8 * j;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int wy = iy - DYk(k), wx = ix - DXk(k);
-        if ((unsigned)wy < 32u && (unsigned)wx < 32u) {
-          const int dl = ps[k][wy * TS + wx];
-          e[j] += dl;
-          r[j][k ^ 1] += dl;
-        }
-      }
-      hn[j] = h[j];
-      if (e[j] > 0 && h[j] < HINF) {
-        int mn = HINF;
-        bool adm = false;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          if (r[j][k] > 0) {
-            const int hu = hs[hidx(iy + DYk(k), ix + DXk(k))];
-            adm |= (hu == h[j] - 1);
-            mn = min(mn, hu);
-          }
-        }
-        if (!adm) hn[j] = (mn >= hmax - 1) ? HINF : mn + 1;
-      }
-    }
-    __syncthreads();
-    int still = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      h[j] = hn[j];
-      hs[hidx(iy0 + 8 * j, ix)] = hn[j];
-      still |= (e[j] > 0) & (hn[j] < HINF);
-    }
-    if (!__syncthreads_or(still)) break;  // tile discharged: nothing left to push
-  }
-  // store state
-  int act = 0;
-  store_er<K>(d, gt, e, r);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
-    act |= (e[j] > 0) & (h[j] < HINF);
-  }
-  store_hedge(d, gt, h, t);
-  // send border pushes to the neighbours' inboxes (unique writer per slot)
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j;
-    if (!on_border(iy, ix)) continue;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (!crosses(k, iy, ix)) continue;
-      const int y2 = iy + DYk(k), x2 = ix + DXk(k);
-      const int sl = recv_slot(k, y2 & 31, x2 & 31);
-      const int dl = oacc[k][sl];
-      if (dl) {
-        const int rty = ty + (y2 < 0 ? -1 : (y2 > 31 ? 1 : 0));
-        const int rtx = tx + (x2 < 0 ? -1 : (x2 > 31 ? 1 : 0));
-        const size_t rgt = (size_t)s * d.T + rty * d.TX + rtx;
-        INBp(d, K, par_out, rgt, k)[sl] = dl;
-        d.recv[par_out * ns_ + rgt] = 1;
-      }
-    }
-  }
-  act = __syncthreads_or(act);
-  if (t == 0) { d.tact[gt] = act; d.mat[gt] = 1; }
-  GC_WORKLIST_END
-}
-
-// ------------------------------------------------------------------------------ a4 closure
-// mask = closure of {v : e(v) > 0} under arcs with positive residual: the
-// source side of the inclusion-minimal minimum cut.  The seed pass covers every tile and
-// writes the caller's mask; relax passes follow reach bits across tile borders.
-template <int K>
-__device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uint8_t* os, int (&mm)[4]) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  for (;;) {
-    int changed = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (mm[j]) continue;
-      const int iy = iy0 + 8 * j;
-      int got = 0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int wy = iy - DYk(k), wx = ix - DXk(k);
-        if ((unsigned)wy < 32u && (unsigned)wx < 32u) {
-          const int w = wy * TS + wx;
-          got |= ms[w] & (os[w] >> k) & 1;
-        }
-      }
-      if (got) {
-        mm[j] = 1;
-        ms[iy * TS + ix] = 1;
-        changed = 1;
-      }
-    }
-    if (!__syncthreads_or(changed)) break;
-  }
-}
-
-template <int K>
-__device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os,
-                                            int par_out) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const size_t ns = NS(d);
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  int sent = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j;
-    if (!send[j] || !on_border(iy, ix)) continue;
-    const int ob = os[iy * TS + ix];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (!crosses(k, iy, ix) || !((ob >> k) & 1)) continue;
-      const int y2 = iy + DYk(k), x2 = ix + DXk(k);
-      const int rty = ty + (y2 < 0 ? -1 : (y2 > 31 ? 1 : 0));
-      const int rtx = tx + (x2 < 0 ? -1 : (x2 > 31 ? 1 : 0));
-      if (rty < 0 || rty >= d.TY || rtx < 0 || rtx >= d.TX) continue;
-      const size_t rgt = (size_t)s * d.T + rty * d.TX + rtx;
-      d.reach[(rgt * K + k) * 64 + recv_slot(k, y2 & 31, x2 & 31)] = 1;
-      d.crecv[par_out * ns + rgt] = 1;
-      sent = 1;
-    }
-  }
-  return sent;
-}
-
-__device__ __forceinline__ void write_mask(const Dev& d, const IO& io, size_t gt, const int (&mm)[4],
-                                           const int (&wr)[4]) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const size_t plane = (size_t)d.H * d.W;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
-    if (wr[j] && y < d.H && x < d.W) io.mask[s * plane + (size_t)y * d.W + x] = (uint8_t)mm[j];
-  }
-}
-
-template <int K>
-__global__ void __launch_bounds__(NTH) k_closure_seed(Dev d, IO io, int sw) {
-  const int tile = blockIdx.x, s = blockIdx.y;
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  if (tile == 0 && s == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
-  const size_t gt = (size_t)s * d.T + tile;
-  const int all[4] = {1, 1, 1, 1};
-  if (d.ferr[s]) {
-    const int z[4] = {0, 0, 0, 0};
-    write_mask(d, io, gt, z, all);
-    return;
-  }
-  count_tile(d, 4);
-  __shared__ uint8_t ms[TPX];
-  __shared__ uint8_t os[TPX];
-  __shared__ long long red[NTH / 32];
-  int mm[4];
-  const int mat = d.mat[gt];
-  long long neg = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int lp = (iy0 + 8 * j) * TS + ix;
-    const int f = d.fl[gt * TPX + lp];
-    mm[j] = (f & FL_POS) ? 1 : 0;
-    ms[lp] = (uint8_t)mm[j];
-    os[lp] = (uint8_t)(f & 0xff);
-    if (mat) {
-      const int ev = d.e[gt * TPX + lp];
-      neg += ev < 0 ? -(long long)ev : 0;
-    }
-  }
-  __syncthreads();
-  closure_fixpoint<K>(ms, os, mm);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = (uint8_t)mm[j];
-  write_mask(d, io, gt, mm, all);
-  int sent = closure_send<K>(d, gt, mm, os, sw & 1);
-  sent = __syncthreads_or(sent);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
-  if ((t & 31) == 0) red[t >> 5] = neg;
-  __syncthreads();
-  if (t == 0) {
-    long long tot = 0;
-    if (mat) {
-      for (int i = 0; i < NTH / 32; ++i) tot += red[i];
-    } else {
-      tot = d.neg0[gt];
-    }
-    if (tot) atomicAdd(&d.sumneg[s], (unsigned long long)tot);
-    if (sent) d.ring[sw & 63] = 1;
-  }
-}
-
-template <int K>
-__global__ void __launch_bounds__(NTH) k_closure_relax(Dev d, IO io, int sw) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  if (blockIdx.x == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
-  const int cur = sw & 1, prv = cur ^ 1;
-  __shared__ uint8_t ms[TPX];
-  __shared__ uint8_t os[TPX];
-  GC_WORKLIST_BEGIN(d.crecv[prv * ns_ + id] && !d.ferr[id / d.T])
-  count_tile(d, 4);
-  int mm[4], m0[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j, lp = iy * TS + ix;
-    m0[j] = d.m[gt * TPX + lp];
-    os[lp] = (uint8_t)(d.fl[gt * TPX + lp] & 0xff);
-    int got = m0[j];
-    if (!got && on_border(iy, ix)) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int wy = iy - DYk(k), wx = ix - DXk(k);
-        if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-        got |= d.reach[(gt * K + k) * 64 + recv_slot(k, iy, ix)];
-      }
-    }
-    mm[j] = got;
-    ms[lp] = (uint8_t)got;
-  }
-  __syncthreads();
-  if (t == 0) d.crecv[prv * ns_ + gt] = 0;
-  closure_fixpoint<K>(ms, os, mm);
-  int nw[4], any = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    nw[j] = mm[j] & !m0[j];
-    any |= nw[j];
-  }
-  any = __syncthreads_or(any);
-  if (any) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (nw[j]) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = 1;
-    write_mask(d, io, gt, mm, nw);
-    int sent = closure_send<K>(d, gt, nw, os, cur);
-    sent = __syncthreads_or(sent);
-    if (t == 0 && sent) d.ring[sw & 63] = 1;
-  }
-  GC_WORKLIST_END
-}
-
-// ------------------------------------------------------------------------------ a5 export
-// Forward-arc flows f = c - r of this solve (the next frame's warm start).
-template <int K>
-__global__ void __launch_bounds__(NTH) k_export(Dev d, IO io) {
-  const int tile = blockIdx.x, s = blockIdx.y;
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int H = d.H, W = d.W;
-  const size_t plane = (size_t)H * W;
-  const size_t gt = (size_t)s * d.T + tile;
-  const int err = d.ferr[s];
-  int e[4], r[4][K];
-  get_er<K>(d, io, gt, e, r);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
-    if (y >= H || x >= W) continue;
-    const size_t o = (size_t)y * W + x;
-#pragma unroll
-    for (int k = 0; k < K; k += 2) {
-      const int y2 = y + DYk(k), x2 = x + DXk(k);
-      int f = 0;
-      if (!err && y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = io.nb[s * plane * K + k * plane + o] - r[j][k];
-      io.fstate[s * plane * (K / 2) + (k >> 1) * plane + o] = f;
-    }
-  }
-}
-
-// F = sum c(v,t) - sum max(0, -e): the flow that reached t.
-__global__ void k_flow(Dev d, IO io) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= d.nslot) return;
-  int st = 0;
-  long long F = (long long)d.sumct[s] - (long long)d.sumneg[s];
-  if (d.ferr[s]) { st = 2; F = -1; }
-  else if (!d.fdone[s]) { st = 5; F = -1; }
-  io.flow[s] = F;
-  if (io.stats) {
-    io.stats[s * 4 + 0] = d.fstat[s * 4 + 0];
-    io.stats[s * 4 + 1] = d.fstat[s * 4 + 1];
-    io.stats[s * 4 + 2] = d.fstat[s * 4 + 2];
-    io.stats[s * 4 + 3] = st;
-  }
-  if (st) atomicAdd(&d.ctr[st == 2 ? 1 : 2], 1);
 }
 
 }  // namespace gcb

@@ -15,12 +15,14 @@
 #include <vector>
 
 #include "gc.h"
-#include "gc_kernels.cuh"
+#include "gc_phases.cuh"
 
 using namespace gcb;
 
 struct gc_ctx {
   int dev = 0, K = 4, max_h = 0, max_w = 0, max_batch = 0, rounds = 8, period = 2;
+  double alpha = 1.0;        // global relabel after alpha x (chunk pixels) relabel operations
+  int max_push_phase = 16384;  // push launches per phase, upper bound
   long long max_launches = 1000000;
   size_t pool_bytes = 0;
   char* pool = nullptr;
@@ -54,7 +56,7 @@ size_t frame_bytes(int K, size_t T) {
   b += T * 128 * 4;               // hedge
   b += 2 * T * K * 64 * 4;        // inbox
   b += T * K * 64;                // reach
-  b += T * 8 + 8 * T * 4;         // neg0 + tile flags
+  b += T * 8 + 10 * T * 4;        // neg0 + tile flags
   b += 64;                        // frame words
   return b + 16 * 256;            // alignment slack
 }
@@ -86,20 +88,29 @@ Dev carve(gc_ctx* c, int nslot, int H, int W) {
   d.dirty = (int32_t*)take(2 * ns * 4);
   d.recv = (int32_t*)take(2 * ns * 4);
   d.crecv = (int32_t*)take(2 * ns * 4);
-  // per-frame words: contiguous so one memset clears them
-  char* fw = take((size_t)nslot * (4 + 4 + 16 + 8 + 8) + 64 * 4 + 8 * 4 + 64);
-  d.fdone = (int32_t*)fw;
-  d.ferr = d.fdone + nslot;
-  d.fstat = d.ferr + nslot;
-  d.sumct = (unsigned long long*)align_up((size_t)(d.fstat + 4 * nslot), 8);
-  d.sumneg = d.sumct + nslot;
-  d.ring = (int32_t*)(d.sumneg + nslot);
+  d.tph = (int32_t*)take(ns * 4);
+  // per-frame words: contiguous so one memset clears them (fmode 0 = M_SEED)
+  char* fw = take((size_t)nslot * (4 * 11 + 8 * 4) + 64 * 4 + 8 * 4 + 64);
+  int32_t* w = (int32_t*)fw;
+  d.fmode = w; w += nslot;
+  d.ferr = w; w += nslot;
+  d.fchg = w; w += 2 * nslot;
+  d.fph = w; w += nslot;
+  d.fpush = w; w += nslot;
+  d.fnew = w; w += nslot;
+  d.fstat = w; w += 4 * nslot;
+  unsigned long long* u = (unsigned long long*)align_up((size_t)w, 8);
+  d.fabs_ = u; u += nslot;
+  d.frel = u; u += nslot;
+  d.sumct = u; u += nslot;
+  d.sumneg = u; u += nslot;
+  d.ring = (int32_t*)u;
   d.ctr = d.ring + 64;
   d.ptiles = c->prof ? c->dtiles : nullptr;
   return d;
 }
 
-size_t frame_words_bytes(const Dev& d) { return (char*)(d.ctr + 8) - (char*)d.fdone; }
+size_t frame_words_bytes(const Dev& d) { return (char*)(d.ctr + 8) - (char*)d.fmode; }
 
 bool ck(gc_ctx* c, cudaError_t e, const char* what) {
   if (e == cudaSuccess) return true;
@@ -164,15 +175,15 @@ template <int K>
 gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStream_t st, Launcher& L) {
   Dev d = carve(c, nslot, H, W);
   const dim3 grid(d.T, nslot), blk(NTH);
-  static int g_relax = 0, g_push = 0, g_clos = 0;  // per-K persistent grid sizes (same device)
-  if (!g_relax) {
-    g_relax = persistent_grid(c, k_bfs_relax<K>);
+  static int g_light = 0, g_push = 0;  // per-K persistent grid sizes (B200: same on every device)
+  if (!g_light) {
+    g_light = persistent_grid(c, k_light<K>);
     g_push = persistent_grid(c, k_push<K>);
-    g_clos = persistent_grid(c, k_closure_relax<K>);
   }
   const size_t ns = (size_t)nslot * d.T;
-  auto wgrid = [&](int g) { return (int)((size_t)g < ns ? g : ns); };
-  if (!ck(c, cudaMemsetAsync(d.fdone, 0, frame_words_bytes(d), st), "memset")) return GC_ERR_CUDA;
+  const int gl = (int)((size_t)g_light < ns ? g_light : ns);
+  const int gp = (int)((size_t)g_push < ns ? g_push : ns);
+  if (!ck(c, cudaMemsetAsync(d.fmode, 0, frame_words_bytes(d), st), "memset")) return GC_ERR_CUDA;
   // ---- a1 (int4 loads when every caller row is 16-byte aligned)
   const bool vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
                    ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
@@ -181,74 +192,29 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStre
   else k_init<K, false><<<grid, blk, 0, st>>>(d, io);
   L.post();
   if (!ck(c, cudaGetLastError(), "k_init")) return GC_ERR_CUDA;
-  // ---- a2: first global relabel, seed sweep (reads fl only)
-  L.pre(1);
-  k_bfs_seed<K><<<grid, blk, 0, st>>>(d, io, -1, 0);
-  L.post();
-
-  int push_launches = 0, relabels = 1, sweeps = 1, last_par = -1, sw = 1;
-  const int BATCH = 4;
+  // ---- device-side state machine, one step = light + push + control.
+  // Goldberg's global-relabel heuristic: a push phase ends at the latest after
+  // alpha x (frame pixels) relabel operations.
+  const long long relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
   gc_status status = GC_OK;
-  auto poll = [&](const int32_t* dptr) -> int {
-    cudaMemcpyAsync(c->hpin, dptr, 4, cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    return c->hpin[0];
-  };
-  for (;;) {
-    // ---- a2: relax sweeps of the global relabel until no border height changes
-    for (;;) {
-      for (int b = 0; b < BATCH; ++b) {
-        L.pre(1);
-        k_bfs_relax<K><<<wgrid(g_relax), blk, 0, st>>>(d, sw);
-        L.post();
-        ++sw; ++sweeps;
-      }
-      if (!ck(c, cudaGetLastError(), "k_bfs_relax")) return GC_ERR_CUDA;
-      if (!poll(d.ring + ((sw - 1) & 63))) break;
-      if (L.n > c->max_launches) { status = GC_ERR_NOCONV; break; }
-    }
-    if (status == GC_ERR_NOCONV) break;  // labels not final: leave unfinished frames not-done
-    // ---- status: done frames have no active node reaching the sink
-    cudaMemsetAsync(d.ctr, 0, 4, st);
-    L.pre(3);
-    k_status<<<nslot, NTH, 0, st>>>(d, push_launches, relabels, sweeps);
-    L.post();
-    if (!poll(d.ctr)) break;
-    if (L.n > c->max_launches) { status = GC_ERR_NOCONV; break; }
-    // ---- a3: push launches
-    for (int j = 0; j < c->period; ++j) {
-      const int par_out = push_launches & 1;
-      const int par_in = (j == 0) ? -1 : (par_out ^ 1);
-      L.pre(2);
-      k_push<K><<<wgrid(g_push), blk, 0, st>>>(d, io, par_in, par_out, c->rounds);
-      L.post();
-      ++push_launches;
-      last_par = par_out;
-    }
-    if (!ck(c, cudaGetLastError(), "k_push")) return GC_ERR_CUDA;
-    // ---- a2: next global relabel, seed sweep
+  int next_poll = 8;
+  for (int sw = 0;; ++sw) {
     L.pre(1);
-    k_bfs_seed<K><<<grid, blk, 0, st>>>(d, io, last_par, sw);
+    k_light<K><<<gl, blk, 0, st>>>(d, io, sw);
     L.post();
-    last_par = -1;
-    ++sw; ++sweeps; ++relabels;
-  }
-  // ---- a4: canonical mask (+ the flow value's sum over e)
-  L.pre(4);
-  k_closure_seed<K><<<grid, blk, 0, st>>>(d, io, sw);
-  L.post();
-  ++sw;
-  if (poll(d.ring + ((sw - 1) & 63))) {
-    for (;;) {
-      for (int b = 0; b < BATCH; ++b) {
-        L.pre(4);
-        k_closure_relax<K><<<wgrid(g_clos), blk, 0, st>>>(d, io, sw);
-        L.post();
-        ++sw;
-      }
-      if (!ck(c, cudaGetLastError(), "k_closure_relax")) return GC_ERR_CUDA;
-      if (!poll(d.ring + ((sw - 1) & 63))) break;
-    }
+    L.pre(2);
+    k_push<K><<<gp, blk, 0, st>>>(d, io, sw, c->rounds);
+    L.post();
+    L.pre(3);
+    k_control<<<nslot, NTH, 0, st>>>(d, sw, relabel_budget, c->max_push_phase);
+    L.post();
+    if (sw + 1 < next_poll) continue;
+    if (!ck(c, cudaGetLastError(), "step")) return GC_ERR_CUDA;
+    cudaMemcpyAsync(c->hpin, d.ring + (sw & 63), 4, cudaMemcpyDeviceToHost, st);
+    if (!ck(c, cudaStreamSynchronize(st), "step sync")) return GC_ERR_CUDA;
+    if (c->hpin[0] == 0) break;  // every frame done
+    if (L.n > c->max_launches) { status = GC_ERR_NOCONV; break; }
+    next_poll = sw + 1 + (sw < 64 ? 4 : (sw < 1024 ? 16 : 64));
   }
   if (io.fstate) {
     L.pre(5);
@@ -265,6 +231,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStre
   if (c->hpin[2] || status == GC_ERR_NOCONV) return GC_ERR_NOCONV;
   return GC_OK;
 }
+
 
 gc_status check_batch(gc_ctx* c, const gc_batch* b) {
   if (!c) return GC_ERR_ARG;
@@ -320,6 +287,8 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   c->period = g.relabel_period > 0 ? g.relabel_period : 2;
   c->max_launches = g.max_launches > 0 ? g.max_launches : 1000000;
   c->max_batch = g.max_batch > 0 ? g.max_batch : 0;
+  if (const char* ev = getenv("GC_ALPHA")) c->alpha = atof(ev);          // tuning knobs
+  if (const char* ev = getenv("GC_MAX_PUSH")) c->max_push_phase = atoi(ev);
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
   if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
   const size_t fb = frame_bytes(c->K, tiles_of(c->max_h, c->max_w));
