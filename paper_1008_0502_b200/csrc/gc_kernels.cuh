@@ -63,8 +63,13 @@ struct Dev {
   int32_t* recv;    // [2][NS] tile has inbound flow in inbox of that parity
   int32_t* crecv;   // [2][NS] tile received new reach bits in the closure sweep of that parity
   int32_t* tph;     // [NS]   push-phase stamp of the last push that touched the tile
-  // per frame (state machine): all zero-initialised by one memset
-  int32_t* fmode;   // [nslot] M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_DONE
+  // per frame slot (state machine): zero-initialised by one memset
+  int32_t* fmode;   // [nslot] M_INIT, M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_EXPORT, M_IDLE
+  int32_t* sfr;     // [nslot] batch frame index held by the slot
+  int32_t* fstall;  // [nslot] consecutive push steps without progress
+  int32_t* gctr;    // [4] next frame to start, frames finished, range-error frames, -
+  int32_t* slist;   // [2][4][nslot] slots of each kernel group for the step of that parity
+  int32_t* lcnt;    // [2][4] list lengths
   int32_t* ferr;    // [nslot] capacity out of range
   int32_t* fchg;    // [2][nslot] something changed in the step of that parity (BFS / closure)
   int32_t* fph;     // [nslot] global relabels so far (push-phase id)
@@ -80,7 +85,7 @@ struct Dev {
   unsigned long long* ptiles;  // [6] tiles processed per kernel class (profiling only, else NULL)
 };
 
-enum { M_SEED = 0, M_BFS = 1, M_PUSH = 2, M_CSEED = 3, M_CLOS = 4, M_DONE = 5 };
+enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_EXPORT = 6, M_IDLE = 7 };
 
 struct IO {
   const int32_t* cs;
@@ -182,10 +187,11 @@ __device__ __forceinline__ void tile_from_caps(const Dev& d, const IO& io, int s
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
-  const int32_t* cs = io.cs + s * plane;
-  const int32_t* ct = io.ct + s * plane;
-  const int32_t* nb = io.nb + s * plane * K;
-  const int32_t* wf = io.wf ? io.wf + s * plane * (K / 2) : nullptr;
+  const size_t f = (size_t)d.sfr[s];  // batch frame held by this slot
+  const int32_t* cs = io.cs + f * plane;
+  const int32_t* ct = io.ct + f * plane;
+  const int32_t* nb = io.nb + f * plane * K;
+  const int32_t* wf = io.wf ? io.wf + f * plane * (K / 2) : nullptr;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
@@ -345,27 +351,25 @@ __device__ __forceinline__ int bfs_seed_tile(const Dev& d, size_t gt, int* hs, c
 // 2-byte fl word per pixel, the frame's sum c(v,t), the tile's sum max(0,-e) and the
 // range flag.  Thread t owns 4 consecutive pixels of row t/8 (int4 loads when the caller's
 // rows are 16-byte aligned).
-template <int K, bool VEC>
-__global__ void __launch_bounds__(NTH) k_init(Dev d, IO io) {
-  const int tile = blockIdx.x, s = blockIdx.y;
+template <int K>
+__device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt, bool vec, long long (*red)[NTH / 32]) {
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
-  const size_t gt = (size_t)s * d.T + tile;
   const size_t ns = NS(d);
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
-  count_tile(d, 0);
-  __shared__ long long red[2][NTH / 32];
-  const int32_t* cs = io.cs + s * plane;
-  const int32_t* ct = io.ct + s * plane;
-  const int32_t* nb = io.nb + s * plane * K;
-  const int32_t* wf = io.wf ? io.wf + s * plane * (K / 2) : nullptr;
+  const size_t fr = (size_t)d.sfr[s];  // batch frame held by this slot
+  const int32_t* cs = io.cs + fr * plane;
+  const int32_t* ct = io.ct + fr * plane;
+  const int32_t* nb = io.nb + fr * plane * K;
+  const int32_t* wf = io.wf ? io.wf + fr * plane * (K / 2) : nullptr;
   const int y = ty * TS + iy, x0 = tx * TS + ix0;
   int bad = 0;
   long long sct = 0, neg = 0;
   int a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0}, c[K][4];
   const size_t o0 = (size_t)y * W + x0;
-  const bool full = VEC && y < H && x0 + 3 < W;
+  const bool full = vec && y < H && x0 + 3 < W;
   if (full) {
     const int4 va = __ldg(reinterpret_cast<const int4*>(cs + o0));
     const int4 vb = __ldg(reinterpret_cast<const int4*>(ct + o0));
@@ -451,6 +455,7 @@ __global__ void __launch_bounds__(NTH) k_init(Dev d, IO io) {
     d.tph[gt] = -1;
     if (bad) d.ferr[s] = 1;
   }
+  __syncthreads();
 }
 
 }  // namespace gcb

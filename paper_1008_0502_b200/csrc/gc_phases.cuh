@@ -1,24 +1,39 @@
 // gc_phases.cuh -- the per-step kernels of the device-side solve loop.
 //
-// Every frame of a chunk runs its own state machine (d.fmode), advanced once per step by
-// k_control:
-//   M_SEED  -- global relabel, seed pass: absorb in-flight flow, h = 1 on nodes with
-//              residual capacity to t, tile-local BFS fixpoint            (a2)
-//   M_BFS   -- global relabel, relax passes over tiles whose neighbours' border heights
-//              changed; ends when a step changes nothing (exact BFS distances)  (a2)
-//              then: no active node left -> M_CSEED, else -> M_PUSH
-//   M_PUSH  -- push/relabel launches over active tiles (a3); ends (-> M_SEED) when a step
-//              neither delivers flow to sink-connected nodes nor reaches new tiles, or
-//              the relabel budget of Goldberg's global-relabel heuristic is spent
-//   M_CSEED -- canonical mask, seed pass over every tile; writes the caller's mask (a4)
-//   M_CLOS  -- mask closure across tile borders until nothing changes      (a4)
-//   M_DONE
-// One step = k_light (SEED/BFS/CSEED/CLOS tiles) + k_push (PUSH tiles) + k_control.  All
-// parities (dirty, inbox, reach flags) follow the global step counter sw.
+// The context holds `nslot` frame slots.  Every slot runs its own state machine (d.fmode),
+// advanced once per step by k_control; a slot whose frame finishes is refilled with the next
+// frame of the batch on the device (continuous batching), so easy and hard frames never wait
+// for each other:
+//   M_INIT   -- streaming pass over the caps: fl bit-planes, sum c(v,t), range check (a1/a1w)
+//   M_SEED   -- global relabel, seed pass: absorb in-flight flow, h = 1 on nodes with
+//               residual capacity to t, tile-local BFS fixpoint                     (a2)
+//   M_BFS    -- global relabel, relax passes over tiles whose neighbours' border heights
+//               changed; ends when a step changes nothing (exact BFS distances)      (a2)
+//               then: no active node left -> M_CSEED, else -> M_PUSH
+//   M_PUSH   -- push/relabel over active tiles (a3); ends (-> M_SEED) when the frame stops
+//               delivering flow to sink-connected nodes and reaching new tiles, or when the
+//               relabel budget of Goldberg's global-relabel heuristic is spent
+//   M_CSEED  -- canonical mask, seed pass over every tile; writes the caller's mask    (a4)
+//   M_CLOS   -- mask closure across tile borders until nothing changes               (a4)
+//   M_EXPORT -- forward-arc flows for the caller's warm-start state                 (a5)
+//   then the flow value is written and the slot takes the next frame (M_INIT) or idles.
+// One step = k_stream (INIT/EXPORT) + k_seed (SEED/CSEED) + k_relax (BFS/CLOS) + k_push
+// (PUSH) + k_control.  Each kernel walks the compact list of slots of its group that
+// k_control built for this step.  Parities (dirty, inbox, reach flags) follow the global
+// step counter sw.
 #pragma once
 #include "gc_kernels.cuh"
 
 namespace gcb {
+
+enum { G_STREAM = 0, G_SEED = 1, G_RELAX = 2, G_PUSH = 3, NGROUP = 4 };
+
+__host__ __device__ __forceinline__ int mode_group(int md) {
+  return (md == M_INIT || md == M_EXPORT) ? G_STREAM
+         : (md == M_SEED || md == M_CSEED) ? G_SEED
+         : (md == M_BFS || md == M_CLOS)   ? G_RELAX
+                                           : G_PUSH;
+}
 
 // Mark the neighbour tiles that read a changed part of this tile's border.
 __device__ __forceinline__ void mark_neighbours(const Dev& d, int32_t* flags, size_t gt, int bits, int K) {
@@ -47,27 +62,38 @@ __device__ __forceinline__ int border_bits(int iy, int ix) {
   return b;
 }
 
-// Persistent-grid worklist: each CTA scans tiles blockIdx.x, +gridDim.x, ... 256 at a time,
-// compacts the flagged ones in shared memory and processes them one by one.
-#define GC_WORKLIST_BEGIN(PRED)                                                      \
-  __shared__ int wl_[NTH];                                                           \
-  __shared__ int wn_;                                                                \
-  const size_t ns_ = NS(d);                                                          \
-  for (size_t base_ = 0; base_ < ns_; base_ += (size_t)NTH * gridDim.x) {            \
-    const size_t id = base_ + (size_t)threadIdx.x * gridDim.x + blockIdx.x;          \
-    int want_ = 0;                                                                   \
-    if (id < ns_) want_ = (PRED);                                                    \
-    if (threadIdx.x == 0) wn_ = 0;                                                   \
-    __syncthreads();                                                                 \
-    if (want_) wl_[atomicAdd(&wn_, 1)] = (int)id;                                    \
-    __syncthreads();                                                                 \
-    const int n_ = wn_;                                                              \
-    for (int i_ = 0; i_ < n_; ++i_) {                                                \
-      const size_t gt = (size_t)wl_[i_];
-#define GC_WORKLIST_END \
-  __syncthreads();      \
-  }                     \
-  __syncthreads();      \
+// Persistent-grid worklist over the tiles of the slots listed for group G in this step:
+// each CTA takes ids blockIdx.x, +gridDim.x, ... 256 at a time, compacts those passing
+// TILEPRED in shared memory and processes them one by one (block-wide body).
+#define GC_LIST_BEGIN(G, TILEPRED)                                                        \
+  __shared__ int wl_[NTH];                                                                \
+  __shared__ int wn_;                                                                     \
+  const size_t ns_ = NS(d);                                                               \
+  const int lb_ = sw & 1;                                                                 \
+  const int cnt_ = d.lcnt[lb_ * NGROUP + (G)];                                            \
+  const int* sl_ = d.slist + ((size_t)lb_ * NGROUP + (G)) * d.nslot;                      \
+  const size_t tot_ = (size_t)cnt_ * d.T;                                                 \
+  for (size_t base_ = 0; base_ < tot_; base_ += (size_t)NTH * gridDim.x) {                \
+    const size_t k_ = base_ + (size_t)threadIdx.x * gridDim.x + blockIdx.x;               \
+    int want_ = 0;                                                                        \
+    size_t id = 0;                                                                        \
+    if (k_ < tot_) {                                                                      \
+      const int li_ = (int)(k_ / d.T);                                                    \
+      id = (size_t)sl_[li_] * d.T + (k_ - (size_t)li_ * d.T);                             \
+      want_ = (TILEPRED);                                                                 \
+    }                                                                                     \
+    if (threadIdx.x == 0) wn_ = 0;                                                        \
+    __syncthreads();                                                                      \
+    if (want_) wl_[atomicAdd(&wn_, 1)] = (int)id;                                         \
+    __syncthreads();                                                                      \
+    const int n_ = wn_;                                                                   \
+    for (int i_ = 0; i_ < n_; ++i_) {                                                     \
+      const size_t gt = (size_t)wl_[i_];                                                  \
+      const int md = d.fmode[gt / d.T];
+#define GC_LIST_END \
+  __syncthreads();  \
+  }                 \
+  __syncthreads();  \
   }
 
 // ---------------------------------------------------------------- a2: seed pass (one tile)
@@ -209,10 +235,11 @@ __device__ __forceinline__ void write_mask(const Dev& d, const IO& io, size_t gt
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const size_t plane = (size_t)d.H * d.W;
+  uint8_t* mask = io.mask + (size_t)d.sfr[s] * plane;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
-    if (wr[j] && y < d.H && x < d.W) io.mask[s * plane + (size_t)y * d.W + x] = (uint8_t)mm[j];
+    if (wr[j] && y < d.H && x < d.W) mask[(size_t)y * d.W + x] = (uint8_t)mm[j];
   }
 }
 
@@ -314,46 +341,91 @@ __device__ __forceinline__ void tile_crelax(const Dev& d, const IO& io, size_t g
   }
 }
 
-// ---------------------------------------------------------------- k_light
-// The light phases (seed, relax, closure seed, closure relax) of every frame in one
-// persistent launch: a tile is listed if its frame's mode needs it this step.
+// ---------------------------------------------------------------- a5: export (one tile)
+// Forward-arc flows f = c - r of this solve (the next frame's warm start).
 template <int K>
-__global__ void __launch_bounds__(NTH) k_light(Dev d, IO io, int sw) {
+__device__ __forceinline__ void tile_export(const Dev& d, const IO& io, size_t gt) {
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  const int H = d.H, W = d.W;
+  const size_t plane = (size_t)H * W;
+  const size_t fr = (size_t)d.sfr[s];
+  int e[4], r[4][K];
+  get_er<K>(d, io, gt, e, r);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
+    if (y >= H || x >= W) continue;
+    const size_t o = (size_t)y * W + x;
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+      const int y2 = y + DYk(k), x2 = x + DXk(k);
+      int f = 0;
+      if (y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = io.nb[fr * plane * K + k * plane + o] - r[j][k];
+      io.fstate[fr * plane * (K / 2) + (k >> 1) * plane + o] = f;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- step kernels
+template <int K>
+__global__ void __launch_bounds__(NTH) k_stream(Dev d, IO io, int sw, int vec) {
+  __shared__ long long red[2][NTH / 32];
+  GC_LIST_BEGIN(G_STREAM, 1)
+  if (md == M_INIT) {
+    count_tile(d, 0);
+    tile_init<K>(d, io, gt, vec != 0, red);
+  } else {
+    count_tile(d, 5);
+    tile_export<K>(d, io, gt);
+  }
+  GC_LIST_END
+}
+
+template <int K>
+__global__ void __launch_bounds__(NTH) k_seed(Dev d, IO io, int sw) {
   __shared__ int hs[HS * HS];
-  __shared__ int bits_s;
   __shared__ long long red[NTH / 32];
   uint8_t* ms = reinterpret_cast<uint8_t*>(hs);  // closure tiles reuse the height buffer
   uint8_t* os = ms + TPX;
-  const int prv = (sw & 1) ^ 1;
-  GC_WORKLIST_BEGIN(([&]() {
-    const int md = d.fmode[id / d.T];
-    return (md == M_SEED) || (md == M_CSEED) || (md == M_BFS && d.dirty[prv * ns_ + id]) ||
-           (md == M_CLOS && d.crecv[prv * ns_ + id]);
-  })())
-  const int md = d.fmode[gt / d.T];
+  GC_LIST_BEGIN(G_SEED, 1)
   if (md == M_SEED) {
     count_tile(d, 1);
     tile_seed<K>(d, io, gt, sw, hs);
-  } else if (md == M_BFS) {
-    count_tile(d, 1);
-    tile_relax<K>(d, gt, sw, hs, &bits_s);
-  } else if (md == M_CSEED) {
+  } else {
     count_tile(d, 4);
     tile_cseed<K>(d, io, gt, sw, ms, os, red);
+  }
+  GC_LIST_END
+}
+
+template <int K>
+__global__ void __launch_bounds__(NTH) k_relax(Dev d, IO io, int sw) {
+  __shared__ int hs[HS * HS];
+  __shared__ int bits_s;
+  uint8_t* ms = reinterpret_cast<uint8_t*>(hs);
+  uint8_t* os = ms + TPX;
+  const int prv = (sw & 1) ^ 1;
+  GC_LIST_BEGIN(G_RELAX, (d.fmode[id / d.T] == M_BFS ? d.dirty[prv * ns_ + id] : d.crecv[prv * ns_ + id]))
+  if (md == M_BFS) {
+    count_tile(d, 1);
+    tile_relax<K>(d, gt, sw, hs, &bits_s);
   } else {
     count_tile(d, 4);
     tile_crelax<K>(d, io, gt, sw, ms, os);
   }
-  GC_WORKLIST_END
+  GC_LIST_END
 }
 
 // ---------------------------------------------------------------- a3: k_push
 // Up to `rounds` synchronous push / gather / relabel rounds inside each active tile (or
-// tile with inbound flow) of the frames in M_PUSH.  Pushes are decided by the owner (it
-// lowers its own e and r); receivers inside the tile gather them in a separate phase;
-// pushes across the tile border go to the receiver tile's inbox and are absorbed at its
-// next step.  Border heights are those of the previous step (stale); the exact global
-// relabel restores valid labels and certifies termination.
+// tile with inbound flow) of the slots in M_PUSH (4x the rounds once a push phase has run
+// 8 steps: long-distance transport).  Pushes are decided by the owner (it lowers its own e
+// and r); receivers inside the tile gather them in a separate phase; pushes across the tile
+// border go to the receiver tile's inbox and are absorbed at its next step.  Border heights
+// are those of the previous step (stale); the exact global relabel restores valid labels
+// and certifies termination.
 template <int K>
 __global__ void __launch_bounds__(NTH) k_push(Dev d, IO io, int sw, int rounds) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
@@ -362,11 +434,13 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, IO io, int sw, int rounds) 
   __shared__ int oacc[K][64];
   const int hmax = d.hmax;
   const int par_out = sw & 1, par_in = par_out ^ 1;
-  GC_WORKLIST_BEGIN(d.fmode[id / d.T] == M_PUSH && (d.tact[id] || d.recv[par_in * ns_ + id]))
+  GC_LIST_BEGIN(G_PUSH, (d.tact[id] || d.recv[par_in * ns_ + id]))
+  (void)md;
   count_tile(d, 2);
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int rcv = d.recv[par_in * ns_ + gt];
+  const int nround = d.fpush[s] >= 8 ? 4 * rounds : rounds;
   int e[4], r[4][K], h[4];
   get_er<K>(d, io, gt, e, r);
   long long neg0 = 0;
@@ -386,7 +460,7 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, IO io, int sw, int rounds) 
   for (int i = t; i < K * 64; i += NTH) (&oacc[0][0])[i] = 0;
   __syncthreads();
   int nrel = 0;  // relabel operations (global-relabel heuristic, k_control)
-  for (int rd = 0; rd < rounds; ++rd) {
+  for (int rd = 0; rd < nround; ++rd) {
     // push phase (owner)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -506,16 +580,35 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, IO io, int sw, int rounds) 
       atomicAdd(&d.fnew[s], 1);
     }
   }
-  GC_WORKLIST_END
+  GC_LIST_END
 }
 
 // ---------------------------------------------------------------- k_control
-// Advances every frame's state machine after a step (one CTA per frame).
-__global__ void __launch_bounds__(NTH) k_control(Dev d, int sw, long long relabel_budget, int max_push) {
+// Advances every slot's state machine after a step (one CTA per slot), finishes frames
+// (flow value, stats), refills finished slots with the next frame, and builds the slot
+// lists of the next step.  F = sum c(v,t) - sum max(0,-e): the flow that reached t.
+__device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s) {
+  const int f = d.sfr[s];
+  int st = 0;
+  long long F = (long long)d.sumct[s] - (long long)d.sumneg[s];
+  if (d.ferr[s]) { st = 2; F = -1; atomicAdd(&d.gctr[2], 1); }
+  io.flow[f] = F;
+  if (io.stats) {
+    io.stats[f * 4 + 0] = d.fstat[s * 4 + 0];
+    io.stats[f * 4 + 1] = d.fstat[s * 4 + 1];
+    io.stats[f * 4 + 2] = d.fstat[s * 4 + 2];
+    io.stats[f * 4 + 3] = st;
+  }
+  atomicAdd(&d.gctr[1], 1);
+}
+
+__global__ void __launch_bounds__(NTH) k_control(Dev d, IO io, int sw, long long relabel_budget, int max_push,
+                                                 int nframes) {
   const int s = blockIdx.x, t = threadIdx.x;
   const int cur = sw & 1, nxt = cur ^ 1;
-  if (s == 0 && t == 0) d.ring[(sw + 1) & 63] = 0;
+  if (s == 0 && t < NGROUP) d.lcnt[cur * NGROUP + t] = 0;  // this step's lists are consumed
   const int md = d.fmode[s];
+  if (md == M_IDLE) return;
   const int chg = d.fchg[cur * d.nslot + s];
   int nact = 0;
   if (md == M_BFS && !chg) {  // relabel converged: any active node left that reaches t?
@@ -525,8 +618,9 @@ __global__ void __launch_bounds__(NTH) k_control(Dev d, int sw, long long relabe
   if (t != 0) return;
   int nm = md;
   int* st = d.fstat + s * 4;
-  if (d.ferr[s] && md != M_CSEED && md != M_DONE) {
-    nm = M_CSEED;
+  bool finished = false;
+  if (md == M_INIT) {
+    nm = d.ferr[s] ? M_CSEED : M_SEED;
   } else if (md == M_SEED) {
     nm = M_BFS;
     st[1] += 1;
@@ -536,6 +630,7 @@ __global__ void __launch_bounds__(NTH) k_control(Dev d, int sw, long long relabe
       if (nact) {
         nm = M_PUSH;
         d.fpush[s] = 0;
+        d.fstall[s] = 0;
         d.frel[s] = 0;
         d.fabs_[s] = 0;
         d.fnew[s] = 0;
@@ -547,65 +642,68 @@ __global__ void __launch_bounds__(NTH) k_control(Dev d, int sw, long long relabe
   } else if (md == M_PUSH) {
     st[0] += 1;
     const int np = ++d.fpush[s];
-    const unsigned long long absorbed = d.fabs_[s];
-    const int fresh = d.fnew[s];
+    const bool stalled = d.fabs_[s] == 0 && d.fnew[s] == 0;
     d.fabs_[s] = 0;
     d.fnew[s] = 0;
-    const bool stalled = absorbed == 0 && fresh == 0;
-    if (stalled || d.frel[s] > (unsigned long long)relabel_budget || np >= max_push) nm = M_SEED;
+    const int stall = stalled ? ++d.fstall[s] : (d.fstall[s] = 0);
+    if (stall >= 1 + np / 4 || d.frel[s] > (unsigned long long)relabel_budget || np >= max_push) nm = M_SEED;
   } else if (md == M_CSEED || md == M_CLOS) {
-    nm = chg ? M_CLOS : M_DONE;
+    if (chg) nm = M_CLOS;
+    else if (io.fstate && !d.ferr[s]) nm = M_EXPORT;
+    else finished = true;
+  } else if (md == M_EXPORT) {
+    finished = true;
+  }
+  if (finished) {
+    finish_frame(d, io, s);
+    const int nf = atomicAdd(&d.gctr[0], 1);
+    if (nf < nframes) {  // refill the slot with the next frame of the batch
+      d.sfr[s] = nf;
+      d.ferr[s] = 0;
+      d.fph[s] = 0; d.fpush[s] = 0; d.fnew[s] = 0; d.fstall[s] = 0;
+      d.fchg[cur * d.nslot + s] = 0;
+      st[0] = st[1] = st[2] = st[3] = 0;
+      d.fabs_[s] = 0; d.frel[s] = 0; d.sumct[s] = 0; d.sumneg[s] = 0;
+      nm = M_INIT;
+    } else {
+      nm = M_IDLE;
+    }
   }
   d.fmode[s] = nm;
   d.fchg[nxt * d.nslot + s] = 0;
-  if (nm != M_DONE) atomicAdd(&d.ring[sw & 63], 1);
-}
-
-// ---------------------------------------------------------------- a5: export
-// Forward-arc flows f = c - r of this solve (the next frame's warm start).
-template <int K>
-__global__ void __launch_bounds__(NTH) k_export(Dev d, IO io) {
-  const int tile = blockIdx.x, s = blockIdx.y;
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int H = d.H, W = d.W;
-  const size_t plane = (size_t)H * W;
-  const size_t gt = (size_t)s * d.T + tile;
-  const int err = d.ferr[s];
-  count_tile(d, 5);
-  int e[4], r[4][K];
-  get_er<K>(d, io, gt, e, r);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
-    if (y >= H || x >= W) continue;
-    const size_t o = (size_t)y * W + x;
-#pragma unroll
-    for (int k = 0; k < K; k += 2) {
-      const int y2 = y + DYk(k), x2 = x + DXk(k);
-      int f = 0;
-      if (!err && y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = io.nb[s * plane * K + k * plane + o] - r[j][k];
-      io.fstate[s * plane * (K / 2) + (k >> 1) * plane + o] = f;
-    }
+  if (nm != M_IDLE) {
+    const int g = mode_group(nm);
+    const int pos = atomicAdd(&d.lcnt[nxt * NGROUP + g], 1);
+    d.slist[((size_t)nxt * NGROUP + g) * d.nslot + pos] = s;
   }
 }
 
-// F = sum c(v,t) - sum max(0, -e): the flow that reached t.
-__global__ void k_flow(Dev d, IO io) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= d.nslot) return;
-  int st = 0;
-  long long F = (long long)d.sumct[s] - (long long)d.sumneg[s];
-  if (d.ferr[s]) { st = 2; F = -1; }
-  else if (d.fmode[s] != M_DONE) { st = 5; F = -1; }
-  io.flow[s] = F;
-  if (io.stats) {
-    io.stats[s * 4 + 0] = d.fstat[s * 4 + 0];
-    io.stats[s * 4 + 1] = d.fstat[s * 4 + 1];
-    io.stats[s * 4 + 2] = d.fstat[s * 4 + 2];
-    io.stats[s * 4 + 3] = st;
+// Initial slot assignment: slot s holds frame s, all slots in M_INIT (listed for step 0).
+__global__ void k_setup(Dev d, int nframes) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < d.nslot; s += gridDim.x * blockDim.x) {
+    d.sfr[s] = s;
+    d.fmode[s] = M_INIT;
+    d.slist[G_STREAM * d.nslot + s] = s;  // list buffer 0, group STREAM
   }
-  if (st) atomicAdd(&d.ctr[st == 2 ? 1 : 2], 1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    d.lcnt[G_STREAM] = d.nslot;
+    d.gctr[0] = d.nslot;
+  }
+}
+
+// max_launches exceeded: frames not finished get F = -1, status GC_ERR_NOCONV.
+__global__ void k_abort(Dev d, IO io, int nframes) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < d.nslot; s += gridDim.x * blockDim.x) {
+    if (d.fmode[s] == M_IDLE) continue;
+    const int f = d.sfr[s];
+    io.flow[f] = -1;
+    if (io.stats) io.stats[f * 4 + 3] = 5;
+  }
+  const int first = d.gctr[0];
+  for (int f = first + blockIdx.x * blockDim.x + threadIdx.x; f < nframes; f += gridDim.x * blockDim.x) {
+    io.flow[f] = -1;
+    if (io.stats) io.stats[f * 4 + 3] = 5;
+  }
 }
 
 }  // namespace gcb

@@ -57,7 +57,7 @@ size_t frame_bytes(int K, size_t T) {
   b += 2 * T * K * 64 * 4;        // inbox
   b += T * K * 64;                // reach
   b += T * 8 + 10 * T * 4;        // neg0 + tile flags
-  b += 64;                        // frame words
+  b += 4 * 2 * 4 + 96;            // frame words + slot lists
   return b + 16 * 256;            // alignment slack
 }
 
@@ -90,9 +90,14 @@ Dev carve(gc_ctx* c, int nslot, int H, int W) {
   d.crecv = (int32_t*)take(2 * ns * 4);
   d.tph = (int32_t*)take(ns * 4);
   // per-frame words: contiguous so one memset clears them (fmode 0 = M_SEED)
-  char* fw = take((size_t)nslot * (4 * 11 + 8 * 4) + 64 * 4 + 8 * 4 + 64);
+  char* fw = take((size_t)nslot * (4 * 13 + 4 * 2 * NGROUP + 8 * 4) + 64 * 4 + 8 * 4 + 4 * 2 * NGROUP + 64);
   int32_t* w = (int32_t*)fw;
   d.fmode = w; w += nslot;
+  d.sfr = w; w += nslot;
+  d.fstall = w; w += nslot;
+  d.slist = w; w += 2 * NGROUP * nslot;
+  d.lcnt = w; w += 2 * NGROUP;
+  d.gctr = w; w += 4;
   d.ferr = w; w += nslot;
   d.fchg = w; w += 2 * nslot;
   d.fph = w; w += nslot;
@@ -171,64 +176,76 @@ int persistent_grid(gc_ctx* c, F kernel) {
   return sms * per;
 }
 
+int chunk_frames(gc_ctx* c, int H, int W) {
+  const size_t fb = frame_bytes(c->K, tiles_of(H, W));
+  size_t n = c->pool_bytes / fb;
+  if (n < 1) n = 1;
+  if (c->max_batch > 0 && n > (size_t)c->max_batch) n = c->max_batch;
+  const char* env = getenv("GC_CHUNK");
+  if (env && atoi(env) > 0 && (size_t)atoi(env) < n) n = atoi(env);
+  return (int)n;
+}
+
+// Solve `nframes` frames of geometry H x W with the slots the pool holds: slots are refilled
+// on the device as frames finish (continuous batching).
 template <int K>
-gc_status solve_chunk(gc_ctx* c, const IO& io, int nslot, int H, int W, cudaStream_t st, Launcher& L) {
+gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaStream_t st, Launcher& L) {
+  const int nslot = chunk_frames(c, H, W) < nframes ? chunk_frames(c, H, W) : nframes;
   Dev d = carve(c, nslot, H, W);
-  const dim3 grid(d.T, nslot), blk(NTH);
-  static int g_light = 0, g_push = 0;  // per-K persistent grid sizes (B200: same on every device)
-  if (!g_light) {
-    g_light = persistent_grid(c, k_light<K>);
+  static int g_stream = 0, g_seed = 0, g_relax = 0, g_push = 0;  // per-K persistent grid sizes
+  if (!g_stream) {
+    g_stream = persistent_grid(c, k_stream<K>);
+    g_seed = persistent_grid(c, k_seed<K>);
+    g_relax = persistent_grid(c, k_relax<K>);
     g_push = persistent_grid(c, k_push<K>);
   }
   const size_t ns = (size_t)nslot * d.T;
-  const int gl = (int)((size_t)g_light < ns ? g_light : ns);
-  const int gp = (int)((size_t)g_push < ns ? g_push : ns);
+  auto cap = [&](int g) { return (int)((size_t)g < ns ? g : ns); };
+  const dim3 blk(NTH);
   if (!ck(c, cudaMemsetAsync(d.fmode, 0, frame_words_bytes(d), st), "memset")) return GC_ERR_CUDA;
-  // ---- a1 (int4 loads when every caller row is 16-byte aligned)
-  const bool vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
-                   ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
-  L.pre(0);
-  if (vec) k_init<K, true><<<grid, blk, 0, st>>>(d, io);
-  else k_init<K, false><<<grid, blk, 0, st>>>(d, io);
-  L.post();
-  if (!ck(c, cudaGetLastError(), "k_init")) return GC_ERR_CUDA;
-  // ---- device-side state machine, one step = light + push + control.
+  k_setup<<<(nslot + NTH - 1) / NTH, NTH, 0, st>>>(d, nframes);
+  ++L.n;
+  // int4 loads in the init pass when every caller row is 16-byte aligned
+  const int vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
+                  ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
   // Goldberg's global-relabel heuristic: a push phase ends at the latest after
   // alpha x (frame pixels) relabel operations.
   const long long relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
   gc_status status = GC_OK;
   int next_poll = 8;
   for (int sw = 0;; ++sw) {
+    L.pre(0);
+    k_stream<K><<<cap(g_stream), blk, 0, st>>>(d, io, sw, vec);
+    L.post();
     L.pre(1);
-    k_light<K><<<gl, blk, 0, st>>>(d, io, sw);
+    k_seed<K><<<cap(g_seed), blk, 0, st>>>(d, io, sw);
+    L.post();
+    L.pre(4);
+    k_relax<K><<<cap(g_relax), blk, 0, st>>>(d, io, sw);
     L.post();
     L.pre(2);
-    k_push<K><<<gp, blk, 0, st>>>(d, io, sw, c->rounds);
+    k_push<K><<<cap(g_push), blk, 0, st>>>(d, io, sw, c->rounds);
     L.post();
     L.pre(3);
-    k_control<<<nslot, NTH, 0, st>>>(d, sw, relabel_budget, c->max_push_phase);
+    k_control<<<nslot, NTH, 0, st>>>(d, io, sw, relabel_budget, c->max_push_phase, nframes);
     L.post();
     if (sw + 1 < next_poll) continue;
     if (!ck(c, cudaGetLastError(), "step")) return GC_ERR_CUDA;
-    cudaMemcpyAsync(c->hpin, d.ring + (sw & 63), 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(c->hpin, d.gctr, 16, cudaMemcpyDeviceToHost, st);
     if (!ck(c, cudaStreamSynchronize(st), "step sync")) return GC_ERR_CUDA;
-    if (c->hpin[0] == 0) break;  // every frame done
-    if (L.n > c->max_launches) { status = GC_ERR_NOCONV; break; }
+    if (c->hpin[1] >= nframes) break;  // every frame finished
+    if (L.n > c->max_launches) {
+      k_abort<<<(nslot + NTH - 1) / NTH, NTH, 0, st>>>(d, io, nframes);
+      ++L.n;
+      status = GC_ERR_NOCONV;
+      break;
+    }
     next_poll = sw + 1 + (sw < 64 ? 4 : (sw < 1024 ? 16 : 64));
   }
-  if (io.fstate) {
-    L.pre(5);
-    k_export<K><<<grid, blk, 0, st>>>(d, io);
-    L.post();
-  }
-  cudaMemsetAsync(d.ctr, 0, 16, st);
-  k_flow<<<(nslot + 127) / 128, 128, 0, st>>>(d, io);
-  ++L.n;
-  if (!ck(c, cudaGetLastError(), "k_flow")) return GC_ERR_CUDA;
-  cudaMemcpyAsync(c->hpin, d.ctr, 12, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(c->hpin, d.gctr, 16, cudaMemcpyDeviceToHost, st);
   if (!ck(c, cudaStreamSynchronize(st), "solve")) return GC_ERR_CUDA;
-  if (c->hpin[1]) return GC_ERR_RANGE;
-  if (c->hpin[2] || status == GC_ERR_NOCONV) return GC_ERR_NOCONV;
+  if (status == GC_ERR_NOCONV) return GC_ERR_NOCONV;
+  if (c->hpin[2]) return GC_ERR_RANGE;
   return GC_OK;
 }
 
@@ -247,16 +264,6 @@ gc_status check_batch(gc_ctx* c, const gc_batch* b) {
     return GC_ERR_ARG;
   }
   return GC_OK;
-}
-
-int chunk_frames(gc_ctx* c, int H, int W) {
-  const size_t fb = frame_bytes(c->K, tiles_of(H, W));
-  size_t n = c->pool_bytes / fb;
-  if (n < 1) n = 1;
-  if (c->max_batch > 0 && n > (size_t)c->max_batch) n = c->max_batch;
-  const char* env = getenv("GC_CHUNK");
-  if (env && atoi(env) > 0 && (size_t)atoi(env) < n) n = atoi(env);
-  return (int)n;
 }
 
 gc_status worst(gc_status a, gc_status b) {
@@ -352,24 +359,13 @@ gc_status gc_solve_batch(gc_ctx* c, const gc_batch* b, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int H = b->H, W = b->W, K = c->K;
   const size_t plane = (size_t)H * W;
-  const int chunk = chunk_frames(c, H, W);
   Launcher L{c, st};
   gc_status res = GC_OK;
-  for (int f0 = 0; f0 < b->n; f0 += chunk) {
-    const int m = b->n - f0 < chunk ? b->n - f0 : chunk;
-    IO io;
-    io.cs = b->cap_s + f0 * plane;
-    io.ct = b->cap_t + f0 * plane;
-    io.nb = b->cap_nb + f0 * plane * K;
-    io.wf = b->warm_flow ? b->warm_flow + f0 * plane * (K / 2) : nullptr;
-    io.flow = b->flow_out + f0;
-    io.mask = b->mask_out + f0 * plane;
-    io.fstate = b->flow_state_out ? b->flow_state_out + f0 * plane * (K / 2) : nullptr;
-    io.stats = b->stats_out ? b->stats_out + f0 * 4 : nullptr;
-    gc_status r = (K == 8) ? solve_chunk<8>(c, io, m, H, W, st, L) : solve_chunk<4>(c, io, m, H, W, st, L);
-    res = worst(res, r);
-    if (r == GC_ERR_CUDA) break;
+  if (b->n > 0) {
+    IO io{b->cap_s, b->cap_t, b->cap_nb, b->warm_flow, b->flow_out, b->mask_out, b->flow_state_out, b->stats_out};
+    res = (K == 8) ? solve_chunk<8>(c, io, b->n, H, W, st, L) : solve_chunk<4>(c, io, b->n, H, W, st, L);
   }
+  (void)plane;
   c->last_launches = L.n;
   if (c->prof) resolve_profile(c);
   if (res == GC_ERR_RANGE && c->err.empty()) c->err = "capacity out of range [0, GC_CAP_MAX] in some frame";
