@@ -345,6 +345,151 @@ __device__ __forceinline__ int bfs_seed_tile(const Dev& d, size_t gt, int* hs, c
   return __syncthreads_or(act);
 }
 
+// One pixel's current e and r: from the materialised state, else recomputed from the caps
+// (+ clamped warm flows) exactly as tile_from_caps does.  (y, x) are frame coordinates.
+template <int K>
+__device__ __forceinline__ void px_er(const Dev& d, const IO& io, size_t gt, int lp, int y, int x, int& e,
+                                      int (&r)[K]) {
+  if (d.mat[gt]) {
+    e = d.e[gt * TPX + lp];
+#pragma unroll
+    for (int k = 0; k < K; ++k) r[k] = Rp(d, K, gt, k)[lp];
+    return;
+  }
+  const int s = (int)(gt / d.T);
+  const int H = d.H, W = d.W;
+  const size_t plane = (size_t)H * W;
+  const size_t f = (size_t)d.sfr[s];
+  const int32_t* nb = io.nb + f * plane * K;
+  const int32_t* wf = io.wf ? io.wf + f * plane * (K / 2) : nullptr;
+  const bool in = y < H && x < W;
+  const size_t o = (size_t)y * W + x;
+  e = in ? __ldg(io.cs + f * plane + o) - __ldg(io.ct + f * plane + o) : 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int y2 = y + DYk(k), x2 = x + DXk(k);
+    int rk = 0;
+    if (in && y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) {
+      const int c = __ldg(nb + k * plane + o);
+      rk = c;
+      if (wf) {
+        const size_t oq = (size_t)y2 * W + x2;
+        const int cq = __ldg(nb + (k ^ 1) * plane + oq);
+        if ((k & 1) == 0) {
+          const int fv = max(-cq, min(c, __ldg(wf + (k >> 1) * plane + o)));
+          rk = c - fv;
+          e -= fv;
+        } else {
+          const int fv = max(-c, min(cq, __ldg(wf + ((k ^ 1) >> 1) * plane + oq)));
+          rk = c + fv;
+          e += fv;
+        }
+      }
+    }
+    r[k] = rk;
+  }
+}
+
+// ---- shared-memory tile state (push kernel): es[TPX], rs[K][TPX]; pixel-at-a-time so
+// no register arrays stay live.
+template <int K>
+__device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_t gt, int* es, int* rs) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  if (d.mat[gt]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int lp = (iy0 + 8 * j) * TS + ix;
+      es[lp] = d.e[gt * TPX + lp];
+#pragma unroll
+      for (int k = 0; k < K; ++k) rs[k * TPX + lp] = Rp(d, K, gt, k)[lp];
+    }
+    return;
+  }
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  const int H = d.H, W = d.W;
+  const size_t plane = (size_t)H * W;
+  const size_t f = (size_t)d.sfr[s];
+  const int32_t* cs = io.cs + f * plane;
+  const int32_t* ct = io.ct + f * plane;
+  const int32_t* nb = io.nb + f * plane * K;
+  const int32_t* wf = io.wf ? io.wf + f * plane * (K / 2) : nullptr;
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix, lp = (iy0 + 8 * j) * TS + ix;
+    int ev = 0;
+    const bool in = y < H && x < W;
+    const size_t o = (size_t)y * W + x;
+    if (in) ev = __ldg(cs + o) - __ldg(ct + o);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int y2 = y + DYk(k), x2 = x + DXk(k);
+      int rk = 0;
+      if (in && y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) {
+        const int c = __ldg(nb + k * plane + o);
+        rk = c;
+        if (wf) {  // a1w: identical clamp to tile_from_caps / tile_init
+          const size_t oq = (size_t)y2 * W + x2;
+          const int cq = __ldg(nb + (k ^ 1) * plane + oq);
+          if ((k & 1) == 0) {
+            const int fv = max(-cq, min(c, __ldg(wf + (k >> 1) * plane + o)));
+            rk = c - fv;
+            ev -= fv;
+          } else {
+            const int fv = max(-c, min(cq, __ldg(wf + ((k ^ 1) >> 1) * plane + oq)));
+            rk = c + fv;
+            ev += fv;
+          }
+        }
+      }
+      rs[k * TPX + lp] = rk;
+    }
+    es[lp] = ev;
+  }
+}
+
+// Absorb inbound border flow (inbox parity `par`) into the shared-memory state.
+template <int K>
+__device__ __forceinline__ void absorb_smem(const Dev& d, int par, size_t gt, int* es, int* rs) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int iy = iy0 + 8 * j, lp = iy * TS + ix;
+    if (!on_border(iy, ix)) continue;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int wy = iy - DYk(k), wx = ix - DXk(k);
+      if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
+      int32_t* p = INBp(d, K, par, gt, k) + recv_slot(k, iy, ix);
+      const int dl = *p;
+      if (dl) {
+        es[lp] += dl;
+        rs[(k ^ 1) * TPX + lp] += dl;  // residual u -> w grows by the flow w -> u
+        *p = 0;
+      }
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void tile_store_smem(const Dev& d, size_t gt, const int* es, const int* rs) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int lp = (iy0 + 8 * j) * TS + ix;
+    const int ev = es[lp];
+    d.e[gt * TPX + lp] = ev;
+    int f = (ev > 0 ? FL_POS : 0) | (ev < 0 ? FL_NEG : 0);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int rk = rs[k * TPX + lp];
+      Rp(d, K, gt, k)[lp] = rk;
+      f |= (rk > 0) << k;
+    }
+    d.fl[gt * TPX + lp] = (uint16_t)f;
+  }
+}
+
 // ------------------------------------------------------------------------------ a1
 // Init: a streaming pass over the caps.  Computes e and r in registers (the tile stays
 // un-materialised -- e, r are recomputed if a push ever touches it) and writes only the

@@ -105,12 +105,29 @@ __device__ __forceinline__ void tile_seed(const Dev& d, const IO& io, size_t gt,
   const int par_in = (sw - 1) & 1;
   int fl[4];
   if (d.recv[par_in * ns + gt]) {  // flow still in flight from the last push step
-    int e[4], r[4][K];
-    get_er<K>(d, io, gt, e, r);
-    absorb<K>(d, par_in, gt, e, r);
-    store_er<K>(d, gt, e, r);
+    const int tile = (int)(gt - (size_t)s * d.T);
+    const int ty = tile / d.TX, tx = tile - ty * d.TX;
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {  // pixel at a time: materialise, absorb, store
+      const int iy = iy0 + 8 * j, lp = iy * TS + ix;
+      int e, r[K];
+      px_er<K>(d, io, gt, lp, ty * TS + iy, tx * TS + ix, e, r);
+      if (on_border(iy, ix)) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) fl[j] = make_fl<K>(e[j], r[j]);
+        for (int k = 0; k < K; ++k) {
+          const int wy = iy - DYk(k), wx = ix - DXk(k);
+          if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
+          int32_t* p = INBp(d, K, par_in, gt, k) + recv_slot(k, iy, ix);
+          const int dl = *p;
+          if (dl) { e += dl; r[k ^ 1] += dl; *p = 0; }
+        }
+      }
+      d.e[gt * TPX + lp] = e;
+#pragma unroll
+      for (int k = 0; k < K; ++k) Rp(d, K, gt, k)[lp] = r[k];
+      fl[j] = make_fl<K>(e, r);
+      d.fl[gt * TPX + lp] = (uint16_t)fl[j];
+    }
     __syncthreads();
     if (t == 0) { d.mat[gt] = 1; d.recv[par_in * ns + gt] = 0; }
   } else {
@@ -351,18 +368,18 @@ __device__ __forceinline__ void tile_export(const Dev& d, const IO& io, size_t g
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const size_t fr = (size_t)d.sfr[s];
-  int e[4], r[4][K];
-  get_er<K>(d, io, gt, e, r);
-#pragma unroll
+#pragma unroll 1
   for (int j = 0; j < 4; ++j) {
     const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
     if (y >= H || x >= W) continue;
+    int e, r[K];
+    px_er<K>(d, io, gt, (iy0 + 8 * j) * TS + ix, y, x, e, r);
     const size_t o = (size_t)y * W + x;
 #pragma unroll
     for (int k = 0; k < K; k += 2) {
       const int y2 = y + DYk(k), x2 = x + DXk(k);
       int f = 0;
-      if (y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = io.nb[fr * plane * K + k * plane + o] - r[j][k];
+      if (y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = io.nb[fr * plane * K + k * plane + o] - r[k];
       io.fstate[fr * plane * (K / 2) + (k >> 1) * plane + o] = f;
     }
   }
@@ -370,7 +387,7 @@ __device__ __forceinline__ void tile_export(const Dev& d, const IO& io, size_t g
 
 // ---------------------------------------------------------------- step kernels
 template <int K>
-__global__ void __launch_bounds__(NTH) k_stream(Dev d, IO io, int sw, int vec) {
+__global__ void __launch_bounds__(NTH, 4) k_stream(Dev d, IO io, int sw, int vec) {
   __shared__ long long red[2][NTH / 32];
   GC_LIST_BEGIN(G_STREAM, 1)
   if (md == M_INIT) {
@@ -384,7 +401,7 @@ __global__ void __launch_bounds__(NTH) k_stream(Dev d, IO io, int sw, int vec) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(NTH) k_seed(Dev d, IO io, int sw) {
+__global__ void __launch_bounds__(NTH, 4) k_seed(Dev d, IO io, int sw) {
   __shared__ int hs[HS * HS];
   __shared__ long long red[NTH / 32];
   uint8_t* ms = reinterpret_cast<uint8_t*>(hs);  // closure tiles reuse the height buffer
@@ -401,7 +418,7 @@ __global__ void __launch_bounds__(NTH) k_seed(Dev d, IO io, int sw) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(NTH) k_relax(Dev d, IO io, int sw) {
+__global__ void __launch_bounds__(NTH, 4) k_relax(Dev d, IO io, int sw) {
   __shared__ int hs[HS * HS];
   __shared__ int bits_s;
   uint8_t* ms = reinterpret_cast<uint8_t*>(hs);
@@ -419,19 +436,28 @@ __global__ void __launch_bounds__(NTH) k_relax(Dev d, IO io, int sw) {
 }
 
 // ---------------------------------------------------------------- a3: k_push
-// Up to `rounds` synchronous push / gather / relabel rounds inside each active tile (or
-// tile with inbound flow) of the slots in M_PUSH (4x the rounds once a push phase has run
-// 8 steps: long-distance transport).  Pushes are decided by the owner (it lowers its own e
-// and r); receivers inside the tile gather them in a separate phase; pushes across the tile
-// border go to the receiver tile's inbox and are absorbed at its next step.  Border heights
-// are those of the previous step (stale); the exact global relabel restores valid labels
-// and certifies termination.
+// Up to `rounds` synchronous push / relabel rounds inside each active tile (or tile with
+// inbound flow) of the slots in M_PUSH (4x the rounds once a push phase has run 8 steps:
+// long-distance transport).  e, r and two height buffers live in shared memory.  Push
+// phase: every active pixel v (e > 0, finite h) pushes delta = min(e, r_k) along admissible
+// arcs (h(u) = h(v) - 1): it lowers its own r_k, raises r_opp(u) (unique writer: u cannot
+// push back to v in the same round) and moves delta between e(v) and e(u) with shared-memory
+// atomics.  Relabel phase (Jacobi): h'(v) = 1 + min h(u) over residual arcs for active
+// pixels without an admissible arc.  Pushes across the tile border accumulate per receiver
+// slot and go to the receiver tile's inbox at the end (absorbed at its next step).  Border
+// heights are those of the previous step (stale); the exact global relabel restores valid
+// labels and certifies termination.
 template <int K>
-__global__ void __launch_bounds__(NTH) k_push(Dev d, IO io, int sw, int rounds) {
+constexpr size_t push_smem_bytes() { return sizeof(int) * (2 * HS * HS + TPX + K * TPX + K * 64); }
+
+template <int K>
+__global__ void __launch_bounds__(NTH, 4) k_push(Dev d, IO io, int sw, int rounds) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  __shared__ int hs[HS * HS];
-  __shared__ int ps[K][TPX];
-  __shared__ int oacc[K][64];
+  extern __shared__ int smem_push[];  // push_smem_bytes<K>() of dynamic shared memory
+  int(*hb)[HS * HS] = reinterpret_cast<int(*)[HS * HS]>(smem_push);  // heights, 2 buffers
+  int* es = smem_push + 2 * HS * HS;                                  // excess
+  int* rs = es + TPX;                                                 // residuals [K][TPX]
+  int(*oacc)[64] = reinterpret_cast<int(*)[64]>(rs + K * TPX);        // border pushes by slot
   const int hmax = d.hmax;
   const int par_out = sw & 1, par_in = par_out ^ 1;
   GC_LIST_BEGIN(G_PUSH, (d.tact[id] || d.recv[par_in * ns_ + id]))
@@ -441,103 +467,105 @@ __global__ void __launch_bounds__(NTH) k_push(Dev d, IO io, int sw, int rounds) 
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int rcv = d.recv[par_in * ns_ + gt];
   const int nround = d.fpush[s] >= 8 ? 4 * rounds : rounds;
-  int e[4], r[4][K], h[4];
-  get_er<K>(d, io, gt, e, r);
   long long neg0 = 0;
+  tile_load_smem<K>(d, io, gt, es, rs);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    h[j] = d.h[gt * TPX + (iy0 + 8 * j) * TS + ix];
-    neg0 += e[j] < 0 ? -(long long)e[j] : 0;
+    const int ev = es[(iy0 + 8 * j) * TS + ix];
+    neg0 += ev < 0 ? -(long long)ev : 0;
   }
-  if (rcv) {
-    absorb<K>(d, par_in, gt, e, r);
-    __syncthreads();
-    if (t == 0) d.recv[par_in * ns_ + gt] = 0;
-  }
+  if (rcv) absorb_smem<K>(d, par_in, gt, es, rs);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) hs[hidx(iy0 + 8 * j, ix)] = h[j];
-  load_halo(d, s, ty, tx, hs, t);
+  for (int j = 0; j < 4; ++j) {
+    const int hv = d.h[gt * TPX + (iy0 + 8 * j) * TS + ix];
+    hb[0][hidx(iy0 + 8 * j, ix)] = hv;
+    hb[1][hidx(iy0 + 8 * j, ix)] = hv;
+  }
+  load_halo(d, s, ty, tx, hb[0], t);
+  load_halo(d, s, ty, tx, hb[1], t);
   for (int i = t; i < K * 64; i += NTH) (&oacc[0][0])[i] = 0;
   __syncthreads();
+  if (rcv && t == 0) d.recv[par_in * ns_ + gt] = 0;
   int nrel = 0;  // relabel operations (global-relabel heuristic, k_control)
+  int cb = 0;    // current height buffer
   for (int rd = 0; rd < nround; ++rd) {
+    const int* hc = hb[cb];
     // push phase (owner)
-#pragma unroll
+#pragma unroll 1
     for (int j = 0; j < 4; ++j) {
       const int iy = iy0 + 8 * j, lp = iy * TS + ix;
-      int ee = e[j];
-      const int hv = h[j];
-      const bool act = ee > 0 && hv < HINF;
+      int ee = es[lp];
+      const int hv = hc[hidx(iy, ix)];
+      if (ee > 0 && hv < HINF) {
+        int sent = 0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        int dl = 0;
-        if (act && ee > 0 && r[j][k] > 0 && hs[hidx(iy + DYk(k), ix + DXk(k))] == hv - 1) {
-          dl = min(ee, r[j][k]);
-          ee -= dl;
-          r[j][k] -= dl;
+        for (int k = 0; k < K; ++k) {
+          const int rk = rs[k * TPX + lp];
+          if (ee > 0 && rk > 0 && hc[hidx(iy + DYk(k), ix + DXk(k))] == hv - 1) {
+            const int dl = min(ee, rk);
+            ee -= dl;
+            sent += dl;
+            rs[k * TPX + lp] = rk - dl;
+            if (crosses(k, iy, ix)) {
+              oacc[k][recv_slot(k, (iy + DYk(k)) & 31, (ix + DXk(k)) & 31)] += dl;
+            } else {
+              const int u = (iy + DYk(k)) * TS + ix + DXk(k);
+              atomicAdd(&es[u], dl);
+              rs[(k ^ 1) * TPX + u] += dl;  // unique writer: u cannot push back to v this round
+            }
+          }
         }
-        if (crosses(k, iy, ix)) {
-          if (dl) oacc[k][recv_slot(k, (iy + DYk(k)) & 31, (ix + DXk(k)) & 31)] += dl;
-        } else {
-          ps[k][lp] = dl;
-        }
+        if (sent) atomicSub(&es[lp], sent);
       }
-      e[j] = ee;
     }
     __syncthreads();
-    // gather phase (receiver) + relabel decision
-    int hn[4];
-#pragma unroll
+    // relabel phase (Jacobi: read hc, write the other buffer)
+    int* hn = hb[cb ^ 1];
+    int still = 0;
+#pragma unroll 1
     for (int j = 0; j < 4; ++j) {
-      const int iy = iy0 + 8 * j;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int wy = iy - DYk(k), wx = ix - DXk(k);
-        if ((unsigned)wy < 32u && (unsigned)wx < 32u) {
-          const int dl = ps[k][wy * TS + wx];
-          e[j] += dl;
-          r[j][k ^ 1] += dl;
-        }
-      }
-      hn[j] = h[j];
-      if (e[j] > 0 && h[j] < HINF) {
+      const int iy = iy0 + 8 * j, lp = iy * TS + ix;
+      const int hv = hc[hidx(iy, ix)];
+      int h2 = hv;
+      if (es[lp] > 0 && hv < HINF) {
         int mn = HINF;
         bool adm = false;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if (r[j][k] > 0) {
-            const int hu = hs[hidx(iy + DYk(k), ix + DXk(k))];
-            adm |= (hu == h[j] - 1);
+          if (rs[k * TPX + lp] > 0) {
+            const int hu = hc[hidx(iy + DYk(k), ix + DXk(k))];
+            adm |= (hu == hv - 1);
             mn = min(mn, hu);
           }
         }
         if (!adm) {
-          hn[j] = (mn >= hmax - 1) ? HINF : mn + 1;
+          h2 = (mn >= hmax - 1) ? HINF : mn + 1;
           ++nrel;
         }
+        still |= h2 < HINF;
       }
+      hn[hidx(iy, ix)] = h2;
     }
-    __syncthreads();
-    int still = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      h[j] = hn[j];
-      hs[hidx(iy0 + 8 * j, ix)] = hn[j];
-      still |= (e[j] > 0) & (hn[j] < HINF);
-    }
+    cb ^= 1;
     if (!__syncthreads_or(still)) break;  // tile discharged: nothing left to push
   }
   // store state
   int act = 0;
   long long neg1 = 0;
-  store_er<K>(d, gt, e, r);
+  {
+    int h[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
-    act |= (e[j] > 0) & (h[j] < HINF);
-    neg1 += e[j] < 0 ? -(long long)e[j] : 0;
+    for (int j = 0; j < 4; ++j) {
+      const int lp = (iy0 + 8 * j) * TS + ix;
+      const int ev = es[lp];
+      h[j] = hb[cb][hidx(iy0 + 8 * j, ix)];
+      d.h[gt * TPX + lp] = h[j];
+      act |= (ev > 0) & (h[j] < HINF);
+      neg1 += ev < 0 ? -(long long)ev : 0;
+    }
+    tile_store_smem<K>(d, gt, es, rs);
+    store_hedge(d, gt, h, t);
   }
-  store_hedge(d, gt, h, t);
   // send border pushes to the neighbours' inboxes (unique writer per slot)
 #pragma unroll
   for (int j = 0; j < 4; ++j) {

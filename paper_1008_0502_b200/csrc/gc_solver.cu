@@ -167,10 +167,10 @@ void resolve_profile(gc_ctx* c) {
 
 // Persistent grid size of a worklist kernel: resident CTAs per SM x SMs.
 template <typename F>
-int persistent_grid(gc_ctx* c, F kernel) {
+int persistent_grid(gc_ctx* c, F kernel, size_t dyn_smem = 0) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, NTH, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, NTH, dyn_smem);
   if (per < 1) per = 1;
   if (sms < 1) sms = 148;
   return sms * per;
@@ -193,11 +193,13 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   const int nslot = chunk_frames(c, H, W) < nframes ? chunk_frames(c, H, W) : nframes;
   Dev d = carve(c, nslot, H, W);
   static int g_stream = 0, g_seed = 0, g_relax = 0, g_push = 0;  // per-K persistent grid sizes
+  const size_t push_smem = push_smem_bytes<K>();
   if (!g_stream) {
+    cudaFuncSetAttribute(k_push<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)push_smem);
     g_stream = persistent_grid(c, k_stream<K>);
     g_seed = persistent_grid(c, k_seed<K>);
     g_relax = persistent_grid(c, k_relax<K>);
-    g_push = persistent_grid(c, k_push<K>);
+    g_push = persistent_grid(c, k_push<K>, push_smem);
   }
   const size_t ns = (size_t)nslot * d.T;
   auto cap = [&](int g) { return (int)((size_t)g < ns ? g : ns); };
@@ -224,7 +226,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
     k_relax<K><<<cap(g_relax), blk, 0, st>>>(d, io, sw);
     L.post();
     L.pre(2);
-    k_push<K><<<cap(g_push), blk, 0, st>>>(d, io, sw, c->rounds);
+    k_push<K><<<cap(g_push), blk, push_smem, st>>>(d, io, sw, c->rounds);
     L.post();
     L.pre(3);
     k_control<<<nslot, NTH, 0, st>>>(d, io, sw, relabel_budget, c->max_push_phase, nframes);
