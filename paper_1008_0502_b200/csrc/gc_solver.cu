@@ -312,6 +312,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
     cudaMemGetInfo(&fr, &tot);
     size_t budget = (size_t)8 << 30;
     if (tot > 0 && tot / 16 < budget) budget = tot / 16;
+    if (const char* ev = getenv("GC_SCRATCH_MB")) budget = (size_t)atoll(ev) << 20;  // tuning knob
     nf = budget / fb;
     if (nf < 1) nf = 1;
   }
