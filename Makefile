@@ -7,7 +7,7 @@ PKG := paper_1008_0502_b200
 all: $(PKG)/libgc.so synth/libsynth.so oracle/liboracle.so
 
 $(PKG)/libgc.so: $(PKG)/csrc/gc_solver.cu $(wildcard $(PKG)/csrc/*.cuh) include/gc.h
-	$(NVCC) $(NVFLAGS) -Xptxas -v -shared -cudart static -o $@ $(PKG)/csrc/gc_solver.cu 2> build_gc_ptxas.log || (cat build_gc_ptxas.log; false)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -Xptxas -dlcm=cg -shared -cudart static -o $@ $(PKG)/csrc/gc_solver.cu 2> build_gc_ptxas.log || (cat build_gc_ptxas.log; false)
 
 synth/libsynth.so: synth/synth_host.c synth/synth_cuda.cu synth/synth.h
 	gcc -O2 -fPIC -c synth/synth_host.c -o synth/synth_host.o

@@ -48,8 +48,8 @@ def tile_bytes(cls: str, K: int) -> int:
         return (4 * (2 + K) + 4 * (2 + K) + 2) * px
     if cls == "bfs":       # read fl, h; write h (relax sweeps; the seed sweep moves less)
         return (2 + 4 + 4) * px
-    if cls == "init":      # read cs, ct, c[K]; write fl, h
-        return (4 * (2 + K) + 2 + 4) * px
+    if cls == "init":      # read cs, ct, c[K]; write fl
+        return (4 * (2 + K) + 2) * px
     if cls == "closure":   # read fl; write m and the caller's mask
         return (2 + 1 + 1) * px
     if cls == "export":    # read r[K/2] (or caps) ; write f[K/2]
@@ -291,34 +291,37 @@ def main():
         per_frame = torch.cat(gathered)
     bad_frames = int(stats[2].item())
 
-    # ---- profiled replica steps: per-kernel-class device time and tiles processed
+    # ---- profiled replica steps: the persistent kernel's device time (CUDA events on the
+    # launching stream) and the tile tasks of each class it ran
     g.set_profiling(True)
     g.profile(reset=True)
+    g.kernel_ms(reset=True)
     for _ in range(args.profile_steps):
         g.solve(cs, ct, nb, out=(flow, mask))
     torch.cuda.synchronize()
     prof = g.profile(reset=True)
+    kms = g.kernel_ms(reset=True)
     g.set_profiling(False)
     peak, peak_src = load_peak()
-    dom = max(prof, key=lambda c: prof[c][1])
-    nl, pms, ptiles = prof[dom]
-    avg_ms = pms / max(nl, 1)
-    bytes_launch = tile_bytes(dom, K) * ptiles / max(nl, 1)
+    nl = max(prof["init"][0], 1)
+    avg_ms = kms / nl
+    bytes_launch = sum(tile_bytes(c, K) * prof[c][2] for c in prof) / nl
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+            traffic = json.load(open(tp)).get(args.config, {}).get("k_solve")
         except Exception:
             traffic = None
-    tot_prof_ms = sum(v[1] for v in prof.values())
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": f"k_{dom}",
-                "bytes_per_launch": int(bytes_launch), "avg_launch_ms": round(avg_ms, 5),
-                "tiles_per_launch": round(ptiles / max(nl, 1), 1), "share_of_step": round(pms / max(tot_prof_ms, 1e-9), 3),
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": f"k_solve<{K}>",
+                "bytes_per_launch": int(bytes_launch), "avg_launch_ms": round(avg_ms, 4),
+                "launches_per_step": round(nl / args.profile_steps, 2),
+                "share_of_step": round(kms / max(args.profile_steps * ms_max / args.steps, 1e-9), 3),
                 "peak_source": peak_src,
-                "classes": {c: {"launches": v[0], "ms": round(v[1], 3), "tiles": v[2]} for c, v in prof.items()}}
+                "classes": {c: {"tasks": v[2], "cta_ms": round(v[1], 3), "bytes": tile_bytes(c, K) * v[2]}
+                            for c, v in prof.items()}}
     comp = compulsory_bytes_per_px(K) * n * H * W * world * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with HOST buffers (pinned), copies inside timing

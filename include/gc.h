@@ -34,8 +34,9 @@
  *   makes that frame's flow_out = -1, its mask all 0, its stats status GC_ERR_RANGE,
  *   and the call returns GC_ERR_RANGE (other frames are still solved).  n-link entries
  *   that point off the grid are IGNORED (any value, reading c7).  If the solve needs
- *   more than max_launches kernel launches the unfinished frames get flow_out = -1 and
- *   the call returns GC_ERR_NOCONV.  CUDA failures return GC_ERR_CUDA; the message is
+ *   more than max_launches x (tiles in flight) tile tasks, or runs longer than the
+ *   context's wall-clock bound (GC_TIMEOUT_S, default 300 s), the unfinished frames get
+ *   flow_out = -1 and the call returns GC_ERR_NOCONV.  CUDA failures return GC_ERR_CUDA; the message is
  *   available from gc_last_error().  Calls return after all work on `stream` for this
  *   call has completed.
  */
@@ -67,9 +68,10 @@ typedef struct {
   int max_h, max_w;      /* largest frame the context will accept (default 1080 x 1920)  */
   int max_batch;         /* frames solved concurrently per device pass (default: as many
                             as a scratch budget of min(8 GB, 1/16 device memory) holds) */
-  int rounds_per_launch; /* push/relabel rounds inside a tile per launch (default 8)     */
-  int relabel_period;    /* push launches between global relabels (default 2)            */
-  long long max_launches;/* per chunk; exceeded -> GC_ERR_NOCONV (default 1,000,000)     */
+  int rounds_per_launch; /* push/relabel rounds inside a tile per push task (default 8)  */
+  int relabel_period;    /* reserved (global relabels follow Goldberg's heuristic)       */
+  long long max_launches;/* watchdog: a call may run max_launches x (tiles in flight) tile
+                            tasks; exceeded -> GC_ERR_NOCONV (default 1,000,000)          */
 } gc_config;
 
 /* Allocates the context and its device scratch.  *out is NULL on failure. */
@@ -90,8 +92,8 @@ typedef struct {
   int64_t* flow_out;         /* [n] max-flow value of the graph as given                   */
   uint8_t* mask_out;         /* [n][H][W] 1 iff reachable from s in the final residual     */
   int32_t* flow_state_out;   /* NULL, or [n][K/2][H][W]: this solve's forward-arc flows    */
-  int32_t* stats_out;        /* NULL, or [n][4]: push launches, global relabels, BFS sweeps,
-                                status (gc_status of the frame)                            */
+  int32_t* stats_out;        /* NULL, or [n][4]: push tile tasks, global relabels, BFS relax
+                                tile tasks, status (gc_status of the frame)                */
 } gc_batch;
 
 /* Device-pointer entry point.  `stream` is a cudaStream_t (NULL = legacy default). */
@@ -104,19 +106,23 @@ gc_status gc_solve_batch_host(gc_ctx* ctx, const gc_batch* batch, void* stream);
 /* Message for the last failing call on this context ("" if none).  Never NULL. */
 const char* gc_last_error(const gc_ctx* ctx);
 
-/* Number of kernel launches the last solve issued (for the bench's gpu_launches). */
+/* Number of kernel launches the last solve issued (for the bench's gpu_launches): a setup
+ * kernel and one persistent k_solve per chunk of frames (+ k_abort after a watchdog stop). */
 long long gc_last_launches(const gc_ctx* ctx);
 
-/* Profiling: when enabled, the library brackets every launch of each kernel class with
- * CUDA events on the launching stream, accumulates device time, and counts the 32x32
- * tiles each class actually processed (tiles skipped as inactive are not counted).
- * Classes: 0 init (+ first BFS seed), 1 bfs (seed+relax), 2 push, 3 status, 4 closure,
- * 5 export (flow_state_out).
- * Off by default (the events add host overhead to every launch). */
+/* Profiling: when enabled, the persistent kernel times every tile task (globaltimer) and
+ * the host brackets every k_solve launch with CUDA events on the launching stream.
+ * Task classes: 0 init, 1 bfs (seed + relax), 2 push, 3 scheduler (waiting for a task,
+ * phase transitions), 4 closure, 5 export (flow_state_out).
+ * Off by default (the timers add a few atomics per task). */
 void gc_set_profiling(gc_ctx* ctx, int enable);
-/* Fills launches[6], ms[6] and tiles[6] (any may be NULL) accumulated since the last
- * reset; resets the counters if reset != 0. */
+/* Fills launches[6] (k_solve launches, the same in every class), ms[6] (CTA time spent in
+ * the class, averaged over the CTAs of the persistent grid, so the six add up to the
+ * kernel's duration) and tiles[6] (tile tasks of the class), accumulated since the last
+ * reset; any pointer may be NULL; resets the counters if reset != 0. */
 void gc_get_profile(gc_ctx* ctx, long long* launches, double* ms, long long* tiles, int reset);
+/* Device time (ms, CUDA events) of the k_solve launches since the last reset (profiling on). */
+double gc_get_kernel_ms(gc_ctx* ctx, int reset);
 
 #ifdef __cplusplus
 }

@@ -16,14 +16,14 @@ import os
 import numpy as np
 
 __all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host",
-           "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "CAP_MAX",
+           "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "CAP_MAX",
            "STATUS", "lib_path"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libgc.so")
 CAP_MAX = (1 << 26) - 1
 STATUS = {0: "GC_OK", 1: "GC_ERR_ARG", 2: "GC_ERR_RANGE", 3: "GC_ERR_OOM", 4: "GC_ERR_CUDA", 5: "GC_ERR_NOCONV"}
-PROFILE_CLASSES = ("init", "bfs", "push", "status", "closure", "export")
+PROFILE_CLASSES = ("init", "bfs", "push", "sched", "closure", "export")
 
 if not os.path.exists(lib_path):
     raise ImportError(f"{lib_path} is missing: build it with __graft_entry__.build() (make). "
@@ -61,9 +61,11 @@ _lib.gc_set_profiling.restype = None
 _lib.gc_get_profile.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong),
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 _lib.gc_get_profile.restype = None
+_lib.gc_get_kernel_ms.argtypes = [ctypes.c_void_p, ctypes.c_int]
+_lib.gc_get_kernel_ms.restype = ctypes.c_double
 
 EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
-            "gc_last_launches", "gc_set_profiling", "gc_get_profile")
+            "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms")
 
 
 class GcError(RuntimeError):
@@ -110,6 +112,10 @@ def gc_get_profile(ctx, reset: bool = False):
     tl = (ctypes.c_longlong * 6)()
     _lib.gc_get_profile(ctx, n, ms, tl, int(bool(reset)))
     return {c: (int(n[i]), float(ms[i]), int(tl[i])) for i, c in enumerate(PROFILE_CLASSES)}
+
+
+def gc_get_kernel_ms(ctx, reset: bool = False) -> float:
+    return float(_lib.gc_get_kernel_ms(ctx, int(bool(reset))))
 
 
 def _ptr(x):
@@ -210,3 +216,6 @@ class GridCut:
 
     def profile(self, reset=False):
         return gc_get_profile(self.ctx, reset)
+
+    def kernel_ms(self, reset=False) -> float:
+        return gc_get_kernel_ms(self.ctx, reset)

@@ -1,10 +1,11 @@
 // gc_kernels.cuh -- sm_100a kernels of the grid min-cut hot path.
 //
 // Algorithm: push-relabel (Goldberg-Tarjan) on the pixel grid graph of P:331-357, run as
-// tile-synchronous region discharges, with exact global relabels (BFS from the sink) as
-// the termination certificate, and the canonical mask taken as the residual closure of
+// asynchronous 32x32-tile region discharges, with exact global relabels (BFS from the sink)
+// as the termination certificate, and the canonical mask taken as the residual closure of
 // the excess nodes.  The paper's GPU solver is "CUDA Cuts";
-// this is a fresh B200 design, not a translation of it.
+// this is a fresh B200 design, not a translation of it.  This header holds the tile-level
+// building blocks; gc_phases.cuh holds the task bodies and the persistent scheduler.
 //
 // State (tile-major, 32x32 tiles, frame padded to whole tiles):
 //   fl [slot][tile][1024] u16  bit k: r_k > 0 (arc open), bit 8: e > 0, bit 9: e < 0.
@@ -16,13 +17,14 @@
 //                              (+ warm flows) the first time a push touches it, so tiles
 //                              the push phase never visits are never written.
 //   hedge [slot][tile][4][32]  copy of the tile's border heights (top, bottom, left, right)
-//   inbox [2][slot][tile][k][64] flow pushed INTO the tile across its border, by arc direction
-//                              and receiver edge slot; double-buffered by launch parity,
-//                              written by the unique sender, zeroed by the receiver
+//   sent/got [slot][tile][k][64] cumulative flow pushed INTO the tile across its border, by
+//                              arc direction and receiver edge slot: `sent` written only by
+//                              the sending tile, `got` only by the receiver (no atomics)
 //   reach [slot][tile][k][64]  sticky min-cut reach bits arriving across the border
 //   m  [slot][tile][1024] u8   mask bit (closure phase)
-// Sparse phases (BFS relax, push, closure relax) run as persistent grids over a worklist of
-// flagged tiles, compacted per CTA in shared memory.  No global atomics on the push path.
+// A tile is processed by at most one CTA at a time (gc_phases.cuh); all mutable state is
+// read through L2 (the library is compiled with -dlcm=cg), the caps through the read-only
+// path.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -53,36 +55,45 @@ struct Dev {
   int32_t* r;
   uint16_t* fl;
   int32_t* hedge;
-  int32_t* inbox;
+  uint32_t* sent;   // [NS][K][64] cumulative flow pushed INTO the tile across its border, by
+                    //             arc direction and receiver edge slot (written by the sender)
+  uint32_t* got;    // [NS][K][64] cumulative flow the tile has absorbed from `sent` (receiver)
   uint8_t* reach;
   uint8_t* m;
   long long* neg0;  // [NS] sum max(0,-e) of the tile as initialised (for never-materialised tiles)
   int32_t* mat;     // [NS]   e, r of the tile are materialised
   int32_t* tact;    // [NS]   tile has an active node (e > 0, h < HINF)
-  int32_t* dirty;   // [2][NS] tile must be re-relaxed in the next BFS sweep of that parity
-  int32_t* recv;    // [2][NS] tile has inbound flow in inbox of that parity
-  int32_t* crecv;   // [2][NS] tile received new reach bits in the closure sweep of that parity
-  int32_t* tph;     // [NS]   push-phase stamp of the last push that touched the tile
+  int32_t* flag;    // [NS]   tile is in the first task set of the next phase (seed -> BFS, cseed -> closure)
+  int32_t* recv1;   // [NS]   tile has inbound flow not yet absorbed
+  int32_t* treq;    // [NS]   requests for the tile in the running phase (> 0: queued or running)
+  int32_t* tuni;    // [NS]   uniform sink tile: every in-frame pixel has e < 0 and h = 1 (h is not
+                    //        stored; hedge is); such a tile is neither seeded nor relaxed
+  int32_t* tfix;    // [NS]   a BFS relax of the tile cannot change it (every pixel with an
+                    //        open arc has h = 1)
+  int32_t* tph;     // [NS]   push-phase id of the tile's last push task
   // per frame slot (state machine): zero-initialised by one memset
   int32_t* fmode;   // [nslot] M_INIT, M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_EXPORT, M_IDLE
   int32_t* sfr;     // [nslot] batch frame index held by the slot
-  int32_t* fstall;  // [nslot] consecutive push steps without progress
+  int32_t* fout;    // [nslot] tasks of the running phase queued or running
   int32_t* gctr;    // [4] next frame to start, frames finished, range-error frames, -
-  int32_t* slist;   // [2][4][nslot] slots of each kernel group for the step of that parity
-  int32_t* lcnt;    // [2][4] list lengths
   int32_t* ferr;    // [nslot] capacity out of range
-  int32_t* fchg;    // [2][nslot] something changed in the step of that parity (BFS / closure)
   int32_t* fph;     // [nslot] global relabels so far (push-phase id)
-  int32_t* fpush;   // [nslot] push steps in the current phase
-  int32_t* fnew;    // [nslot] tiles first touched by a push in this step
-  int32_t* fstat;   // [nslot][4] push steps, global relabels, BFS sweeps, -
-  unsigned long long* fabs_;  // [nslot] flow absorbed by sink-connected nodes in this step
+  int32_t* fvis;    // [nslot] push tasks in the current push phase
+  int32_t* fprog;   // [nslot] value of fvis after the last push task that made progress
+  int32_t* fstat;   // [nslot][4] push tasks, global relabels, BFS relax tasks, -
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]
   unsigned long long* sumneg; // [nslot]
-  int32_t* ring;    // [64] frames not done, per step
-  int32_t* ctr;     // [8]
-  unsigned long long* ptiles;  // [6] tiles processed per kernel class (profiling only, else NULL)
+  // work queue: ring of tile ids, ticketed by two 64-bit counters
+  uint32_t* q;
+  uint32_t qmask;
+  unsigned long long* qhead;
+  unsigned long long* qtail;
+  int32_t* done;    // [0] every frame finished, [1] aborted
+  unsigned long long* ntask;  // tasks executed (watchdog)
+  const volatile int32_t* hostabort;  // mapped host word: the host asks the kernel to stop
+  unsigned long long* ptiles;  // [6] tasks per class (profiling only, else NULL)
+  unsigned long long* pns;     // [6] ns per class summed over CTAs (profiling only)
 };
 
 enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_EXPORT = 6, M_IDLE = 7 };
@@ -98,17 +109,13 @@ struct IO {
   int32_t* stats;
 };
 
-__device__ __forceinline__ void count_tile(const Dev& d, int cls) {
-  if (d.ptiles && threadIdx.x == 0) atomicAdd(&d.ptiles[cls], 1ULL);
-}
 __device__ __forceinline__ size_t NS(const Dev& d) { return (size_t)d.nslot * d.T; }
 __device__ __forceinline__ int32_t* Rp(const Dev& d, int K, size_t gt, int k) {
   const size_t s = gt / d.T, tile = gt - s * d.T;
   return d.r + ((s * K + k) * d.T + tile) * TPX;
 }
-__device__ __forceinline__ int32_t* INBp(const Dev& d, int K, int par, size_t gt, int k) {
-  return d.inbox + (((size_t)par * NS(d) + gt) * K + k) * 64;
-}
+__device__ __forceinline__ uint32_t* SENTp(const Dev& d, int K, size_t gt, int k) { return d.sent + (gt * K + k) * 64; }
+__device__ __forceinline__ uint32_t* GOTp(const Dev& d, int K, size_t gt, int k) { return d.got + (gt * K + k) * 64; }
 
 // Does arc (iy,ix) -> (iy,ix)+d_k leave the tile?
 __device__ __forceinline__ bool crosses(int k, int iy, int ix) {
@@ -270,29 +277,6 @@ __device__ __forceinline__ void get_er(const Dev& d, const IO& io, size_t gt, in
   }
 }
 
-// Absorb the flow pushed into this tile in the previous launch (inbox parity `par`).
-template <int K>
-__device__ __forceinline__ void absorb(const Dev& d, int par, size_t gt, int (&e)[4], int (&r)[4][K]) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j;
-    if (!on_border(iy, ix)) continue;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int wy = iy - DYk(k), wx = ix - DXk(k);
-      if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-      int32_t* p = INBp(d, K, par, gt, k) + recv_slot(k, iy, ix);
-      const int dl = *p;
-      if (dl) {
-        e[j] += dl;
-        r[j][k ^ 1] += dl;  // residual u -> w grows by the flow w -> u
-        *p = 0;
-      }
-    }
-  }
-}
-
 // Tile-local BFS fixpoint: h(v) = min(h(v), 1 + min{h(v+d_k) : arc k open}) until stable.
 // hs holds the halo'd heights (halo fixed); updates are written in place (monotone, so a
 // racing reader sees an old or a new upper bound -- both valid).
@@ -448,9 +432,24 @@ __device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_
   }
 }
 
-// Absorb inbound border flow (inbox parity `par`) into the shared-memory state.
+// Flow that arrived across the border of receiver pixel (iy, ix) along direction k since
+// the tile last absorbed: sent - got (wrapping uint32 arithmetic: the amount in flight on
+// one arc is below 2^31).  Marks it absorbed.  Sender and receiver each own one counter,
+// so no atomics are needed.
 template <int K>
-__device__ __forceinline__ void absorb_smem(const Dev& d, int par, size_t gt, int* es, int* rs) {
+__device__ __forceinline__ int take_inflow(const Dev& d, size_t gt, int k, int iy, int ix) {
+  const int sl = recv_slot(k, iy, ix);
+  const uint32_t snt = __ldcg(SENTp(d, K, gt, k) + sl);
+  uint32_t* g = GOTp(d, K, gt, k) + sl;
+  const uint32_t gv = *g;
+  if (snt == gv) return 0;
+  *g = snt;
+  return (int)(snt - gv);
+}
+
+// Absorb inbound border flow into the shared-memory state.
+template <int K>
+__device__ __forceinline__ void absorb_smem(const Dev& d, size_t gt, int* es, int* rs) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -460,12 +459,10 @@ __device__ __forceinline__ void absorb_smem(const Dev& d, int par, size_t gt, in
     for (int k = 0; k < K; ++k) {
       const int wy = iy - DYk(k), wx = ix - DXk(k);
       if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-      int32_t* p = INBp(d, K, par, gt, k) + recv_slot(k, iy, ix);
-      const int dl = *p;
+      const int dl = take_inflow<K>(d, gt, k, iy, ix);
       if (dl) {
         es[lp] += dl;
         rs[(k ^ 1) * TPX + lp] += dl;  // residual u -> w grows by the flow w -> u
-        *p = 0;
       }
     }
   }
@@ -501,7 +498,6 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
-  const size_t ns = NS(d);
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const size_t fr = (size_t)d.sfr[s];  // batch frame held by this slot
@@ -510,7 +506,7 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
   const int32_t* nb = io.nb + fr * plane * K;
   const int32_t* wf = io.wf ? io.wf + fr * plane * (K / 2) : nullptr;
   const int y = ty * TS + iy, x0 = tx * TS + ix0;
-  int bad = 0;
+  int bad = 0, uni = 1;
   long long sct = 0, neg = 0;
   int a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0}, c[K][4];
   const size_t o0 = (size_t)y * W + x0;
@@ -568,6 +564,7 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
       }
       f |= (ev > 0 ? FL_POS : 0) | (ev < 0 ? FL_NEG : 0);
       neg += ev < 0 ? -(long long)ev : 0;
+      uni &= ev < 0;
     }
     fl4[i] = f;
   }
@@ -575,12 +572,14 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
   w.x = (unsigned short)fl4[0]; w.y = (unsigned short)fl4[1];
   w.z = (unsigned short)fl4[2]; w.w = (unsigned short)fl4[3];
   *reinterpret_cast<ushort4*>(d.fl + gt * TPX + iy * TS + ix0) = w;
-  for (int i = t; i < 2 * K * 64; i += NTH) {
-    const int par = i / (K * 64), rest = i - par * K * 64;
-    INBp(d, K, par, gt, 0)[rest] = 0;
-  }
   for (int i = t; i < K * 64; i += NTH) d.reach[gt * K * 64 + i] = 0;
   bad = __syncthreads_or(bad);
+  uni = __syncthreads_and(uni);
+  if (uni && t < 128) {  // uniform sink tile: publish its border heights now (h = 1 in frame)
+    const int side = t >> 5, j = t & 31;
+    const int py = side == 0 ? 0 : (side == 1 ? 31 : j), px = side == 2 ? 0 : (side == 3 ? 31 : j);
+    d.hedge[gt * 128 + t] = (ty * TS + py < H && tx * TS + px < W) ? 1 : HINF;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     sct += __shfl_xor_sync(0xffffffffu, sct, o);
@@ -594,9 +593,11 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
     if (sa) atomicAdd(&d.sumct[s], (unsigned long long)sa);
     d.neg0[gt] = sb;
     d.mat[gt] = 0;
-    d.dirty[gt] = 0; d.dirty[ns + gt] = 0;
-    d.recv[gt] = 0; d.recv[ns + gt] = 0;
-    d.crecv[gt] = 0; d.crecv[ns + gt] = 0;
+    d.flag[gt] = 0;
+    d.recv1[gt] = 0;
+    d.tact[gt] = 0;
+    d.tuni[gt] = uni;
+    d.tfix[gt] = uni;
     d.tph[gt] = -1;
     if (bad) d.ferr[s] = 1;
   }

@@ -1,54 +1,98 @@
-// gc_phases.cuh -- the per-step kernels of the device-side solve loop.
+// gc_phases.cuh -- the device-side solver: one persistent kernel (k_solve) runs every phase
+// of every frame of a batch as 32x32-tile tasks taken from a global work queue
+// (DESIGN.md §3).
 //
-// The context holds `nslot` frame slots.  Every slot runs its own state machine (d.fmode),
-// advanced once per step by k_control; a slot whose frame finishes is refilled with the next
-// frame of the batch on the device (continuous batching), so easy and hard frames never wait
-// for each other:
-//   M_INIT   -- streaming pass over the caps: fl bit-planes, sum c(v,t), range check (a1/a1w)
-//   M_SEED   -- global relabel, seed pass: absorb in-flight flow, h = 1 on nodes with
-//               residual capacity to t, tile-local BFS fixpoint                     (a2)
-//   M_BFS    -- global relabel, relax passes over tiles whose neighbours' border heights
-//               changed; ends when a step changes nothing (exact BFS distances)      (a2)
+// The context holds `nslot` frame slots.  Each slot runs a state machine (d.fmode):
+//   M_INIT   -- all tiles: streaming pass over the caps: fl bit-planes, sum c(v,t), range
+//               check (a1 / a1w)
+//   M_SEED   -- all tiles: global relabel, seed: absorb in-flight flow, h = 1 on nodes with
+//               residual capacity to t, tile-local BFS fixpoint with an INF halo        (a2)
+//   M_BFS    -- tiles whose neighbours' border heights changed: tile-local fixpoint with
+//               the neighbours' border heights as halo; a changed border requests the
+//               neighbour tiles (asynchronous Bellman-Ford over tiles, exact at
+//               quiescence)                                                            (a2)
 //               then: no active node left -> M_CSEED, else -> M_PUSH
-//   M_PUSH   -- push/relabel over active tiles (a3); ends (-> M_SEED) when the frame stops
-//               delivering flow to sink-connected nodes and reaching new tiles, or when the
-//               relabel budget of Goldberg's global-relabel heuristic is spent
-//   M_CSEED  -- canonical mask, seed pass over every tile; writes the caller's mask    (a4)
-//   M_CLOS   -- mask closure across tile borders until nothing changes               (a4)
-//   M_EXPORT -- forward-arc flows for the caller's warm-start state                 (a5)
+//   M_PUSH   -- active tiles and tiles with inbound flow: push/relabel rounds in shared
+//               memory (a3); a tile that stays active requests itself, border flow
+//               requests the receiver; ends at quiescence or when the phase's relabel /
+//               task budget (Goldberg's global-relabel heuristic) is spent -> M_SEED
+//   M_CSEED  -- all tiles: canonical mask seed, writes the caller's mask                (a4)
+//   M_CLOS   -- mask closure across tile borders until nothing changes                (a4)
+//   M_EXPORT -- all tiles: forward-arc flows for the caller's warm-start state         (a5)
 //   then the flow value is written and the slot takes the next frame (M_INIT) or idles.
-// One step = k_stream (INIT/EXPORT) + k_seed (SEED/CSEED) + k_relax (BFS/CLOS) + k_push
-// (PUSH) + k_control.  Each kernel walks the compact list of slots of its group that
-// k_control built for this step.  Parities (dirty, inbox, reach flags) follow the global
-// step counter sw.
+//
+// Scheduling.  A ring of tile ids with ticket counters (qhead, qtail).  Per frame, fout
+// counts the tasks of the running phase that are queued or running; the CTA whose task
+// brings it to zero runs the phase transition and enqueues the next phase's tasks (it
+// holds a +1 guard on fout while it enqueues).  In the request-driven phases (BFS, PUSH,
+// CLOS) treq[tile] > 0 means "queued or running": a request that finds it 0 enqueues the
+// tile; a task subtracts the requests it started with when it ends and re-enqueues the
+// tile if more arrived meanwhile -- so a tile is never processed by two CTAs at once and
+// every change a tile must react to is seen by a later run of it.  Writers fence before
+// they signal; all mutable state is read through L2.
 #pragma once
 #include "gc_kernels.cuh"
 
 namespace gcb {
 
-enum { G_STREAM = 0, G_SEED = 1, G_RELAX = 2, G_PUSH = 3, NGROUP = 4 };
+constexpr uint32_t QEMPTY = 0xffffffffu;
+constexpr uint32_t QEXIT = 0xfffffffeu;
 
-__host__ __device__ __forceinline__ int mode_group(int md) {
-  return (md == M_INIT || md == M_EXPORT) ? G_STREAM
-         : (md == M_SEED || md == M_CSEED) ? G_SEED
-         : (md == M_BFS || md == M_CLOS)   ? G_RELAX
-                                           : G_PUSH;
+struct Ctl {
+  long long relabel_budget;  // relabels per push phase (alpha x frame pixels)
+  long long max_tasks;       // watchdog: tasks per launch before GC_ERR_NOCONV
+  int vis_budget;            // push tasks per push phase
+  int stall;                 // push tasks without progress before the phase drains
+  int rounds;                // push/relabel rounds per push task
+  int nframes;
+  int vec;                   // caller rows 16-byte aligned: int4 loads in the init pass
+};
+
+// ------------------------------------------------------------------ queue primitives
+// Release/acquire fence at GPU scope (cheaper than __threadfence's sequentially consistent
+// fence); every mutable load goes to L2 (-dlcm=cg), so it is all the ordering needed.
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ void q_put(const Dev& d, unsigned long long p, uint32_t v) {
+  volatile uint32_t* slot = d.q + (p & d.qmask);
+  while (*slot != QEMPTY) __nanosleep(32);  // previous lap not consumed yet (capacity 2x: never in practice)
+  *slot = v;
 }
 
-// Mark the neighbour tiles that read a changed part of this tile's border.
-__device__ __forceinline__ void mark_neighbours(const Dev& d, int32_t* flags, size_t gt, int bits, int K) {
-  const int t = threadIdx.x;
-  if (t < 8 && ((bits >> t) & 1)) {
-    // bit: 0 N, 1 S, 2 W, 3 E, 4 NW, 5 NE, 6 SW, 7 SE
-    const int dy = (t == 0 || t == 4 || t == 5) ? -1 : ((t == 1 || t == 6 || t == 7) ? 1 : 0);
-    const int dx = (t == 2 || t == 4 || t == 6) ? -1 : ((t == 3 || t == 5 || t == 7) ? 1 : 0);
-    if (t >= 4 && K == 4) return;
-    const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-    const int ty = tile / d.TX + dy, tx = tile % d.TX + dx;
-    if (ty >= 0 && ty < d.TY && tx >= 0 && tx < d.TX) flags[(size_t)s * d.T + ty * d.TX + tx] = 1;
+// One thread: enqueue tile gt of frame slot s in a request-driven phase.  The caller has
+// fenced the writes the tile must see.
+__device__ __forceinline__ void request(const Dev& d, size_t gt, int s) {
+  if (atomicAdd(&d.treq[gt], 1) == 0) {
+    atomicAdd(&d.fout[s], 1);
+    q_put(d, atomicAdd(d.qtail, 1ULL), (uint32_t)gt);
   }
 }
 
+// Neighbour tile of gt on side b (0 N, 1 S, 2 W, 3 E, 4 NW, 5 NE, 6 SW, 7 SE); -1 if off-frame.
+__device__ __forceinline__ long long side_tile(const Dev& d, size_t gt, int b) {
+  const int dy = (b == 0 || b == 4 || b == 5) ? -1 : ((b == 1 || b == 6 || b == 7) ? 1 : 0);
+  const int dx = (b == 2 || b == 4 || b == 6) ? -1 : ((b == 3 || b == 5 || b == 7) ? 1 : 0);
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX + dy, tx = tile % d.TX + dx;
+  if (ty < 0 || ty >= d.TY || tx < 0 || tx >= d.TX) return -1;
+  return (long long)s * d.T + ty * d.TX + tx;
+}
+
+__device__ __forceinline__ int side_bit(int dy, int dx) {
+  return dy < 0 ? (dx < 0 ? 4 : (dx > 0 ? 5 : 0)) : (dy > 0 ? (dx < 0 ? 6 : (dx > 0 ? 7 : 1)) : (dx < 0 ? 2 : 3));
+}
+
+// Block-wide: flag the neighbour tiles on the sides set in `bits` as part of the first task
+// set of the next phase (the phase transition collects the flags).
+__device__ __forceinline__ void flag_sides(const Dev& d, size_t gt, int bits, int K) {
+  const int t = threadIdx.x;
+  if (t < 8 && ((bits >> t) & 1) && !(t >= 4 && K == 4)) {
+    const long long n = side_tile(d, gt, t);
+    if (n >= 0) d.flag[n] = 1;
+  }
+}
+
+// Sides of the tile whose halo reads pixel (iy, ix)'s height.
 __device__ __forceinline__ int border_bits(int iy, int ix) {
   int b = 0;
   b |= (iy == 0) << 0;
@@ -62,49 +106,25 @@ __device__ __forceinline__ int border_bits(int iy, int ix) {
   return b;
 }
 
-// Persistent-grid worklist over the tiles of the slots listed for group G in this step:
-// each CTA takes ids blockIdx.x, +gridDim.x, ... 256 at a time, compacts those passing
-// TILEPRED in shared memory and processes them one by one (block-wide body).
-#define GC_LIST_BEGIN(G, TILEPRED)                                                        \
-  __shared__ int wl_[NTH];                                                                \
-  __shared__ int wn_;                                                                     \
-  const size_t ns_ = NS(d);                                                               \
-  const int lb_ = sw & 1;                                                                 \
-  const int cnt_ = d.lcnt[lb_ * NGROUP + (G)];                                            \
-  const int* sl_ = d.slist + ((size_t)lb_ * NGROUP + (G)) * d.nslot;                      \
-  const size_t tot_ = (size_t)cnt_ * d.T;                                                 \
-  for (size_t base_ = 0; base_ < tot_; base_ += (size_t)NTH * gridDim.x) {                \
-    const size_t k_ = base_ + (size_t)threadIdx.x * gridDim.x + blockIdx.x;               \
-    int want_ = 0;                                                                        \
-    size_t id = 0;                                                                        \
-    if (k_ < tot_) {                                                                      \
-      const int li_ = (int)(k_ / d.T);                                                    \
-      id = (size_t)sl_[li_] * d.T + (k_ - (size_t)li_ * d.T);                             \
-      want_ = (TILEPRED);                                                                 \
-    }                                                                                     \
-    if (threadIdx.x == 0) wn_ = 0;                                                        \
-    __syncthreads();                                                                      \
-    if (want_) wl_[atomicAdd(&wn_, 1)] = (int)id;                                         \
-    __syncthreads();                                                                      \
-    const int n_ = wn_;                                                                   \
-    for (int i_ = 0; i_ < n_; ++i_) {                                                     \
-      const size_t gt = (size_t)wl_[i_];                                                  \
-      const int md = d.fmode[gt / d.T];
-#define GC_LIST_END \
-  __syncthreads();  \
-  }                 \
-  __syncthreads();  \
-  }
-
-// ---------------------------------------------------------------- a2: seed pass (one tile)
+// ---------------------------------------------------------------- a2: seed (one tile)
+// Absorbs flow still in flight from the push phase (materialising e, r pixel at a time),
+// seeds h = 1 where the node has residual capacity to t, relaxes to the tile-local
+// fixpoint with an INF halo, and flags the tiles that must be relaxed first: the
+// neighbours that see a finite border height, and itself if a neighbour is a uniform sink
+// tile (whose seed is skipped: nothing can have changed in it).
 template <int K>
-__device__ __forceinline__ void tile_seed(const Dev& d, const IO& io, size_t gt, int sw, int* hs) {
+__device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt, int* hs, int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const size_t ns = NS(d);
   const int s = (int)(gt / d.T);
-  const int par_in = (sw - 1) & 1;
+  if (t == 0) {
+    bc[0] = __ldcg(d.recv1 + gt);
+    bc[2] = __ldcg(d.tuni + gt);
+  }
+  __syncthreads();
+  const int rcv = bc[0];
+  if (bc[2] && !rcv) return;  // untouched uniform sink tile: h = 1, hedge published
   int fl[4];
-  if (d.recv[par_in * ns + gt]) {  // flow still in flight from the last push step
+  if (rcv) {
     const int tile = (int)(gt - (size_t)s * d.T);
     const int ty = tile / d.TX, tx = tile - ty * d.TX;
 #pragma unroll 1
@@ -117,9 +137,8 @@ __device__ __forceinline__ void tile_seed(const Dev& d, const IO& io, size_t gt,
         for (int k = 0; k < K; ++k) {
           const int wy = iy - DYk(k), wx = ix - DXk(k);
           if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-          int32_t* p = INBp(d, K, par_in, gt, k) + recv_slot(k, iy, ix);
-          const int dl = *p;
-          if (dl) { e += dl; r[k ^ 1] += dl; *p = 0; }
+          const int dl = take_inflow<K>(d, gt, k, iy, ix);
+          if (dl) { e += dl; r[k ^ 1] += dl; }
         }
       }
       d.e[gt * TPX + lp] = e;
@@ -128,29 +147,66 @@ __device__ __forceinline__ void tile_seed(const Dev& d, const IO& io, size_t gt,
       fl[j] = make_fl<K>(e, r);
       d.fl[gt * TPX + lp] = (uint16_t)fl[j];
     }
-    __syncthreads();
-    if (t == 0) { d.mat[gt] = 1; d.recv[par_in * ns + gt] = 0; }
+    if (t == 0) { d.mat[gt] = 1; d.recv1[gt] = 0; }
   } else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
   }
-  const int act = bfs_seed_tile<K>(d, gt, hs, fl);
+  for (int i = t; i < HS * HS; i += NTH) hs[i] = HINF;
+  __syncthreads();
+  int h[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    h[j] = (fl[j] & FL_NEG) ? 1 : HINF;
+    hs[hidx(iy0 + 8 * j, ix)] = h[j];
+  }
+  __syncthreads();
+  bfs_fixpoint<K>(hs, fl, h);
+  int act = 0, fix = 1, uni = 1, bits = 0;
+  const int tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int iy = iy0 + 8 * j;
+    d.h[gt * TPX + iy * TS + ix] = h[j];
+    act |= (fl[j] & FL_POS) && h[j] < HINF;
+    fix &= (h[j] == 1) || !(fl[j] & 0xff);
+    const bool in = ty * TS + iy < d.H && tx * TS + ix < d.W;
+    uni &= !in || (fl[j] & FL_NEG);
+    if (on_border(iy, ix) && h[j] < HINF) bits |= border_bits(iy, ix);
+  }
+  store_hedge(d, gt, h, t);
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if (t == 0) bc[1] = 0;
+  act = __syncthreads_or(act);
+  fix = __syncthreads_and(fix);
+  uni = __syncthreads_and(uni);
+  if ((t & 31) == 0 && bits) atomicOr(&bc[1], bits);
+  // a uniform sink neighbour (seed skipped) cannot flag this tile: flag it here
+  int self = 0;
+  if (t < 8 && !(t >= 4 && K == 4)) {
+    const long long n = side_tile(d, gt, t);
+    self = n >= 0 && __ldcg(d.tuni + n);
+  }
+  self = __syncthreads_or(self);
   if (t == 0) {
     d.tact[gt] = act;
-    d.dirty[(sw & 1) * ns + gt] = 1;
-    d.fchg[(sw & 1) * d.nslot + s] = 1;
+    d.tfix[gt] = fix;
+    d.tuni[gt] = uni;
+    if (self && !fix) d.flag[gt] = 1;
   }
+  flag_sides(d, gt, bc[1], K);
 }
 
-// ---------------------------------------------------------------- a2: relax pass (one tile)
+// ---------------------------------------------------------------- a2: relax (one tile)
+// Returns (in bc[1]) the sides whose tiles must be requested: their halo reads a changed
+// border height.
 template <int K>
-__device__ __forceinline__ void tile_relax(const Dev& d, size_t gt, int sw, int* hs, int* bits_s) {
+__device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const size_t ns = NS(d);
-  const int cur = sw & 1, prv = cur ^ 1;
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  if (t == 0) { d.dirty[prv * ns + gt] = 0; *bits_s = 0; }
+  if (t == 0) bc[1] = 0;
   int fl[4], h[4], h0[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -162,27 +218,25 @@ __device__ __forceinline__ void tile_relax(const Dev& d, size_t gt, int sw, int*
   load_halo(d, s, ty, tx, hs, t);
   __syncthreads();
   bfs_fixpoint<K>(hs, fl, h);
-  int any = 0, bits = 0, act = 0;
+  int any = 0, bits = 0, act = 0, fix = 1;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int ch = h[j] != h0[j];
     any |= ch;
     if (ch) bits |= border_bits(iy0 + 8 * j, ix);
     act |= (fl[j] & FL_POS) && h[j] < HINF;
+    fix &= (h[j] == 1) || !(fl[j] & 0xff);
   }
-  if (bits) atomicOr(bits_s, bits);
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if ((t & 31) == 0 && bits) atomicOr(&bc[1], bits);
   any = __syncthreads_or(any);
   act = __syncthreads_or(act);
+  fix = __syncthreads_and(fix);
   if (any) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
     store_hedge(d, gt, h, t);
-    if (t == 0) d.tact[gt] = act;
-  }
-  const int b = *bits_s;
-  if (b) {
-    mark_neighbours(d, d.dirty + cur * ns, gt, b, K);
-    if (t == 0) d.fchg[cur * d.nslot + s] = 1;
+    if (t == 0) { d.tact[gt] = act; d.tfix[gt] = fix; }
   }
 }
 
@@ -217,14 +271,14 @@ __device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uin
   }
 }
 
+// Sets the reach bits of the border arcs leaving newly reached pixels; returns the sides
+// (side_bit) of the neighbour tiles that received bits.
 template <int K>
-__device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os,
-                                            int par_out) {
+__device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const size_t ns = NS(d);
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  int sent = 0;
+  int sides = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j;
@@ -234,16 +288,15 @@ __device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (
     for (int k = 0; k < K; ++k) {
       if (!crosses(k, iy, ix) || !((ob >> k) & 1)) continue;
       const int y2 = iy + DYk(k), x2 = ix + DXk(k);
-      const int rty = ty + (y2 < 0 ? -1 : (y2 > 31 ? 1 : 0));
-      const int rtx = tx + (x2 < 0 ? -1 : (x2 > 31 ? 1 : 0));
+      const int dy = y2 < 0 ? -1 : (y2 > 31 ? 1 : 0), dx = x2 < 0 ? -1 : (x2 > 31 ? 1 : 0);
+      const int rty = ty + dy, rtx = tx + dx;
       if (rty < 0 || rty >= d.TY || rtx < 0 || rtx >= d.TX) continue;
       const size_t rgt = (size_t)s * d.T + rty * d.TX + rtx;
       d.reach[(rgt * K + k) * 64 + recv_slot(k, y2 & 31, x2 & 31)] = 1;
-      d.crecv[par_out * ns + rgt] = 1;
-      sent = 1;
+      sides |= 1 << side_bit(dy, dx);
     }
   }
-  return sent;
+  return sides;
 }
 
 __device__ __forceinline__ void write_mask(const Dev& d, const IO& io, size_t gt, const int (&mm)[4],
@@ -260,12 +313,23 @@ __device__ __forceinline__ void write_mask(const Dev& d, const IO& io, size_t gt
   }
 }
 
+// OR of per-thread side bits into bc[1] (block-wide); returns it.
+__device__ __forceinline__ int block_or_bits(int bits, int* bc) {
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if (threadIdx.x == 0) bc[1] = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(&bc[1], bits);
+  __syncthreads();
+  return bc[1];
+}
+
 // ---------------------------------------------------------------- a4: closure seed (one tile)
-// Every tile: m = (e > 0) closed inside the tile; writes m and the caller's mask; sends
-// reach bits across the border; adds the tile's sum max(0,-e) to the flow value's sum.
+// Every tile: m = (e > 0) closed inside the tile; writes m and the caller's mask; sets reach
+// bits across the border (flagging the receivers for the closure phase); adds the tile's
+// sum max(0,-e) to the flow value's sum.
 template <int K>
-__device__ __forceinline__ void tile_cseed(const Dev& d, const IO& io, size_t gt, int sw, uint8_t* ms, uint8_t* os,
-                                           long long* red) {
+__device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
+                                           long long* red, int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)(gt / d.T);
   const int all[4] = {1, 1, 1, 1};
@@ -294,8 +358,7 @@ __device__ __forceinline__ void tile_cseed(const Dev& d, const IO& io, size_t gt
 #pragma unroll
   for (int j = 0; j < 4; ++j) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = (uint8_t)mm[j];
   write_mask(d, io, gt, mm, all);
-  int sent = closure_send<K>(d, gt, mm, os, sw & 1);
-  sent = __syncthreads_or(sent);
+  const int sides = block_or_bits(closure_send<K>(d, gt, mm, os), bc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
   if ((t & 31) == 0) red[t >> 5] = neg;
@@ -308,17 +371,15 @@ __device__ __forceinline__ void tile_cseed(const Dev& d, const IO& io, size_t gt
       tot = d.neg0[gt];
     }
     if (tot) atomicAdd(&d.sumneg[s], (unsigned long long)tot);
-    if (sent) d.fchg[(sw & 1) * d.nslot + s] = 1;
   }
+  flag_sides(d, gt, sides, K);
 }
 
 // ---------------------------------------------------------------- a4: closure relax (one tile)
 template <int K>
-__device__ __forceinline__ void tile_crelax(const Dev& d, const IO& io, size_t gt, int sw, uint8_t* ms, uint8_t* os) {
+__device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
+                                            int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const size_t ns = NS(d);
-  const int cur = sw & 1, prv = cur ^ 1;
-  const int s = (int)(gt / d.T);
   int mm[4], m0[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -331,14 +392,13 @@ __device__ __forceinline__ void tile_crelax(const Dev& d, const IO& io, size_t g
       for (int k = 0; k < K; ++k) {
         const int wy = iy - DYk(k), wx = ix - DXk(k);
         if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-        got |= d.reach[(gt * K + k) * 64 + recv_slot(k, iy, ix)];
+        got |= __ldcg(d.reach + (gt * K + k) * 64 + recv_slot(k, iy, ix));
       }
     }
     mm[j] = got;
     ms[lp] = (uint8_t)got;
   }
   __syncthreads();
-  if (t == 0) d.crecv[prv * ns + gt] = 0;
   closure_fixpoint<K>(ms, os, mm);
   int nw[4], any = 0;
 #pragma unroll
@@ -347,21 +407,20 @@ __device__ __forceinline__ void tile_crelax(const Dev& d, const IO& io, size_t g
     any |= nw[j];
   }
   any = __syncthreads_or(any);
+  if (t == 0) bc[1] = 0;
   if (any) {
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (nw[j]) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = 1;
     write_mask(d, io, gt, mm, nw);
-    int sent = closure_send<K>(d, gt, nw, os, cur);
-    sent = __syncthreads_or(sent);
-    if (t == 0 && sent) d.fchg[cur * d.nslot + s] = 1;
+    block_or_bits(closure_send<K>(d, gt, nw, os), bc);  // sides to request, in bc[1]
   }
 }
 
 // ---------------------------------------------------------------- a5: export (one tile)
 // Forward-arc flows f = c - r of this solve (the next frame's warm start).
 template <int K>
-__device__ __forceinline__ void tile_export(const Dev& d, const IO& io, size_t gt) {
+__device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t gt) {
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
@@ -385,110 +444,71 @@ __device__ __forceinline__ void tile_export(const Dev& d, const IO& io, size_t g
   }
 }
 
-// ---------------------------------------------------------------- step kernels
-template <int K>
-__global__ void __launch_bounds__(NTH, 4) k_stream(Dev d, IO io, int sw, int vec) {
-  __shared__ long long red[2][NTH / 32];
-  GC_LIST_BEGIN(G_STREAM, 1)
-  if (md == M_INIT) {
-    count_tile(d, 0);
-    tile_init<K>(d, io, gt, vec != 0, red);
-  } else {
-    count_tile(d, 5);
-    tile_export<K>(d, io, gt);
-  }
-  GC_LIST_END
-}
-
-template <int K>
-__global__ void __launch_bounds__(NTH, 4) k_seed(Dev d, IO io, int sw) {
-  __shared__ int hs[HS * HS];
-  __shared__ long long red[NTH / 32];
-  uint8_t* ms = reinterpret_cast<uint8_t*>(hs);  // closure tiles reuse the height buffer
-  uint8_t* os = ms + TPX;
-  GC_LIST_BEGIN(G_SEED, 1)
-  if (md == M_SEED) {
-    count_tile(d, 1);
-    tile_seed<K>(d, io, gt, sw, hs);
-  } else {
-    count_tile(d, 4);
-    tile_cseed<K>(d, io, gt, sw, ms, os, red);
-  }
-  GC_LIST_END
-}
-
-template <int K>
-__global__ void __launch_bounds__(NTH, 4) k_relax(Dev d, IO io, int sw) {
-  __shared__ int hs[HS * HS];
-  __shared__ int bits_s;
-  uint8_t* ms = reinterpret_cast<uint8_t*>(hs);
-  uint8_t* os = ms + TPX;
-  const int prv = (sw & 1) ^ 1;
-  GC_LIST_BEGIN(G_RELAX, (d.fmode[id / d.T] == M_BFS ? d.dirty[prv * ns_ + id] : d.crecv[prv * ns_ + id]))
-  if (md == M_BFS) {
-    count_tile(d, 1);
-    tile_relax<K>(d, gt, sw, hs, &bits_s);
-  } else {
-    count_tile(d, 4);
-    tile_crelax<K>(d, io, gt, sw, ms, os);
-  }
-  GC_LIST_END
-}
-
-// ---------------------------------------------------------------- a3: k_push
-// Up to `rounds` synchronous push / relabel rounds inside each active tile (or tile with
-// inbound flow) of the slots in M_PUSH (4x the rounds once a push phase has run 8 steps:
-// long-distance transport).  e, r and two height buffers live in shared memory.  Push
-// phase: every active pixel v (e > 0, finite h) pushes delta = min(e, r_k) along admissible
-// arcs (h(u) = h(v) - 1): it lowers its own r_k, raises r_opp(u) (unique writer: u cannot
-// push back to v in the same round) and moves delta between e(v) and e(u) with shared-memory
-// atomics.  Relabel phase (Jacobi): h'(v) = 1 + min h(u) over residual arcs for active
-// pixels without an admissible arc.  Pushes across the tile border accumulate per receiver
-// slot and go to the receiver tile's inbox at the end (absorbed at its next step).  Border
-// heights are those of the previous step (stale); the exact global relabel restores valid
-// labels and certifies termination.
+// ---------------------------------------------------------------- a3: push (one tile)
+// Up to `rounds` synchronous push / relabel rounds inside the tile.  e, r and two height
+// buffers live in shared memory.  Push phase: every active pixel v (e > 0, finite h)
+// pushes delta = min(e, r_k) along admissible arcs (h(u) = h(v) - 1): it lowers its own
+// r_k, raises r_opp(u) (unique writer: u cannot push back to v in the same round) and
+// moves delta between e(v) and e(u) with shared-memory atomics.  Relabel phase (Jacobi):
+// h'(v) = 1 + min h(u) over residual arcs for active pixels without an admissible arc.
+// Pushes across the tile border accumulate per receiver slot and are added to the
+// receiver's cumulative `sent` counters at the end; the receiver is requested.  Border
+// heights are the neighbours' last published ones (possibly stale); the exact global
+// relabel restores valid labels and certifies termination.
 template <int K>
 constexpr size_t push_smem_bytes() { return sizeof(int) * (2 * HS * HS + TPX + K * TPX + K * 64); }
 
+// Returns the sides whose tiles received border flow in bc[1] and "still active" in bc[3].
 template <int K>
-__global__ void __launch_bounds__(NTH, 4) k_push(Dev d, IO io, int sw, int rounds) {
+__device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt, const Ctl& c, int* smem, int* bc,
+                                          long long* red) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  extern __shared__ int smem_push[];  // push_smem_bytes<K>() of dynamic shared memory
-  int(*hb)[HS * HS] = reinterpret_cast<int(*)[HS * HS]>(smem_push);  // heights, 2 buffers
-  int* es = smem_push + 2 * HS * HS;                                  // excess
-  int* rs = es + TPX;                                                 // residuals [K][TPX]
-  int(*oacc)[64] = reinterpret_cast<int(*)[64]>(rs + K * TPX);        // border pushes by slot
+  int(*hb)[HS * HS] = reinterpret_cast<int(*)[HS * HS]>(smem);  // heights, 2 buffers
+  int* es = smem + 2 * HS * HS;                                   // excess
+  int* rs = es + TPX;                                             // residuals [K][TPX]
+  int(*oacc)[64] = reinterpret_cast<int(*)[64]>(rs + K * TPX);    // border pushes by slot
   const int hmax = d.hmax;
-  const int par_out = sw & 1, par_in = par_out ^ 1;
-  GC_LIST_BEGIN(G_PUSH, (d.tact[id] || d.recv[par_in * ns_ + id]))
-  (void)md;
-  count_tile(d, 2);
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const int rcv = d.recv[par_in * ns_ + gt];
-  const int nround = d.fpush[s] >= 8 ? 4 * rounds : rounds;
-  long long neg0 = 0;
+  if (t == 0) {
+    // phase budget spent or no progress lately: the frame drains to the next global relabel
+    const int vis = __ldcg(d.fvis + s);
+    bc[0] = ((long long)__ldcg(d.frel + s) > c.relabel_budget) || (vis >= c.vis_budget) ||
+            (vis - __ldcg(d.fprog + s) > c.stall);
+    bc[1] = 0;
+    bc[2] = __ldcg(d.recv1 + gt);
+    bc[3] = 0;
+    bc[4] = __ldcg(d.tuni + gt);
+  }
+  __syncthreads();
+  if (bc[0]) return;
+  const int rcv = bc[2], uni = bc[4];
   tile_load_smem<K>(d, io, gt, es, rs);
+  long long neg0 = 0;  // deficit of the tile before the task (flow absorbed = progress)
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int ev = es[(iy0 + 8 * j) * TS + ix];
     neg0 += ev < 0 ? -(long long)ev : 0;
   }
-  if (rcv) absorb_smem<K>(d, par_in, gt, es, rs);
+  if (rcv) {
+    if (t == 0) d.recv1[gt] = 0;
+    absorb_smem<K>(d, gt, es, rs);
+  }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int hv = d.h[gt * TPX + (iy0 + 8 * j) * TS + ix];
-    hb[0][hidx(iy0 + 8 * j, ix)] = hv;
-    hb[1][hidx(iy0 + 8 * j, ix)] = hv;
+    const int iy = iy0 + 8 * j;
+    // a uniform sink tile's heights are not stored: h = 1 in frame
+    const int hv = uni ? ((ty * TS + iy < d.H && tx * TS + ix < d.W) ? 1 : HINF) : d.h[gt * TPX + iy * TS + ix];
+    hb[0][hidx(iy, ix)] = hv;
+    hb[1][hidx(iy, ix)] = hv;
   }
   load_halo(d, s, ty, tx, hb[0], t);
   load_halo(d, s, ty, tx, hb[1], t);
   for (int i = t; i < K * 64; i += NTH) (&oacc[0][0])[i] = 0;
   __syncthreads();
-  if (rcv && t == 0) d.recv[par_in * ns_ + gt] = 0;
-  int nrel = 0;  // relabel operations (global-relabel heuristic, k_control)
+  int nrel = 0;  // relabel operations (global-relabel heuristic)
   int cb = 0;    // current height buffer
-  for (int rd = 0; rd < nround; ++rd) {
+  for (int rd = 0; rd < c.rounds; ++rd) {
     const int* hc = hb[cb];
     // push phase (owner)
 #pragma unroll 1
@@ -566,7 +586,8 @@ __global__ void __launch_bounds__(NTH, 4) k_push(Dev d, IO io, int sw, int round
     tile_store_smem<K>(d, gt, es, rs);
     store_hedge(d, gt, h, t);
   }
-  // send border pushes to the neighbours' inboxes (unique writer per slot)
+  // border pushes: add to the receivers' cumulative counters (unique writer per slot)
+  int sides = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j;
@@ -578,44 +599,48 @@ __global__ void __launch_bounds__(NTH, 4) k_push(Dev d, IO io, int sw, int round
       const int sl = recv_slot(k, y2 & 31, x2 & 31);
       const int dl = oacc[k][sl];
       if (dl) {
-        const int rty = ty + (y2 < 0 ? -1 : (y2 > 31 ? 1 : 0));
-        const int rtx = tx + (x2 < 0 ? -1 : (x2 > 31 ? 1 : 0));
-        const size_t rgt = (size_t)s * d.T + rty * d.TX + rtx;
-        INBp(d, K, par_out, rgt, k)[sl] = dl;
-        d.recv[par_out * ns_ + rgt] = 1;
+        const int dy = y2 < 0 ? -1 : (y2 > 31 ? 1 : 0), dx = x2 < 0 ? -1 : (x2 > 31 ? 1 : 0);
+        const size_t rgt = (size_t)s * d.T + (ty + dy) * d.TX + (tx + dx);
+        uint32_t* p = SENTp(d, K, rgt, k) + sl;
+        *p = *p + (uint32_t)dl;
+        d.recv1[rgt] = 1;
+        sides |= 1 << side_bit(dy, dx);
       }
     }
   }
   act = __syncthreads_or(act);
-  // progress counters of this step (k_control): flow delivered to sink-connected nodes,
-  // relabels, tiles touched for the first time in this push phase
+  sides = block_or_bits(sides, bc);
+  // progress counters: relabels of this phase, tasks, flow absorbed by deficit nodes
   long long absorbed = neg0 - neg1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     nrel += __shfl_xor_sync(0xffffffffu, nrel, o);
     absorbed += __shfl_xor_sync(0xffffffffu, absorbed, o);
   }
-  if ((t & 31) == 0) {
-    if (nrel) atomicAdd(&d.frel[s], (unsigned long long)nrel);
-    if (absorbed > 0) atomicAdd(&d.fabs_[s], (unsigned long long)absorbed);
-  }
+  if ((t & 31) == 0) red[t >> 5] = absorbed;
+  if ((t & 31) == 0 && nrel) atomicAdd(&d.frel[s], (unsigned long long)nrel);
+  __syncthreads();
   if (t == 0) {
+    long long ab = 0;
+    for (int i = 0; i < NTH / 32; ++i) ab += red[i];
+    const int ph = d.fph[s];
+    const bool first = d.tph[gt] != ph;  // first visit in this phase: transport progress
+    d.tph[gt] = ph;
     d.tact[gt] = act;
     d.mat[gt] = 1;
-    const int ph = d.fph[s];
-    if (d.tph[gt] != ph) {
-      d.tph[gt] = ph;
-      atomicAdd(&d.fnew[s], 1);
-    }
+    d.tuni[gt] = 0;
+    d.tfix[gt] = 0;
+    const int v = atomicAdd(&d.fvis[s], 1) + 1;
+    if (ab > 0 || first) atomicMax(&d.fprog[s], v);
+    atomicAdd(&d.fstat[s * 4 + 0], 1);
+    bc[3] = act;
   }
-  GC_LIST_END
 }
 
-// ---------------------------------------------------------------- k_control
-// Advances every slot's state machine after a step (one CTA per slot), finishes frames
-// (flow value, stats), refills finished slots with the next frame, and builds the slot
-// lists of the next step.  F = sum c(v,t) - sum max(0,-e): the flow that reached t.
-__device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s) {
+// ---------------------------------------------------------------- transitions
+enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3 };
+
+__device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
   const int f = d.sfr[s];
   int st = 0;
   long long F = (long long)d.sumct[s] - (long long)d.sumneg[s];
@@ -627,99 +652,257 @@ __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s) 
     io.stats[f * 4 + 2] = d.fstat[s * 4 + 2];
     io.stats[f * 4 + 3] = st;
   }
-  atomicAdd(&d.gctr[1], 1);
+  if (atomicAdd(&d.gctr[1], 1) + 1 == c.nframes) {
+    __threadfence();
+    *(volatile int*)&d.done[0] = 1;
+  }
 }
 
-__global__ void __launch_bounds__(NTH) k_control(Dev d, IO io, int sw, long long relabel_budget, int max_push,
-                                                 int nframes) {
-  const int s = blockIdx.x, t = threadIdx.x;
-  const int cur = sw & 1, nxt = cur ^ 1;
-  if (s == 0 && t < NGROUP) d.lcnt[cur * NGROUP + t] = 0;  // this step's lists are consumed
-  const int md = d.fmode[s];
-  if (md == M_IDLE) return;
-  const int chg = d.fchg[cur * d.nslot + s];
-  int nact = 0;
-  if (md == M_BFS && !chg) {  // relabel converged: any active node left that reaches t?
-    for (int i = t; i < d.T; i += NTH) nact |= d.tact[(size_t)s * d.T + i];
+// Run by one CTA when the phase of slot s has no task left (fout[s] == 0): decide the next
+// phase and enqueue its tasks.  Loops while a phase turns out to have no task at all.
+__device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const Ctl& c, int* bc) {
+  const int t = threadIdx.x;
+  if (t == 0) atomicAdd(&d.fout[s], 1);  // guard: no other CTA can see fout == 0 while we enqueue
+  for (;;) {
+    fence_gpu();
+    const int md = __ldcg(d.fmode + s);
+    int nact = 0;
+    if (md == M_BFS) {
+      for (int i = t; i < d.T; i += NTH) nact |= __ldcg(d.tact + (size_t)s * d.T + i);
+    }
     nact = __syncthreads_or(nact);
+    if (t == 0) {
+      int nm = md, kind = SET_ALL;
+      int* st = d.fstat + s * 4;
+      bool finished = false;
+      if (md == M_INIT) {
+        nm = d.ferr[s] ? M_CSEED : M_SEED;
+      } else if (md == M_SEED) {
+        nm = M_BFS;
+        kind = SET_FLAG;
+        st[1] += 1;
+      } else if (md == M_BFS) {
+        if (nact) {
+          nm = M_PUSH;
+          kind = SET_TACT;
+          d.frel[s] = 0;
+          d.fvis[s] = 0;
+          d.fprog[s] = 0;
+          d.fph[s] += 1;
+        } else {
+          nm = M_CSEED;  // termination certificate: the preflow is maximum
+        }
+      } else if (md == M_PUSH) {
+        nm = M_SEED;
+      } else if (md == M_CSEED) {
+        nm = M_CLOS;
+        kind = SET_FLAG;
+      } else if (md == M_CLOS) {
+        if (io.fstate && !d.ferr[s]) nm = M_EXPORT;
+        else finished = true;
+      } else if (md == M_EXPORT) {
+        finished = true;
+      }
+      if (finished) {
+        finish_frame(d, io, s, c);
+        const int nf = atomicAdd(&d.gctr[0], 1);
+        if (nf < c.nframes) {  // refill the slot with the next frame of the batch
+          d.sfr[s] = nf;
+          d.ferr[s] = 0;
+          d.fph[s] = 0; d.fvis[s] = 0; d.fprog[s] = 0;
+          st[0] = st[1] = st[2] = st[3] = 0;
+          d.frel[s] = 0; d.sumct[s] = 0; d.sumneg[s] = 0;
+          nm = M_INIT;
+        } else {
+          nm = M_IDLE;
+          kind = SET_NONE;
+        }
+      }
+      d.fmode[s] = nm;
+      bc[4] = kind;
+    }
+    __syncthreads();
+    const int kind = bc[4];
+    if (kind == SET_NONE) break;
+    // enqueue the phase's first task set, NTH tiles at a time
+    const size_t base_gt = (size_t)s * d.T;
+    for (int b0 = 0; b0 < d.T; b0 += NTH) {
+      const int i = b0 + t;
+      int want = 0;
+      if (i < d.T) {
+        const size_t gt = base_gt + i;
+        if (kind == SET_ALL) want = 1;
+        else if (kind == SET_FLAG) {
+          want = __ldcg(d.flag + gt);
+          if (want) d.flag[gt] = 0;
+          if (md == M_SEED && __ldcg(d.tfix + gt)) want = 0;  // a relax cannot change it
+        }
+        else want = __ldcg(d.tact + gt);
+        if (want && kind != SET_ALL) d.treq[gt] = 1;
+      }
+      if (t == 0) bc[5] = 0;
+      __syncthreads();
+      int li = want ? atomicAdd(&bc[5], 1) : 0;
+      fence_gpu();
+      __syncthreads();
+      const int cnt = bc[5];
+      if (cnt == 0) continue;
+      if (t == 0) {
+        atomicAdd(&d.fout[s], cnt);
+        const unsigned long long p0 = atomicAdd(d.qtail, (unsigned long long)cnt);
+        bc[6] = (int)(p0 & 0xffffffffu);
+        bc[7] = (int)(p0 >> 32);
+      }
+      __syncthreads();
+      const unsigned long long p0 = ((unsigned long long)(uint32_t)bc[7] << 32) | (uint32_t)bc[6];
+      if (want) q_put(d, p0 + li, (uint32_t)(base_gt + i));
+      __syncthreads();
+    }
+    if (t == 0) {
+      const int left = atomicSub(&d.fout[s], 1) - 1;
+      if (left == 0) atomicAdd(&d.fout[s], 1);  // every task already done (or none): go on
+      bc[4] = left;
+    }
+    __syncthreads();
+    if (bc[4] != 0) break;
   }
-  if (t != 0) return;
-  int nm = md;
-  int* st = d.fstat + s * 4;
-  bool finished = false;
-  if (md == M_INIT) {
-    nm = d.ferr[s] ? M_CSEED : M_SEED;
-  } else if (md == M_SEED) {
-    nm = M_BFS;
-    st[1] += 1;
-  } else if (md == M_BFS) {
-    st[2] += 1;
-    if (!chg) {
-      if (nact) {
-        nm = M_PUSH;
-        d.fpush[s] = 0;
-        d.fstall[s] = 0;
-        d.frel[s] = 0;
-        d.fabs_[s] = 0;
-        d.fnew[s] = 0;
-        d.fph[s] += 1;
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- the persistent kernel
+template <int K>
+__global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
+  extern __shared__ int smem[];
+  __shared__ int bc[8];
+  __shared__ long long red[NTH / 32];
+  __shared__ uint32_t task_s;
+  const int t = threadIdx.x;
+  const bool prof = d.pns != nullptr;
+  unsigned long long t_idle = 0;
+  for (;;) {
+    if (t == 0) {
+      uint64_t w0 = 0;
+      if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0));
+      const unsigned long long tk = atomicAdd(d.qhead, 1ULL);
+      volatile uint32_t* slot = d.q + (tk & d.qmask);
+      uint32_t v;
+      int ns = 32, spins = 0;
+      while ((v = *slot) == QEMPTY) {
+        if (*(volatile int*)&d.done[0] || *(volatile int*)&d.done[1]) { v = QEXIT; break; }
+        if ((++spins & 255) == 0 && *d.hostabort) { *(volatile int*)&d.done[1] = 1; v = QEXIT; break; }
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : 1024;
+      }
+      if (v != QEXIT) {
+        *slot = QEMPTY;
+        if (atomicAdd(d.ntask, 1ULL) >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
+      }
+      if (prof) {
+        uint64_t w1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
+        t_idle += w1 - w0;
+      }
+      task_s = v;
+    }
+    __syncthreads();
+    const uint32_t v = task_s;
+    if (v == QEXIT || *(volatile int*)&d.done[1]) break;
+    const size_t gt = v;
+    const int s = (int)(gt / d.T);
+    const int md = __ldcg(d.fmode + s);
+    const bool reqd = md == M_BFS || md == M_PUSH || md == M_CLOS;  // request-driven phase
+    int c0 = 0;
+    uint64_t w0 = 0;
+    if (t == 0) {
+      if (reqd) c0 = atomicAdd(&d.treq[gt], 0);
+      fence_gpu();  // acquire: the writes of the task's producers
+      if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0));
+      bc[1] = 0;
+      bc[3] = 0;
+    }
+    __syncthreads();
+    int cls = 0;
+    switch (md) {
+      case M_INIT: tile_init<K>(d, io, gt, c.vec != 0, reinterpret_cast<long long(*)[NTH / 32]>(smem)); cls = 0; break;
+      case M_SEED: task_seed<K>(d, io, gt, smem, bc); cls = 1; break;
+      case M_BFS:
+        task_relax<K>(d, gt, smem, bc);
+        if (t == 0) atomicAdd(&d.fstat[s * 4 + 2], 1);
+        cls = 1;
+        break;
+      case M_PUSH: task_push<K>(d, io, gt, c, smem, bc, red); cls = 2; break;
+      case M_CSEED:
+        task_cseed<K>(d, io, gt, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, red, bc);
+        cls = 4;
+        break;
+      case M_CLOS:
+        task_crelax<K>(d, io, gt, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, bc);
+        cls = 4;
+        break;
+      default: task_export<K>(d, io, gt); cls = 5; break;
+    }
+    // release this task's writes, then request the neighbour tiles it changed
+    fence_gpu();
+    __syncthreads();
+    if (reqd) {
+      const int bits = bc[1];
+      if (t < 8 && ((bits >> t) & 1) && !(t >= 4 && K == 4)) {
+        const long long n = side_tile(d, gt, t);
+        if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) request(d, (size_t)n, s);
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      int last = 0;
+      if (reqd) {
+        const int sub = c0 - (bc[3] ? 1 : 0);  // a push task still active keeps one request
+        const int rem = atomicSub(&d.treq[gt], sub) - sub;
+        if (rem > 0) q_put(d, atomicAdd(d.qtail, 1ULL), (uint32_t)gt);  // requested meanwhile: run again
+        else last = atomicSub(&d.fout[s], 1) == 1;
       } else {
-        nm = M_CSEED;  // termination certificate: the preflow is maximum
+        last = atomicSub(&d.fout[s], 1) == 1;
+      }
+      bc[3] = last;
+      if (prof) {
+        uint64_t w1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
+        atomicAdd(&d.pns[cls], (unsigned long long)(w1 - w0));
+        atomicAdd(&d.ptiles[cls], 1ULL);
       }
     }
-  } else if (md == M_PUSH) {
-    st[0] += 1;
-    const int np = ++d.fpush[s];
-    const bool stalled = d.fabs_[s] == 0 && d.fnew[s] == 0;
-    d.fabs_[s] = 0;
-    d.fnew[s] = 0;
-    const int stall = stalled ? ++d.fstall[s] : (d.fstall[s] = 0);
-    if (stall >= 1 + np / 4 || d.frel[s] > (unsigned long long)relabel_budget || np >= max_push) nm = M_SEED;
-  } else if (md == M_CSEED || md == M_CLOS) {
-    if (chg) nm = M_CLOS;
-    else if (io.fstate && !d.ferr[s]) nm = M_EXPORT;
-    else finished = true;
-  } else if (md == M_EXPORT) {
-    finished = true;
-  }
-  if (finished) {
-    finish_frame(d, io, s);
-    const int nf = atomicAdd(&d.gctr[0], 1);
-    if (nf < nframes) {  // refill the slot with the next frame of the batch
-      d.sfr[s] = nf;
-      d.ferr[s] = 0;
-      d.fph[s] = 0; d.fpush[s] = 0; d.fnew[s] = 0; d.fstall[s] = 0;
-      d.fchg[cur * d.nslot + s] = 0;
-      st[0] = st[1] = st[2] = st[3] = 0;
-      d.fabs_[s] = 0; d.frel[s] = 0; d.sumct[s] = 0; d.sumneg[s] = 0;
-      nm = M_INIT;
-    } else {
-      nm = M_IDLE;
+    __syncthreads();
+    if (bc[3]) {
+      uint64_t w0t = 0;
+      if (prof && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0t));
+      transition(d, io, s, c, bc);
+      if (prof && t == 0) {
+        uint64_t w1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
+        t_idle += w1 - w0t;
+      }
     }
   }
-  d.fmode[s] = nm;
-  d.fchg[nxt * d.nslot + s] = 0;
-  if (nm != M_IDLE) {
-    const int g = mode_group(nm);
-    const int pos = atomicAdd(&d.lcnt[nxt * NGROUP + g], 1);
-    d.slist[((size_t)nxt * NGROUP + g) * d.nslot + pos] = s;
-  }
+  if (prof && t == 0) atomicAdd(&d.pns[3], t_idle);
 }
 
-// Initial slot assignment: slot s holds frame s, all slots in M_INIT (listed for step 0).
+// Initial slot assignment: slot s holds frame s in M_INIT, every tile of every slot queued.
 __global__ void k_setup(Dev d, int nframes) {
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < d.nslot; s += gridDim.x * blockDim.x) {
-    d.sfr[s] = s;
-    d.fmode[s] = M_INIT;
-    d.slist[G_STREAM * d.nslot + s] = s;  // list buffer 0, group STREAM
+  const size_t ns = NS(d);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ns; i += (size_t)gridDim.x * blockDim.x) {
+    d.q[i] = (uint32_t)i;
+    if (i < (size_t)d.nslot) {
+      d.sfr[i] = (int)i;
+      d.fmode[i] = M_INIT;
+      d.fout[i] = d.T;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    d.lcnt[G_STREAM] = d.nslot;
+    *d.qtail = ns;
     d.gctr[0] = d.nslot;
   }
 }
 
-// max_launches exceeded: frames not finished get F = -1, status GC_ERR_NOCONV.
+// Aborted (watchdog / host timeout): frames not finished get F = -1, status GC_ERR_NOCONV.
 __global__ void k_abort(Dev d, IO io, int nframes) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < d.nslot; s += gridDim.x * blockDim.x) {
     if (d.fmode[s] == M_IDLE) continue;

@@ -1,15 +1,16 @@
 // gc_solver.cu -- host driver and C ABI (include/gc.h) of the B200 grid min-cut library.
 //
-// Per chunk of frames (all frames of a chunk share H, W, K):
-//   init (a1 / a1w) -> loop { global relabel: seed sweep + relax sweeps until no border
-//   change (a2); status: frames with no active node are done; R push launches (a3) }
-//   -> closure seed + relax sweeps (a4) -> finalize (mask, F, flow export a5).
-// The loop polls two device flags per iteration through pinned host memory.
+// Per call: carve the scratch pool into frame slots, queue every tile of the first frames,
+// and launch ONE persistent kernel (k_solve, gc_phases.cuh) that runs all phases of all
+// frames of the batch from a device-side work queue, refilling slots as frames finish.
+// The host only waits (with a timeout that asks the kernel to stop through a mapped host
+// word) and reads three counters back.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include <string>
 #include <vector>
@@ -22,24 +23,31 @@ using namespace gcb;
 struct gc_ctx {
   int dev = 0, K = 4, max_h = 0, max_w = 0, max_batch = 0, rounds = 8, period = 2;
   double alpha = 1.0;        // global relabel after alpha x (chunk pixels) relabel operations
-  int max_push_phase = 16384;  // push launches per phase, upper bound
   long long max_launches = 1000000;
   size_t pool_bytes = 0;
   char* pool = nullptr;
   int32_t* hpin = nullptr;  // pinned host words for polling
+  int32_t* habort = nullptr;      // mapped pinned word: host -> kernel stop request
+  int32_t* habort_dev = nullptr;  // its device alias
+  double timeout_s = 300.0;       // wall-clock bound of one k_solve launch
+  int vis_mult = 64;              // push tasks per push phase = vis_mult x frame tiles
+  int stall = 64;                 // push tasks without progress before a push phase drains
+  int grid = 0;                   // k_solve CTAs of the last launch
   std::string err;
   long long last_launches = 0;
   bool prof = false;
   long long prof_n[6] = {0, 0, 0, 0, 0, 0};
   long long prof_tiles[6] = {0, 0, 0, 0, 0, 0};
-  unsigned long long* dtiles = nullptr;  // device counters [6]
+  unsigned long long* dtiles = nullptr;  // device counters [12]: tasks [6], ns [6]
   double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+  double kernel_ms = 0;
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   size_t evnext = 0;
   // host-API staging (device)
   char* stage = nullptr;
   size_t stage_bytes = 0;
+  size_t words_bytes = 0;
 };
 
 namespace {
@@ -54,17 +62,24 @@ size_t frame_bytes(int K, size_t T) {
   b += T * TPX * 2;               // fl
   b += T * TPX;                   // m
   b += T * 128 * 4;               // hedge
-  b += 2 * T * K * 64 * 4;        // inbox
+  b += 2 * T * K * 64 * 4;        // sent, got
   b += T * K * 64;                // reach
-  b += T * 8 + 10 * T * 4;        // neg0 + tile flags
-  b += 4 * 2 * 4 + 96;            // frame words + slot lists
+  b += T * 8 + 8 * T * 4;         // neg0 + tile flags
+  b += 2 * T * 4 * 2;             // queue (capacity >= 2 x tiles in flight)
+  b += 4 * 16 + 8 * 4;            // frame words
   return b + 16 * 256;            // alignment slack
 }
 
 int tiles_of(int H, int W) { return ((H + TS - 1) / TS) * ((W + TS - 1) / TS); }
 
+size_t pow2_at_least(size_t x) {
+  size_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
 // Carve the pool for nslot frames of geometry H x W.
-Dev carve(gc_ctx* c, int nslot, int H, int W) {
+Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_bytes) {
   Dev d;
   memset(&d, 0, sizeof(d));
   d.H = H; d.W = W;
@@ -74,48 +89,56 @@ Dev carve(gc_ctx* c, int nslot, int H, int W) {
   const size_t T = d.T, ns = (size_t)nslot * T, K = c->K;
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
+  // per-frame words and the queue counters first: contiguous, so one memset clears them
+  char* fw = take((size_t)nslot * (4 * 16 + 8 * 4) + 64 * 4);  // 11 int + 3 u64 per slot
+  int32_t* w = (int32_t*)fw;
+  d.fmode = w; w += nslot;
+  d.sfr = w; w += nslot;
+  d.fout = w; w += nslot;
+  d.ferr = w; w += nslot;
+  d.fph = w; w += nslot;
+  d.fvis = w; w += nslot;
+  d.fprog = w; w += nslot;
+  d.fstat = w; w += 4 * nslot;
+  d.gctr = w; w += 4;
+  d.done = w; w += 4;
+  unsigned long long* u = (unsigned long long*)align_up((size_t)w, 8);
+  d.frel = u; u += nslot;
+  d.sumct = u; u += nslot;
+  d.sumneg = u; u += nslot;
+  d.qhead = u; u += 1;
+  d.qtail = u; u += 1;
+  d.ntask = u; u += 1;
+  c->words_bytes = (char*)u - fw;
+  d.treq = (int32_t*)take(ns * 4);
+  d.sent = (uint32_t*)take(ns * K * 64 * 4);
+  d.got = (uint32_t*)take(ns * K * 64 * 4);
+  *sentgot_bytes = (char*)(d.got + ns * K * 64) - (char*)d.treq;
+  const size_t qcap = pow2_at_least(2 * ns + 1024);
+  d.q = (uint32_t*)take(qcap * 4);
+  d.qmask = (uint32_t)(qcap - 1);
+  *q_bytes = qcap * 4;
   d.e = (int32_t*)take(ns * TPX * 4);
   d.h = (int32_t*)take(ns * TPX * 4);
   d.r = (int32_t*)take(ns * K * TPX * 4);
   d.fl = (uint16_t*)take(ns * TPX * 2);
   d.m = (uint8_t*)take(ns * TPX);
   d.hedge = (int32_t*)take(ns * 128 * 4);
-  d.inbox = (int32_t*)take(2 * ns * K * 64 * 4);
   d.reach = (uint8_t*)take(ns * K * 64);
   d.neg0 = (long long*)take(ns * 8);
   d.mat = (int32_t*)take(ns * 4);
   d.tact = (int32_t*)take(ns * 4);
-  d.dirty = (int32_t*)take(2 * ns * 4);
-  d.recv = (int32_t*)take(2 * ns * 4);
-  d.crecv = (int32_t*)take(2 * ns * 4);
+  d.flag = (int32_t*)take(ns * 4);
+  d.recv1 = (int32_t*)take(ns * 4);
+  d.tuni = (int32_t*)take(ns * 4);
+  d.tfix = (int32_t*)take(ns * 4);
   d.tph = (int32_t*)take(ns * 4);
-  // per-frame words: contiguous so one memset clears them (fmode 0 = M_SEED)
-  char* fw = take((size_t)nslot * (4 * 13 + 4 * 2 * NGROUP + 8 * 4) + 64 * 4 + 8 * 4 + 4 * 2 * NGROUP + 64);
-  int32_t* w = (int32_t*)fw;
-  d.fmode = w; w += nslot;
-  d.sfr = w; w += nslot;
-  d.fstall = w; w += nslot;
-  d.slist = w; w += 2 * NGROUP * nslot;
-  d.lcnt = w; w += 2 * NGROUP;
-  d.gctr = w; w += 4;
-  d.ferr = w; w += nslot;
-  d.fchg = w; w += 2 * nslot;
-  d.fph = w; w += nslot;
-  d.fpush = w; w += nslot;
-  d.fnew = w; w += nslot;
-  d.fstat = w; w += 4 * nslot;
-  unsigned long long* u = (unsigned long long*)align_up((size_t)w, 8);
-  d.fabs_ = u; u += nslot;
-  d.frel = u; u += nslot;
-  d.sumct = u; u += nslot;
-  d.sumneg = u; u += nslot;
-  d.ring = (int32_t*)u;
-  d.ctr = d.ring + 64;
+  d.hostabort = c->habort_dev;
   d.ptiles = c->prof ? c->dtiles : nullptr;
+  d.pns = c->prof ? c->dtiles + 6 : nullptr;
   return d;
 }
 
-size_t frame_words_bytes(const Dev& d) { return (char*)(d.ctr + 8) - (char*)d.fmode; }
 
 bool ck(gc_ctx* c, cudaError_t e, const char* what) {
   if (e == cudaSuccess) return true;
@@ -128,44 +151,33 @@ bool ck(gc_ctx* c, cudaError_t e, const char* what) {
 struct Launcher {
   gc_ctx* c;
   cudaStream_t st;
-  long long n = 0;
-  void pre(int cls) {
-    if (!c->prof) return;
-    if (c->evnext + 2 > c->evpool.size()) {
-      for (int i = 0; i < 256; ++i) {
-        cudaEvent_t ev;
-        cudaEventCreate(&ev);
-        c->evpool.push_back(ev);
-      }
-    }
-    cudaEvent_t a = c->evpool[c->evnext++], b = c->evpool[c->evnext++];
-    cudaEventRecord(a, st);
-    c->pending.push_back({cls, {a, b}});
-  }
-  void post() {
-    ++n;
-    if (!c->prof) return;
-    cudaEventRecord(c->pending.back().second.second, st);
-  }
+  long long n = 0;  // kernel launches issued
 };
 
+// Profiling counters of the last solve: tasks and summed CTA time per class, plus the
+// device time of each k_solve launch (CUDA events on the launching stream).
 void resolve_profile(gc_ctx* c) {
-  unsigned long long t[6];
+  unsigned long long t[12];
   if (cudaMemcpy(t, c->dtiles, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
-    for (int i = 0; i < 6; ++i) c->prof_tiles[i] += (long long)t[i];
+    for (int i = 0; i < 6; ++i) {
+      c->prof_tiles[i] += (long long)t[i];
+      // CTA-time of the class averaged over the persistent grid: the classes (3 = queue
+      // wait + transitions) then add up to the kernel's duration
+      c->prof_ms[i] += c->grid > 0 ? (double)t[6 + i] / 1e6 / c->grid : 0.0;
+    }
     cudaMemset(c->dtiles, 0, sizeof(t));
   }
   for (auto& p : c->pending) {
     float ms = 0;
     cudaEventElapsedTime(&ms, p.second.first, p.second.second);
-    c->prof_n[p.first] += 1;
-    c->prof_ms[p.first] += ms;
+    for (int i = 0; i < 6; ++i) c->prof_n[i] += 1;
+    c->kernel_ms += ms;
   }
   c->pending.clear();
   c->evnext = 0;
 }
 
-// Persistent grid size of a worklist kernel: resident CTAs per SM x SMs.
+// Persistent grid size: resident CTAs per SM x SMs.
 template <typename F>
 int persistent_grid(gc_ctx* c, F kernel, size_t dyn_smem = 0) {
   int sms = 0, per = 0;
@@ -186,71 +198,89 @@ int chunk_frames(gc_ctx* c, int H, int W) {
   return (int)n;
 }
 
+double now_s() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
+
 // Solve `nframes` frames of geometry H x W with the slots the pool holds: slots are refilled
 // on the device as frames finish (continuous batching).
 template <int K>
 gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaStream_t st, Launcher& L) {
   const int nslot = chunk_frames(c, H, W) < nframes ? chunk_frames(c, H, W) : nframes;
-  Dev d = carve(c, nslot, H, W);
-  static int g_stream = 0, g_seed = 0, g_relax = 0, g_push = 0;  // per-K persistent grid sizes
-  const size_t push_smem = push_smem_bytes<K>();
-  if (!g_stream) {
-    cudaFuncSetAttribute(k_push<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)push_smem);
-    g_stream = persistent_grid(c, k_stream<K>);
-    g_seed = persistent_grid(c, k_seed<K>);
-    g_relax = persistent_grid(c, k_relax<K>);
-    g_push = persistent_grid(c, k_push<K>, push_smem);
+  size_t sg_bytes = 0, q_bytes = 0;
+  Dev d = carve(c, nslot, H, W, &sg_bytes, &q_bytes);
+  static int g_solve[9] = {0};
+  const size_t smem = push_smem_bytes<K>();
+  if (!g_solve[K]) {
+    cudaFuncSetAttribute(k_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    g_solve[K] = persistent_grid(c, k_solve<K>, smem);
   }
   const size_t ns = (size_t)nslot * d.T;
-  auto cap = [&](int g) { return (int)((size_t)g < ns ? g : ns); };
-  const dim3 blk(NTH);
-  if (!ck(c, cudaMemsetAsync(d.fmode, 0, frame_words_bytes(d), st), "memset")) return GC_ERR_CUDA;
-  k_setup<<<(nslot + NTH - 1) / NTH, NTH, 0, st>>>(d, nframes);
+  int grid = g_solve[K];
+  if (const char* ev = getenv("GC_GRID")) grid = atoi(ev) > 0 && atoi(ev) < grid ? atoi(ev) : grid;
+  c->grid = grid;
+  if (!ck(c, cudaMemsetAsync(d.fmode, 0, c->words_bytes, st), "memset")) return GC_ERR_CUDA;
+  if (!ck(c, cudaMemsetAsync(d.treq, 0, sg_bytes, st), "memset")) return GC_ERR_CUDA;
+  if (!ck(c, cudaMemsetAsync(d.q, 0xff, q_bytes, st), "memset")) return GC_ERR_CUDA;
+  k_setup<<<(unsigned)((ns + NTH - 1) / NTH < 4096 ? (ns + NTH - 1) / NTH : 4096), NTH, 0, st>>>(d, nframes);
   ++L.n;
+  Ctl ctl;
+  ctl.relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
+  ctl.vis_budget = c->vis_mult * d.T;
+  ctl.stall = c->stall;
+  ctl.rounds = c->rounds;
+  ctl.nframes = nframes;
   // int4 loads in the init pass when every caller row is 16-byte aligned
-  const int vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
-                  ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
-  // Goldberg's global-relabel heuristic: a push phase ends at the latest after
-  // alpha x (frame pixels) relabel operations.
-  const long long relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
-  gc_status status = GC_OK;
-  int next_poll = 8;
-  for (int sw = 0;; ++sw) {
-    L.pre(0);
-    k_stream<K><<<cap(g_stream), blk, 0, st>>>(d, io, sw, vec);
-    L.post();
-    L.pre(1);
-    k_seed<K><<<cap(g_seed), blk, 0, st>>>(d, io, sw);
-    L.post();
-    L.pre(4);
-    k_relax<K><<<cap(g_relax), blk, 0, st>>>(d, io, sw);
-    L.post();
-    L.pre(2);
-    k_push<K><<<cap(g_push), blk, push_smem, st>>>(d, io, sw, c->rounds);
-    L.post();
-    L.pre(3);
-    k_control<<<nslot, NTH, 0, st>>>(d, io, sw, relabel_budget, c->max_push_phase, nframes);
-    L.post();
-    if (sw + 1 < next_poll) continue;
-    if (!ck(c, cudaGetLastError(), "step")) return GC_ERR_CUDA;
-    cudaMemcpyAsync(c->hpin, d.gctr, 16, cudaMemcpyDeviceToHost, st);
-    if (!ck(c, cudaStreamSynchronize(st), "step sync")) return GC_ERR_CUDA;
-    if (c->hpin[1] >= nframes) break;  // every frame finished
-    if (L.n > c->max_launches) {
-      k_abort<<<(nslot + NTH - 1) / NTH, NTH, 0, st>>>(d, io, nframes);
-      ++L.n;
-      status = GC_ERR_NOCONV;
-      break;
+  ctl.vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
+            ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
+  // watchdog: max_launches "sweeps" of the tiles in flight
+  const double mt = (double)c->max_launches * (double)ns;
+  ctl.max_tasks = mt > 9e18 ? (long long)9e18 : (long long)mt;
+  *c->habort = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->prof) {
+    if (c->evnext + 2 > c->evpool.size()) {
+      for (int i = 0; i < 16; ++i) {
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        c->evpool.push_back(ev);
+      }
     }
-    next_poll = sw + 1 + (sw < 64 ? 4 : (sw < 1024 ? 16 : 64));
+    e0 = c->evpool[c->evnext++];
+    e1 = c->evpool[c->evnext++];
+    cudaEventRecord(e0, st);
   }
-  cudaMemcpyAsync(c->hpin, d.gctr, 16, cudaMemcpyDeviceToHost, st);
-  if (!ck(c, cudaStreamSynchronize(st), "solve")) return GC_ERR_CUDA;
-  if (status == GC_ERR_NOCONV) return GC_ERR_NOCONV;
+  k_solve<K><<<grid, NTH, smem, st>>>(d, io, ctl);
+  ++L.n;
+  if (c->prof) {
+    cudaEventRecord(e1, st);
+    c->pending.push_back({0, {e0, e1}});
+  }
+  if (!ck(c, cudaGetLastError(), "k_solve launch")) return GC_ERR_CUDA;
+  cudaMemcpyAsync(c->hpin, d.gctr, 32, cudaMemcpyDeviceToHost, st);  // gctr[4], done[4]
+  // wait; past the timeout ask the kernel to stop (it polls the mapped word while idle)
+  const double t0 = now_s();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) { ck(c, q, "k_solve"); return GC_ERR_CUDA; }
+    if (!*c->habort && now_s() - t0 > c->timeout_s) *(volatile int32_t*)c->habort = 1;
+    struct timespec ts = {0, 20000};
+    nanosleep(&ts, nullptr);
+  }
+  const bool aborted = c->hpin[5] != 0 || c->hpin[1] < nframes;
+  if (aborted) {
+    k_abort<<<(nslot + NTH - 1) / NTH, NTH, 0, st>>>(d, io, nframes);
+    ++L.n;
+    if (!ck(c, cudaStreamSynchronize(st), "abort")) return GC_ERR_CUDA;
+    if (*c->habort) c->err = "solve timed out (host watchdog)";
+    return GC_ERR_NOCONV;
+  }
   if (c->hpin[2]) return GC_ERR_RANGE;
   return GC_OK;
 }
-
 
 gc_status check_batch(gc_ctx* c, const gc_batch* b) {
   if (!c) return GC_ERR_ARG;
@@ -297,7 +327,9 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   c->max_launches = g.max_launches > 0 ? g.max_launches : 1000000;
   c->max_batch = g.max_batch > 0 ? g.max_batch : 0;
   if (const char* ev = getenv("GC_ALPHA")) c->alpha = atof(ev);          // tuning knobs
-  if (const char* ev = getenv("GC_MAX_PUSH")) c->max_push_phase = atoi(ev);
+  if (const char* ev = getenv("GC_VIS")) c->vis_mult = atoi(ev);
+  if (const char* ev = getenv("GC_STALL")) c->stall = atoi(ev);
+  if (const char* ev = getenv("GC_TIMEOUT_S")) c->timeout_s = atof(ev);
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
   if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
   const size_t fb = frame_bytes(c->K, tiles_of(c->max_h, c->max_w));
@@ -319,8 +351,17 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   c->pool_bytes = nf * fb;
   if (cudaMalloc(&c->pool, c->pool_bytes) != cudaSuccess) { cudaGetLastError(); delete c; return GC_ERR_OOM; }
   if (cudaMallocHost(&c->hpin, 64) != cudaSuccess) { cudaFree(c->pool); delete c; return GC_ERR_OOM; }
-  if (cudaMalloc(&c->dtiles, 64) != cudaSuccess) { cudaFree(c->pool); cudaFreeHost(c->hpin); delete c; return GC_ERR_OOM; }
-  cudaMemset(c->dtiles, 0, 64);
+  if (cudaMalloc(&c->dtiles, 128) != cudaSuccess) { cudaFree(c->pool); cudaFreeHost(c->hpin); delete c; return GC_ERR_OOM; }
+  cudaMemset(c->dtiles, 0, 128);
+  if (cudaHostAlloc(&c->habort, 64, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&c->habort_dev, c->habort, 0) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(c->pool); cudaFreeHost(c->hpin); cudaFree(c->dtiles);
+    if (c->habort) cudaFreeHost(c->habort);
+    delete c;
+    return GC_ERR_OOM;
+  }
+  *c->habort = 0;
   *out = c;
   return GC_OK;
 }
@@ -331,6 +372,7 @@ void gc_destroy(gc_ctx* c) {
   if (c->pool) cudaFree(c->pool);
   if (c->stage) cudaFree(c->stage);
   if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->habort) cudaFreeHost(c->habort);
   if (c->dtiles) cudaFree(c->dtiles);
   delete c;
 }
@@ -352,6 +394,13 @@ void gc_get_profile(gc_ctx* c, long long* launches, double* ms, long long* tiles
   }
   if (reset)
     for (int i = 0; i < 6; ++i) { c->prof_n[i] = 0; c->prof_ms[i] = 0; c->prof_tiles[i] = 0; }
+}
+
+double gc_get_kernel_ms(gc_ctx* c, int reset) {
+  if (!c) return 0.0;
+  const double v = c->kernel_ms;
+  if (reset) c->kernel_ms = 0;
+  return v;
 }
 
 gc_status gc_solve_batch(gc_ctx* c, const gc_batch* b, void* stream) {
