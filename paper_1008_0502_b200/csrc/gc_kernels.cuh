@@ -21,7 +21,6 @@
 //                              arc direction and receiver edge slot: `sent` written only by
 //                              the sending tile, `got` only by the receiver (no atomics)
 //   reach [slot][tile][k][64]  sticky min-cut reach bits arriving across the border
-//   m  [slot][tile][1024] u8   mask bit (closure phase)
 // A tile is processed by at most one CTA at a time (gc_phases.cuh); all mutable state is
 // read through L2 (the library is compiled with -dlcm=cg), the caps through the read-only
 // path.
@@ -59,7 +58,6 @@ struct Dev {
                     //             arc direction and receiver edge slot (written by the sender)
   uint32_t* got;    // [NS][K][64] cumulative flow the tile has absorbed from `sent` (receiver)
   uint8_t* reach;
-  uint8_t* m;
   long long* neg0;  // [NS] sum max(0,-e) of the tile as initialised (for never-materialised tiles)
   int32_t* mat;     // [NS]   e, r of the tile are materialised
   int32_t* tact;    // [NS]   tile has an active node (e > 0, h < HINF)
@@ -71,6 +69,7 @@ struct Dev {
   int32_t* tfix;    // [NS]   a BFS relax of the tile cannot change it (every pixel with an
                     //        open arc has h = 1)
   int32_t* tph;     // [NS]   push-phase id of the tile's last push task
+  int32_t* tminh;   // [NS]   lowest height of an active pixel of the tile (HINF if none)
   // per frame slot (state machine): zero-initialised by one memset
   int32_t* fmode;   // [nslot] M_INIT, M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_EXPORT, M_IDLE
   int32_t* sfr;     // [nslot] batch frame index held by the slot
@@ -572,6 +571,16 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
   w.x = (unsigned short)fl4[0]; w.y = (unsigned short)fl4[1];
   w.z = (unsigned short)fl4[2]; w.w = (unsigned short)fl4[3];
   *reinterpret_cast<ushort4*>(d.fl + gt * TPX + iy * TS + ix0) = w;
+  if (y < H) {  // the caller's mask starts all 0; the closure phases write the ones
+    uint8_t* mk = io.mask + fr * plane + (size_t)y * W + x0;
+    if (x0 + 3 < W && ((uintptr_t)mk & 3) == 0) {
+      *reinterpret_cast<uint32_t*>(mk) = 0u;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (x0 + i < W) mk[i] = 0;
+    }
+  }
   for (int i = t; i < K * 64; i += NTH) d.reach[gt * K * 64 + i] = 0;
   bad = __syncthreads_or(bad);
   uni = __syncthreads_and(uni);
@@ -591,6 +600,7 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
     long long sa = 0, sb = 0;
     for (int i = 0; i < NTH / 32; ++i) { sa += red[0][i]; sb += red[1][i]; }
     if (sa) atomicAdd(&d.sumct[s], (unsigned long long)sa);
+    if (sb) atomicAdd(&d.sumneg[s], (unsigned long long)sb);  // corrected by the closure seed if e changes
     d.neg0[gt] = sb;
     d.mat[gt] = 0;
     d.flag[gt] = 0;

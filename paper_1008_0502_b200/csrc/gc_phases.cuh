@@ -43,6 +43,7 @@ struct Ctl {
   long long max_tasks;       // watchdog: tasks per launch before GC_ERR_NOCONV
   int vis_budget;            // push tasks per push phase
   int stall;                 // push tasks without progress before the phase drains
+  int wave;                  // push phase starts on active tiles with min height <= lowest + wave
   int rounds;                // push/relabel rounds per push task
   int nframes;
   int vec;                   // caller rows 16-byte aligned: int4 loads in the init pass
@@ -162,7 +163,7 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   }
   __syncthreads();
   bfs_fixpoint<K>(hs, fl, h);
-  int act = 0, fix = 1, uni = 1, bits = 0;
+  int act = 0, fix = 1, uni = 1, bits = 0, mnh = HINF;
   const int tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
 #pragma unroll
@@ -170,6 +171,7 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
     const int iy = iy0 + 8 * j;
     d.h[gt * TPX + iy * TS + ix] = h[j];
     act |= (fl[j] & FL_POS) && h[j] < HINF;
+    if (fl[j] & FL_POS) mnh = min(mnh, h[j]);
     fix &= (h[j] == 1) || !(fl[j] & 0xff);
     const bool in = ty * TS + iy < d.H && tx * TS + ix < d.W;
     uni &= !in || (fl[j] & FL_NEG);
@@ -177,8 +179,10 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   }
   store_hedge(d, gt, h, t);
   bits = __reduce_or_sync(0xffffffffu, bits);
-  if (t == 0) bc[1] = 0;
+  mnh = __reduce_min_sync(0xffffffffu, mnh);
+  if (t == 0) { bc[1] = 0; bc[5] = HINF; }
   act = __syncthreads_or(act);
+  if ((t & 31) == 0) atomicMin(&bc[5], mnh);
   fix = __syncthreads_and(fix);
   uni = __syncthreads_and(uni);
   if ((t & 31) == 0 && bits) atomicOr(&bc[1], bits);
@@ -191,6 +195,7 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   self = __syncthreads_or(self);
   if (t == 0) {
     d.tact[gt] = act;
+    d.tminh[gt] = bc[5];
     d.tfix[gt] = fix;
     d.tuni[gt] = uni;
     if (self && !fix) d.flag[gt] = 1;
@@ -218,17 +223,22 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
   load_halo(d, s, ty, tx, hs, t);
   __syncthreads();
   bfs_fixpoint<K>(hs, fl, h);
-  int any = 0, bits = 0, act = 0, fix = 1;
+  int any = 0, bits = 0, act = 0, fix = 1, mnh = HINF;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int ch = h[j] != h0[j];
     any |= ch;
     if (ch) bits |= border_bits(iy0 + 8 * j, ix);
     act |= (fl[j] & FL_POS) && h[j] < HINF;
+    if (fl[j] & FL_POS) mnh = min(mnh, h[j]);
     fix &= (h[j] == 1) || !(fl[j] & 0xff);
   }
   bits = __reduce_or_sync(0xffffffffu, bits);
+  mnh = __reduce_min_sync(0xffffffffu, mnh);
+  if (t == 0) bc[5] = HINF;
+  __syncthreads();
   if ((t & 31) == 0 && bits) atomicOr(&bc[1], bits);
+  if ((t & 31) == 0) atomicMin(&bc[5], mnh);
   any = __syncthreads_or(any);
   act = __syncthreads_or(act);
   fix = __syncthreads_and(fix);
@@ -236,7 +246,7 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
 #pragma unroll
     for (int j = 0; j < 4; ++j) d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
     store_hedge(d, gt, h, t);
-    if (t == 0) { d.tact[gt] = act; d.tfix[gt] = fix; }
+    if (t == 0) { d.tact[gt] = act; d.tfix[gt] = fix; d.tminh[gt] = bc[5]; }
   }
 }
 
@@ -332,12 +342,7 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
                                            long long* red, int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)(gt / d.T);
-  const int all[4] = {1, 1, 1, 1};
-  if (d.ferr[s]) {  // range error: mask all 0, F = -1
-    const int z[4] = {0, 0, 0, 0};
-    write_mask(d, io, gt, z, all);
-    return;
-  }
+  if (d.ferr[s]) return;  // range error: the mask stays all 0 (zero-filled by init), F = -1
   int mm[4];
   const int mat = d.mat[gt];
   long long neg = 0;
@@ -355,21 +360,16 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   }
   __syncthreads();
   closure_fixpoint<K>(ms, os, mm);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = (uint8_t)mm[j];
-  write_mask(d, io, gt, mm, all);
+  write_mask(d, io, gt, mm, mm);  // the mask was zero-filled by init: write the ones
   const int sides = block_or_bits(closure_send<K>(d, gt, mm, os), bc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
   if ((t & 31) == 0) red[t >> 5] = neg;
   __syncthreads();
-  if (t == 0) {
+  if (t == 0 && mat) {  // init added the tile's initial deficit; replace it by the final one
     long long tot = 0;
-    if (mat) {
-      for (int i = 0; i < NTH / 32; ++i) tot += red[i];
-    } else {
-      tot = d.neg0[gt];
-    }
+    for (int i = 0; i < NTH / 32; ++i) tot += red[i];
+    tot -= d.neg0[gt];
     if (tot) atomicAdd(&d.sumneg[s], (unsigned long long)tot);
   }
   flag_sides(d, gt, sides, K);
@@ -381,10 +381,13 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
                                             int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   int mm[4], m0[4];
+  const uint8_t* mrow = io.mask + (size_t)d.sfr[gt / d.T] * d.H * d.W;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j, lp = iy * TS + ix;
-    m0[j] = d.m[gt * TPX + lp];
+    const int y = (int)((gt - (size_t)(gt / d.T) * d.T) / d.TX) * TS + iy;
+    const int x = (int)((gt - (size_t)(gt / d.T) * d.T) % d.TX) * TS + ix;
+    m0[j] = (y < d.H && x < d.W) ? mrow[(size_t)y * d.W + x] : 0;
     os[lp] = (uint8_t)(d.fl[gt * TPX + lp] & 0xff);
     int got = m0[j];
     if (!got && on_border(iy, ix)) {
@@ -409,9 +412,6 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
   any = __syncthreads_or(any);
   if (t == 0) bc[1] = 0;
   if (any) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (nw[j]) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = 1;
     write_mask(d, io, gt, mm, nw);
     block_or_bits(closure_send<K>(d, gt, nw, os), bc);  // sides to request, in bc[1]
   }
@@ -638,7 +638,9 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
 }
 
 // ---------------------------------------------------------------- transitions
-enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3 };
+// first task set of a phase: NONE = the slot idles; EMPTY = no task (the next transition
+// follows at once)
+enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_CSEED = 5, SET_EMPTY = 6 };
 
 __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
   const int f = d.sfr[s];
@@ -666,17 +668,28 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
   for (;;) {
     fence_gpu();
     const int md = __ldcg(d.fmode + s);
-    int nact = 0;
+    int nact = 0, hlo = HINF;
     if (md == M_BFS) {
-      for (int i = t; i < d.T; i += NTH) nact |= __ldcg(d.tact + (size_t)s * d.T + i);
+      for (int i = t; i < d.T; i += NTH) {
+        const size_t gt = (size_t)s * d.T + i;
+        if (__ldcg(d.tact + gt)) { nact = 1; hlo = min(hlo, __ldcg(d.tminh + gt)); }
+      }
+      hlo = __reduce_min_sync(0xffffffffu, hlo);
+      if (t == 0) bc[6] = HINF;
+      __syncthreads();
+      if ((t & 31) == 0) atomicMin(&bc[6], hlo);
     }
     nact = __syncthreads_or(nact);
+    // push wave: the phase starts on the active tiles nearest the sink; farther ones wait
+    // for the next global relabel (most are cut off by then) unless flow reaches them
+    const int hcap = md == M_BFS ? (bc[6] > HINF - c.wave ? HINF : bc[6] + c.wave) : HINF;
     if (t == 0) {
       int nm = md, kind = SET_ALL;
       int* st = d.fstat + s * 4;
       bool finished = false;
       if (md == M_INIT) {
         nm = d.ferr[s] ? M_CSEED : M_SEED;
+        kind = d.ferr[s] ? SET_EMPTY : SET_SEED;
       } else if (md == M_SEED) {
         nm = M_BFS;
         kind = SET_FLAG;
@@ -691,9 +704,11 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.fph[s] += 1;
         } else {
           nm = M_CSEED;  // termination certificate: the preflow is maximum
+          kind = SET_CSEED;
         }
       } else if (md == M_PUSH) {
         nm = M_SEED;
+        kind = SET_SEED;
       } else if (md == M_CSEED) {
         nm = M_CLOS;
         kind = SET_FLAG;
@@ -726,19 +741,21 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     if (kind == SET_NONE) break;
     // enqueue the phase's first task set, NTH tiles at a time
     const size_t base_gt = (size_t)s * d.T;
-    for (int b0 = 0; b0 < d.T; b0 += NTH) {
+    for (int b0 = 0; kind != SET_EMPTY && b0 < d.T; b0 += NTH) {
       const int i = b0 + t;
       int want = 0;
       if (i < d.T) {
         const size_t gt = base_gt + i;
         if (kind == SET_ALL) want = 1;
+        else if (kind == SET_SEED) want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));  // untouched uniform: h = 1
+        else if (kind == SET_CSEED) want = !(__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt));   // untouched uniform: mask 0
         else if (kind == SET_FLAG) {
           want = __ldcg(d.flag + gt);
           if (want) d.flag[gt] = 0;
           if (md == M_SEED && __ldcg(d.tfix + gt)) want = 0;  // a relax cannot change it
         }
-        else want = __ldcg(d.tact + gt);
-        if (want && kind != SET_ALL) d.treq[gt] = 1;
+        else want = __ldcg(d.tact + gt) && __ldcg(d.tminh + gt) <= hcap;
+        if (want && (kind == SET_FLAG || kind == SET_TACT)) d.treq[gt] = 1;
       }
       if (t == 0) bc[5] = 0;
       __syncthreads();

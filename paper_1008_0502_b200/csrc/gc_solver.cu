@@ -22,7 +22,7 @@ using namespace gcb;
 
 struct gc_ctx {
   int dev = 0, K = 4, max_h = 0, max_w = 0, max_batch = 0, rounds = 8, period = 2;
-  double alpha = 1.0;        // global relabel after alpha x (chunk pixels) relabel operations
+  double alpha = 0.2;        // global relabel after alpha x (frame pixels) relabel operations
   long long max_launches = 1000000;
   size_t pool_bytes = 0;
   char* pool = nullptr;
@@ -32,6 +32,7 @@ struct gc_ctx {
   double timeout_s = 300.0;       // wall-clock bound of one k_solve launch
   int vis_mult = 64;              // push tasks per push phase = vis_mult x frame tiles
   int stall = 64;                 // push tasks without progress before a push phase drains
+  int wave = 32;                  // push wave width (heights above the lowest active one)
   int grid = 0;                   // k_solve CTAs of the last launch
   std::string err;
   long long last_launches = 0;
@@ -60,11 +61,10 @@ size_t frame_bytes(int K, size_t T) {
   b += 2 * T * TPX * 4;           // e, h
   b += (size_t)K * T * TPX * 4;   // r
   b += T * TPX * 2;               // fl
-  b += T * TPX;                   // m
   b += T * 128 * 4;               // hedge
   b += 2 * T * K * 64 * 4;        // sent, got
   b += T * K * 64;                // reach
-  b += T * 8 + 8 * T * 4;         // neg0 + tile flags
+  b += T * 8 + 9 * T * 4;         // neg0 + tile flags
   b += 2 * T * 4 * 2;             // queue (capacity >= 2 x tiles in flight)
   b += 4 * 16 + 8 * 4;            // frame words
   return b + 16 * 256;            // alignment slack
@@ -122,7 +122,6 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.h = (int32_t*)take(ns * TPX * 4);
   d.r = (int32_t*)take(ns * K * TPX * 4);
   d.fl = (uint16_t*)take(ns * TPX * 2);
-  d.m = (uint8_t*)take(ns * TPX);
   d.hedge = (int32_t*)take(ns * 128 * 4);
   d.reach = (uint8_t*)take(ns * K * 64);
   d.neg0 = (long long*)take(ns * 8);
@@ -133,6 +132,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.tuni = (int32_t*)take(ns * 4);
   d.tfix = (int32_t*)take(ns * 4);
   d.tph = (int32_t*)take(ns * 4);
+  d.tminh = (int32_t*)take(ns * 4);
   d.hostabort = c->habort_dev;
   d.ptiles = c->prof ? c->dtiles : nullptr;
   d.pns = c->prof ? c->dtiles + 6 : nullptr;
@@ -230,6 +230,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   ctl.relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
   ctl.vis_budget = c->vis_mult * d.T;
   ctl.stall = c->stall;
+  ctl.wave = c->wave;
   ctl.rounds = c->rounds;
   ctl.nframes = nframes;
   // int4 loads in the init pass when every caller row is 16-byte aligned
@@ -329,6 +330,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (const char* ev = getenv("GC_ALPHA")) c->alpha = atof(ev);          // tuning knobs
   if (const char* ev = getenv("GC_VIS")) c->vis_mult = atoi(ev);
   if (const char* ev = getenv("GC_STALL")) c->stall = atoi(ev);
+  if (const char* ev = getenv("GC_WAVE")) c->wave = atoi(ev);
   if (const char* ev = getenv("GC_TIMEOUT_S")) c->timeout_s = atof(ev);
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
   if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
