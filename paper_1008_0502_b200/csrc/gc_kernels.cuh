@@ -20,7 +20,8 @@
 //   sent/got [slot][tile][k][64] cumulative flow pushed INTO the tile across its border, by
 //                              arc direction and receiver edge slot: `sent` written only by
 //                              the sending tile, `got` only by the receiver (no atomics)
-//   reach [slot][tile][k][64]  sticky min-cut reach bits arriving across the border
+//   reach [slot][tile][k][64]  min-cut reach marks arriving across the border (closure epoch)
+//   m  [slot][tile][1024] u8   closure membership, as the epoch of the closure attempt
 // A tile is processed by at most one CTA at a time (gc_phases.cuh); all mutable state is
 // read through L2 (the library is compiled with -dlcm=cg), the caps through the read-only
 // path.
@@ -58,7 +59,11 @@ struct Dev {
                     //             arc direction and receiver edge slot (written by the sender)
   uint32_t* got;    // [NS][K][64] cumulative flow the tile has absorbed from `sent` (receiver)
   uint8_t* reach;
-  long long* neg0;  // [NS] sum max(0,-e) of the tile as initialised (for never-materialised tiles)
+  long long* neg0;  // [NS] the tile's share of sumneg: sum max(0,-e) as initialised, updated
+                    //      by each closure seed of a materialised tile
+  uint8_t* m;       // [NS][1024] closure attempt epoch of the pixels in the closure
+  int32_t* tcs;     // [NS]   epoch of the closure attempt that last wrote the tile's m
+  int32_t* tmk;     // [NS]   epoch of the closure attempt in which the tile got closure pixels
   int32_t* mat;     // [NS]   e, r of the tile are materialised
   int32_t* tact;    // [NS]   tile has an active node (e > 0, h < HINF)
   int32_t* flag;    // [NS]   tile is in the first task set of the next phase (seed -> BFS, cseed -> closure)
@@ -79,6 +84,8 @@ struct Dev {
   int32_t* fph;     // [nslot] global relabels so far (push-phase id)
   int32_t* fvis;    // [nslot] push tasks in the current push phase
   int32_t* fprog;   // [nslot] value of fvis after the last push task that made progress
+  int32_t* cep;     // [nslot] closure attempts so far (epoch = cep % 255 + 1)
+  int32_t* cfail;   // [nslot] the running closure attempt reached a node with e < 0
   int32_t* fstat;   // [nslot][4] push tasks, global relabels, BFS relax tasks, -
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]
@@ -95,7 +102,7 @@ struct Dev {
   unsigned long long* pns;     // [6] ns per class summed over CTAs (profiling only)
 };
 
-enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_EXPORT = 6, M_IDLE = 7 };
+enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_MASK = 6, M_EXPORT = 7, M_IDLE = 8 };
 
 struct IO {
   const int32_t* cs;
@@ -609,6 +616,8 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
     d.tuni[gt] = uni;
     d.tfix[gt] = uni;
     d.tph[gt] = -1;
+    d.tcs[gt] = 0;
+    d.tmk[gt] = 0;
     if (bad) d.ferr[s] = 1;
   }
   __syncthreads();

@@ -107,6 +107,42 @@ __device__ __forceinline__ int border_bits(int iy, int ix) {
   return b;
 }
 
+// Flow still in flight into the tile: materialise e, r pixel at a time (from the stored
+// state or the caps), absorb the inbound border flow, store; returns the new fl words.
+template <int K>
+__device__ __forceinline__ void absorb_pixelwise(const Dev& d, const IO& io, size_t gt, int (&fl)[4]) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const int iy = iy0 + 8 * j, lp = iy * TS + ix;
+    int e, r[K];
+    px_er<K>(d, io, gt, lp, ty * TS + iy, tx * TS + ix, e, r);
+    if (on_border(iy, ix)) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int wy = iy - DYk(k), wx = ix - DXk(k);
+        if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
+        const int dl = take_inflow<K>(d, gt, k, iy, ix);
+        if (dl) { e += dl; r[k ^ 1] += dl; }
+      }
+    }
+    d.e[gt * TPX + lp] = e;
+#pragma unroll
+    for (int k = 0; k < K; ++k) Rp(d, K, gt, k)[lp] = r[k];
+    fl[j] = make_fl<K>(e, r);
+    d.fl[gt * TPX + lp] = (uint16_t)fl[j];
+  }
+  __syncthreads();
+  if (t == 0) {
+    d.mat[gt] = 1;
+    d.recv1[gt] = 0;
+    d.tuni[gt] = 0;  // the tile changed: no longer a known uniform sink tile (a seed recomputes)
+    d.tfix[gt] = 0;
+  }
+}
+
 // ---------------------------------------------------------------- a2: seed (one tile)
 // Absorbs flow still in flight from the push phase (materialising e, r pixel at a time),
 // seeds h = 1 where the node has residual capacity to t, relaxes to the tile-local
@@ -125,31 +161,8 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   const int rcv = bc[0];
   if (bc[2] && !rcv) return;  // untouched uniform sink tile: h = 1, hedge published
   int fl[4];
-  if (rcv) {
-    const int tile = (int)(gt - (size_t)s * d.T);
-    const int ty = tile / d.TX, tx = tile - ty * d.TX;
-#pragma unroll 1
-    for (int j = 0; j < 4; ++j) {  // pixel at a time: materialise, absorb, store
-      const int iy = iy0 + 8 * j, lp = iy * TS + ix;
-      int e, r[K];
-      px_er<K>(d, io, gt, lp, ty * TS + iy, tx * TS + ix, e, r);
-      if (on_border(iy, ix)) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int wy = iy - DYk(k), wx = ix - DXk(k);
-          if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-          const int dl = take_inflow<K>(d, gt, k, iy, ix);
-          if (dl) { e += dl; r[k ^ 1] += dl; }
-        }
-      }
-      d.e[gt * TPX + lp] = e;
-#pragma unroll
-      for (int k = 0; k < K; ++k) Rp(d, K, gt, k)[lp] = r[k];
-      fl[j] = make_fl<K>(e, r);
-      d.fl[gt * TPX + lp] = (uint16_t)fl[j];
-    }
-    if (t == 0) { d.mat[gt] = 1; d.recv1[gt] = 0; }
-  } else {
+  if (rcv) absorb_pixelwise<K>(d, io, gt, fl);
+  else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
   }
@@ -251,8 +264,14 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
 }
 
 // ---------------------------------------------------------------- a4: closure helpers
-// mask = closure of {v : e(v) > 0} under arcs with positive residual: the
-// source side of the inclusion-minimal minimum cut.
+// The closure of {v : e(v) > 0} under arcs with positive residual.  If it holds no node
+// with e < 0 (residual capacity to t), no excess can reach t: the preflow is maximum and
+// the closure is the source side of the inclusion-minimal minimum cut --
+// the certificate that ends a solve.  Otherwise the attempt fails (cfail) and the frame
+// returns to a global relabel.  Closure membership and border reach marks carry the
+// attempt's epoch, so a failed attempt leaves nothing behind.
+__device__ __forceinline__ int closure_epoch(const Dev& d, int s) { return __ldcg(d.cep + s) % 255 + 1; }
+
 template <int K>
 __device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uint8_t* os, int (&mm)[4]) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
@@ -281,10 +300,11 @@ __device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uin
   }
 }
 
-// Sets the reach bits of the border arcs leaving newly reached pixels; returns the sides
-// (side_bit) of the neighbour tiles that received bits.
+// Marks the border arcs leaving newly reached pixels with the epoch; returns the sides
+// (side_bit) of the neighbour tiles that were marked.
 template <int K>
-__device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os) {
+__device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os,
+                                            int ep) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
@@ -302,25 +322,11 @@ __device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (
       const int rty = ty + dy, rtx = tx + dx;
       if (rty < 0 || rty >= d.TY || rtx < 0 || rtx >= d.TX) continue;
       const size_t rgt = (size_t)s * d.T + rty * d.TX + rtx;
-      d.reach[(rgt * K + k) * 64 + recv_slot(k, y2 & 31, x2 & 31)] = 1;
+      d.reach[(rgt * K + k) * 64 + recv_slot(k, y2 & 31, x2 & 31)] = (uint8_t)ep;
       sides |= 1 << side_bit(dy, dx);
     }
   }
   return sides;
-}
-
-__device__ __forceinline__ void write_mask(const Dev& d, const IO& io, size_t gt, const int (&mm)[4],
-                                           const int (&wr)[4]) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const size_t plane = (size_t)d.H * d.W;
-  uint8_t* mask = io.mask + (size_t)d.sfr[s] * plane;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
-    if (wr[j] && y < d.H && x < d.W) mask[(size_t)y * d.W + x] = (uint8_t)mm[j];
-  }
 }
 
 // OR of per-thread side bits into bc[1] (block-wide); returns it.
@@ -334,25 +340,36 @@ __device__ __forceinline__ int block_or_bits(int bits, int* bc) {
 }
 
 // ---------------------------------------------------------------- a4: closure seed (one tile)
-// Every tile: m = (e > 0) closed inside the tile; writes m and the caller's mask; sets reach
-// bits across the border (flagging the receivers for the closure phase); adds the tile's
-// sum max(0,-e) to the flow value's sum.
+// Absorbs flow still in flight, closes {e > 0} inside the tile, writes the tile's m,
+// marks reach across the border (flagging the receivers for the closure phase), checks the
+// certificate, and brings the tile's share of sum max(0,-e) up to date.
 template <int K>
 __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
                                            long long* red, int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)(gt / d.T);
-  if (d.ferr[s]) return;  // range error: the mask stays all 0 (zero-filled by init), F = -1
+  if (t == 0) {
+    bc[0] = __ldcg(d.recv1 + gt);
+    bc[2] = __ldcg(d.ferr + s) || __ldcg(d.cfail + s) > 0;
+  }
+  __syncthreads();
+  if (bc[2]) return;  // range error (mask stays 0, F = -1) or the attempt already failed
+  int fl[4];
+  if (bc[0]) absorb_pixelwise<K>(d, io, gt, fl);
+  else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
+  }
+  const int ep = closure_epoch(d, s);
+  const int mat = bc[0] ? 1 : d.mat[gt];
   int mm[4];
-  const int mat = d.mat[gt];
   long long neg = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int lp = (iy0 + 8 * j) * TS + ix;
-    const int f = d.fl[gt * TPX + lp];
-    mm[j] = (f & FL_POS) ? 1 : 0;
+    mm[j] = (fl[j] & FL_POS) ? 1 : 0;
     ms[lp] = (uint8_t)mm[j];
-    os[lp] = (uint8_t)(f & 0xff);
+    os[lp] = (uint8_t)(fl[j] & 0xff);
     if (mat) {
       const int ev = d.e[gt * TPX + lp];
       neg += ev < 0 ? -(long long)ev : 0;
@@ -360,42 +377,64 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   }
   __syncthreads();
   closure_fixpoint<K>(ms, os, mm);
-  write_mask(d, io, gt, mm, mm);  // the mask was zero-filled by init: write the ones
-  const int sides = block_or_bits(closure_send<K>(d, gt, mm, os), bc);
+  int fail = 0, any = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = mm[j] ? (uint8_t)ep : (uint8_t)0;
+    fail |= mm[j] && (fl[j] & FL_NEG);
+    any |= mm[j];
+  }
+  fail = __syncthreads_or(fail);
+  any = __syncthreads_or(any);
+  const int sides = block_or_bits(closure_send<K>(d, gt, mm, os, ep), bc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
   if ((t & 31) == 0) red[t >> 5] = neg;
   __syncthreads();
-  if (t == 0 && mat) {  // init added the tile's initial deficit; replace it by the final one
-    long long tot = 0;
-    for (int i = 0; i < NTH / 32; ++i) tot += red[i];
-    tot -= d.neg0[gt];
-    if (tot) atomicAdd(&d.sumneg[s], (unsigned long long)tot);
+  if (t == 0) {
+    if (mat) {  // replace the tile's share of sum max(0,-e) by its current value
+      long long tot = 0;
+      for (int i = 0; i < NTH / 32; ++i) tot += red[i];
+      const long long dl = tot - d.neg0[gt];
+      if (dl) atomicAdd(&d.sumneg[s], (unsigned long long)dl);
+      d.neg0[gt] = tot;
+    }
+    d.tcs[gt] = ep;
+    if (any) d.tmk[gt] = ep;
+    if (fail) atomicAdd(&d.cfail[s], 2);  // cfail: 0 / -1 (after the BFS certificate) + 2 per failure
   }
   flag_sides(d, gt, sides, K);
 }
 
 // ---------------------------------------------------------------- a4: closure relax (one tile)
+// Returns the sides to request in bc[1].
 template <int K>
 __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
                                             int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  int mm[4], m0[4];
-  const uint8_t* mrow = io.mask + (size_t)d.sfr[gt / d.T] * d.H * d.W;
+  const int s = (int)(gt / d.T);
+  if (t == 0) {
+    bc[1] = 0;
+    bc[2] = __ldcg(d.cfail + s) > 0;
+  }
+  __syncthreads();
+  if (bc[2]) return;  // the attempt already failed
+  const int ep = closure_epoch(d, s);
+  const bool valid = __ldcg(d.tcs + gt) == ep;  // else m is stale: the tile was not closure-seeded
+  int mm[4], m0[4], fl[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j, lp = iy * TS + ix;
-    const int y = (int)((gt - (size_t)(gt / d.T) * d.T) / d.TX) * TS + iy;
-    const int x = (int)((gt - (size_t)(gt / d.T) * d.T) % d.TX) * TS + ix;
-    m0[j] = (y < d.H && x < d.W) ? mrow[(size_t)y * d.W + x] : 0;
-    os[lp] = (uint8_t)(d.fl[gt * TPX + lp] & 0xff);
+    fl[j] = d.fl[gt * TPX + lp];
+    m0[j] = valid && d.m[gt * TPX + lp] == ep;
+    os[lp] = (uint8_t)(fl[j] & 0xff);
     int got = m0[j];
     if (!got && on_border(iy, ix)) {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int wy = iy - DYk(k), wx = ix - DXk(k);
         if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-        got |= __ldcg(d.reach + (gt * K + k) * 64 + recv_slot(k, iy, ix));
+        got |= __ldcg(d.reach + (gt * K + k) * 64 + recv_slot(k, iy, ix)) == ep;
       }
     }
     mm[j] = got;
@@ -403,17 +442,41 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
   }
   __syncthreads();
   closure_fixpoint<K>(ms, os, mm);
-  int nw[4], any = 0;
+  int nw[4], any = 0, fail = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     nw[j] = mm[j] & !m0[j];
     any |= nw[j];
+    fail |= nw[j] && (fl[j] & FL_NEG);
   }
   any = __syncthreads_or(any);
-  if (t == 0) bc[1] = 0;
-  if (any) {
-    write_mask(d, io, gt, mm, nw);
-    block_or_bits(closure_send<K>(d, gt, nw, os), bc);  // sides to request, in bc[1]
+  fail = __syncthreads_or(fail);
+  if (any || !valid) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (nw[j] || !valid) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = mm[j] ? (uint8_t)ep : (uint8_t)0;
+  }
+  if (t == 0) {
+    if (!valid) d.tcs[gt] = ep;
+    if (any) d.tmk[gt] = ep;
+    if (fail) atomicAdd(&d.cfail[s], 2);
+  }
+  if (any && !fail) block_or_bits(closure_send<K>(d, gt, nw, os, ep), bc);  // sides to request, in bc[1]
+}
+
+// ---------------------------------------------------------------- a4: mask (one tile)
+// After a certified closure: the caller's mask (zero-filled by init) gets the ones.
+template <int K>
+__device__ __forceinline__ void task_mask(const Dev& d, const IO& io, size_t gt) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  const int ep = closure_epoch(d, s);
+  uint8_t* mask = io.mask + (size_t)d.sfr[s] * d.H * d.W;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
+    if (y < d.H && x < d.W && d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] == ep) mask[(size_t)y * d.W + x] = 1;
   }
 }
 
@@ -640,7 +703,8 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
 // ---------------------------------------------------------------- transitions
 // first task set of a phase: NONE = the slot idles; EMPTY = no task (the next transition
 // follows at once)
-enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_CSEED = 5, SET_EMPTY = 6 };
+enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_CSEED = 5, SET_EMPTY = 6,
+       SET_MASK = 7 };
 
 __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
   const int f = d.sfr[s];
@@ -705,14 +769,35 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         } else {
           nm = M_CSEED;  // termination certificate: the preflow is maximum
           kind = SET_CSEED;
+          d.cfail[s] = -1;  // this closure cannot fail (marker)
         }
       } else if (md == M_PUSH) {
-        nm = M_SEED;
-        kind = SET_SEED;
-      } else if (md == M_CSEED) {
-        nm = M_CLOS;
-        kind = SET_FLAG;
-      } else if (md == M_CLOS) {
+        // try to certify at once: the closure of the excess nodes; if it reaches a node with
+        // e < 0 the frame returns to a global relabel (epochs are unique within a frame for
+        // 250 attempts; beyond that only the BFS certificate leads to the closure)
+        if (d.cep[s] < 250) { nm = M_CSEED; kind = SET_CSEED; }
+        else { nm = M_SEED; kind = SET_SEED; }
+      } else if (md == M_CSEED || md == M_CLOS) {
+        const int cf = d.cfail[s];
+        if (cf > 0 && (cf & 1)) {  // a closure after the BFS certificate failed: internal error
+          atomicExch(&d.gctr[3], 1);
+          *(volatile int*)&d.done[1] = 1;
+          nm = M_IDLE;
+          kind = SET_NONE;
+        } else if (cf > 0) {  // not maximum yet: next attempt after a global relabel
+          d.cfail[s] = 0;
+          d.cep[s] += 1;
+          nm = M_SEED;
+          kind = SET_SEED;
+        } else if (md == M_CSEED) {
+          nm = M_CLOS;
+          kind = SET_FLAG;
+        } else {
+          nm = M_MASK;
+          kind = SET_MASK;
+          d.cfail[s] = 0;
+        }
+      } else if (md == M_MASK) {
         if (io.fstate && !d.ferr[s]) nm = M_EXPORT;
         else finished = true;
       } else if (md == M_EXPORT) {
@@ -727,6 +812,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.fph[s] = 0; d.fvis[s] = 0; d.fprog[s] = 0;
           st[0] = st[1] = st[2] = st[3] = 0;
           d.frel[s] = 0; d.sumct[s] = 0; d.sumneg[s] = 0;
+          d.cep[s] = 0; d.cfail[s] = 0;
           nm = M_INIT;
         } else {
           nm = M_IDLE;
@@ -747,8 +833,15 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (i < d.T) {
         const size_t gt = base_gt + i;
         if (kind == SET_ALL) want = 1;
-        else if (kind == SET_SEED) want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));  // untouched uniform: h = 1
-        else if (kind == SET_CSEED) want = !(__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt));   // untouched uniform: mask 0
+        else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1
+          want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));
+          d.flag[gt] = 0;
+        } else if (kind == SET_CSEED) {  // untouched uniform sink tiles are never in the closure
+          want = !(__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt) && !__ldcg(d.recv1 + gt));
+          d.flag[gt] = 0;
+        } else if (kind == SET_MASK) {
+          want = __ldcg(d.tmk + gt) == __ldcg(d.cep + s) % 255 + 1;
+        }
         else if (kind == SET_FLAG) {
           want = __ldcg(d.flag + gt);
           if (want) d.flag[gt] = 0;
@@ -856,6 +949,7 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
         task_crelax<K>(d, io, gt, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, bc);
         cls = 4;
         break;
+      case M_MASK: task_mask<K>(d, io, gt); cls = 4; break;
       default: task_export<K>(d, io, gt); cls = 5; break;
     }
     // release this task's writes, then request the neighbour tiles it changed

@@ -64,7 +64,8 @@ size_t frame_bytes(int K, size_t T) {
   b += T * 128 * 4;               // hedge
   b += 2 * T * K * 64 * 4;        // sent, got
   b += T * K * 64;                // reach
-  b += T * 8 + 9 * T * 4;         // neg0 + tile flags
+  b += T * 8 + 11 * T * 4;        // neg0 + tile flags
+  b += T * TPX;                   // m
   b += 2 * T * 4 * 2;             // queue (capacity >= 2 x tiles in flight)
   b += 4 * 16 + 8 * 4;            // frame words
   return b + 16 * 256;            // alignment slack
@@ -99,6 +100,8 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.fph = w; w += nslot;
   d.fvis = w; w += nslot;
   d.fprog = w; w += nslot;
+  d.cep = w; w += nslot;
+  d.cfail = w; w += nslot;
   d.fstat = w; w += 4 * nslot;
   d.gctr = w; w += 4;
   d.done = w; w += 4;
@@ -133,6 +136,9 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.tfix = (int32_t*)take(ns * 4);
   d.tph = (int32_t*)take(ns * 4);
   d.tminh = (int32_t*)take(ns * 4);
+  d.tcs = (int32_t*)take(ns * 4);
+  d.tmk = (int32_t*)take(ns * 4);
+  d.m = (uint8_t*)take(ns * TPX);
   d.hostabort = c->habort_dev;
   d.ptiles = c->prof ? c->dtiles : nullptr;
   d.pns = c->prof ? c->dtiles + 6 : nullptr;
@@ -272,10 +278,26 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
     nanosleep(&ts, nullptr);
   }
   const bool aborted = c->hpin[5] != 0 || c->hpin[1] < nframes;
+  if (aborted && getenv("GC_DEBUG")) {  // development aid: where did each slot stop?
+    std::vector<int32_t> w(c->words_bytes / 4);
+    cudaMemcpy(w.data(), d.fmode, w.size() * 4, cudaMemcpyDeviceToHost);
+    const int32_t* base = w.data();
+    for (int i = 0; i < nslot; ++i)
+      fprintf(stderr, "slot %d frame %d mode %d fout %d ferr %d fph %d fvis %d fprog %d cep %d cfail %d\n", i,
+              base[(d.sfr - d.fmode) + i], base[i], base[(d.fout - d.fmode) + i], base[(d.ferr - d.fmode) + i],
+              base[(d.fph - d.fmode) + i], base[(d.fvis - d.fmode) + i], base[(d.fprog - d.fmode) + i],
+              base[(d.cep - d.fmode) + i], base[(d.cfail - d.fmode) + i]);
+    fprintf(stderr, "gctr %d %d %d done %d %d\n", base[d.gctr - d.fmode], base[d.gctr - d.fmode + 1],
+            base[d.gctr - d.fmode + 2], base[d.done - d.fmode], base[d.done - d.fmode + 1]);
+  }
   if (aborted) {
     k_abort<<<(nslot + NTH - 1) / NTH, NTH, 0, st>>>(d, io, nframes);
     ++L.n;
     if (!ck(c, cudaStreamSynchronize(st), "abort")) return GC_ERR_CUDA;
+    if (c->hpin[3]) {
+      c->err = "internal inconsistency: a closure after the BFS certificate reached a node with e < 0";
+      return GC_ERR_CUDA;
+    }
     if (*c->habort) c->err = "solve timed out (host watchdog)";
     return GC_ERR_NOCONV;
   }
