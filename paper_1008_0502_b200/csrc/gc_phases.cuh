@@ -886,11 +886,17 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
   __shared__ int bc[8];
   __shared__ long long red[NTH / 32];
   __shared__ uint32_t task_s;
+  __shared__ uint32_t next_s;  // continuation kept by this CTA (QEMPTY: none)
+  if (threadIdx.x == 0) next_s = QEMPTY;
   const int t = threadIdx.x;
   const bool prof = d.pns != nullptr;
   unsigned long long t_idle = 0;
   for (;;) {
-    if (t == 0) {
+    if (t == 0 && next_s != QEMPTY) {  // local continuation
+      task_s = next_s;
+      next_s = QEMPTY;
+      if (atomicAdd(d.ntask, 1ULL) >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
+    } else if (t == 0) {
       uint64_t w0 = 0;
       if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0));
       const unsigned long long tk = atomicAdd(d.qhead, 1ULL);
@@ -952,27 +958,35 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
       case M_MASK: task_mask<K>(d, io, gt); cls = 4; break;
       default: task_export<K>(d, io, gt); cls = 5; break;
     }
-    // release this task's writes, then request the neighbour tiles it changed
+    // release this task's writes, then request the neighbour tiles it changed.  One
+    // continuation stays in this CTA (next_s): the tile itself if it must run again, else
+    // the first newly queued neighbour -- dependency chains (a BFS wave, flow moving
+    // across tiles) then advance without a trip through the queue.
     fence_gpu();
     __syncthreads();
+    int rem = 0;
     if (reqd) {
+      if (t == 0) {
+        const int sub = c0 - (bc[3] ? 1 : 0);  // a push task still active keeps one request
+        rem = atomicSub(&d.treq[gt], sub) - sub;
+        if (rem > 0) next_s = (uint32_t)gt;  // requested meanwhile: run again, here
+      }
+      __syncthreads();
       const int bits = bc[1];
       if (t < 8 && ((bits >> t) & 1) && !(t >= 4 && K == 4)) {
         const long long n = side_tile(d, gt, t);
-        if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) request(d, (size_t)n, s);
+        if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) {
+          if (atomicAdd(&d.treq[n], 1) == 0) {
+            atomicAdd(&d.fout[s], 1);
+            if (atomicCAS(&next_s, QEMPTY, (uint32_t)n) != QEMPTY) q_put(d, atomicAdd(d.qtail, 1ULL), (uint32_t)n);
+          }
+        }
       }
       __syncthreads();
     }
     if (t == 0) {
       int last = 0;
-      if (reqd) {
-        const int sub = c0 - (bc[3] ? 1 : 0);  // a push task still active keeps one request
-        const int rem = atomicSub(&d.treq[gt], sub) - sub;
-        if (rem > 0) q_put(d, atomicAdd(d.qtail, 1ULL), (uint32_t)gt);  // requested meanwhile: run again
-        else last = atomicSub(&d.fout[s], 1) == 1;
-      } else {
-        last = atomicSub(&d.fout[s], 1) == 1;
-      }
+      if (!reqd || rem <= 0) last = atomicSub(&d.fout[s], 1) == 1;
       bc[3] = last;
       if (prof) {
         uint64_t w1;
