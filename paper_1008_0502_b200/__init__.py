@@ -61,6 +61,8 @@ _lib.gc_set_profiling.restype = None
 _lib.gc_get_profile.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong),
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 _lib.gc_get_profile.restype = None
+_lib.gc_debug_counters.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+_lib.gc_debug_counters.restype = None
 _lib.gc_get_kernel_ms.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.gc_get_kernel_ms.restype = ctypes.c_double
 
@@ -112,6 +114,13 @@ def gc_get_profile(ctx, reset: bool = False):
     tl = (ctypes.c_longlong * 6)()
     _lib.gc_get_profile(ctx, n, ms, tl, int(bool(reset)))
     return {c: (int(n[i]), float(ms[i]), int(tl[i])) for i, c in enumerate(PROFILE_CLASSES)}
+
+
+def debug_counters(ctx, reset: bool = False):
+    """Development counters of the push phase (profiling only; not part of gc.h)."""
+    out = (ctypes.c_ulonglong * 16)()
+    _lib.gc_debug_counters(ctx, out, int(bool(reset)))
+    return list(out)
 
 
 def gc_get_kernel_ms(ctx, reset: bool = False) -> float:

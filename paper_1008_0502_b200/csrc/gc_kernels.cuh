@@ -86,6 +86,8 @@ struct Dev {
   int32_t* fprog;   // [nslot] value of fvis after the last push task that made progress
   int32_t* cep;     // [nslot] closure attempts so far (epoch = cep % 255 + 1)
   int32_t* cfail;   // [nslot] the running closure attempt reached a node with e < 0
+  int32_t* fdrain;  // [nslot] the running push phase drains (no new requests)
+  int32_t* fhmin;   // [nslot] lowest height of an active pixel seen in the running push phase
   int32_t* fstat;   // [nslot][4] push tasks, global relabels, BFS relax tasks, -
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]
@@ -100,6 +102,7 @@ struct Dev {
   const volatile int32_t* hostabort;  // mapped host word: the host asks the kernel to stop
   unsigned long long* ptiles;  // [6] tasks per class (profiling only, else NULL)
   unsigned long long* pns;     // [6] ns per class summed over CTAs (profiling only)
+  unsigned long long* pdbg;    // [16] development counters (profiling only)
 };
 
 enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_MASK = 6, M_EXPORT = 7, M_IDLE = 8 };

@@ -44,6 +44,7 @@ struct Ctl {
   int vis_budget;            // push tasks per push phase
   int stall;                 // push tasks without progress before the phase drains
   int wave;                  // push phase starts on active tiles with min height <= lowest + wave
+  int selfrun;               // 0: an active tile always runs again; 1: only after progress
   int rounds;                // push/relabel rounds per push task
   int nframes;
   int vec;                   // caller rows 16-byte aligned: int4 loads in the init pass
@@ -536,15 +537,22 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
   if (t == 0) {
     // phase budget spent or no progress lately: the frame drains to the next global relabel
     const int vis = __ldcg(d.fvis + s);
-    bc[0] = ((long long)__ldcg(d.frel + s) > c.relabel_budget) || (vis >= c.vis_budget) ||
-            (vis - __ldcg(d.fprog + s) > c.stall);
+    const int cep = __ldcg(d.cep + s);  // failed certificate attempts: longer phases
+    const bool cond = ((long long)__ldcg(d.frel + s) > (c.relabel_budget << min(cep, 10))) || (vis >= c.vis_budget) ||
+                      (vis - __ldcg(d.fprog + s) > c.stall);
+    bc[0] = cond || __ldcg(d.fdrain + s);
+    if (cond) d.fdrain[s] = 1;  // no more requests in this phase
     bc[1] = 0;
     bc[2] = __ldcg(d.recv1 + gt);
     bc[3] = 0;
     bc[4] = __ldcg(d.tuni + gt);
+    bc[5] = HINF;
   }
   __syncthreads();
-  if (bc[0]) return;
+  if (bc[0]) {
+    if (d.pdbg && t == 0) atomicAdd(&d.pdbg[4], 1ULL);
+    return;
+  }
   const int rcv = bc[2], uni = bc[4];
   tile_load_smem<K>(d, io, gt, es, rs);
   long long neg0 = 0;  // deficit of the tile before the task (flow absorbed = progress)
@@ -571,8 +579,16 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
   __syncthreads();
   int nrel = 0;  // relabel operations (global-relabel heuristic)
   int cb = 0;    // current height buffer
-  for (int rd = 0; rd < c.rounds; ++rd) {
+  // rounds: c.rounds, extended block by block (up to 8x) while the last block moved flow
+  // out of the tile or into deficit nodes (long-distance transport)
+  int blockprog = 0;
+  for (int rd = 0;; ++rd) {
+    if (rd >= c.rounds && (rd % c.rounds) == 0) {
+      if (!blockprog || rd >= 8 * c.rounds) break;
+      blockprog = 0;
+    }
     const int* hc = hb[cb];
+    int prog = 0;
     // push phase (owner)
 #pragma unroll 1
     for (int j = 0; j < 4; ++j) {
@@ -591,9 +607,10 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
             rs[k * TPX + lp] = rk - dl;
             if (crosses(k, iy, ix)) {
               oacc[k][recv_slot(k, (iy + DYk(k)) & 31, (ix + DXk(k)) & 31)] += dl;
+              prog = 1;
             } else {
               const int u = (iy + DYk(k)) * TS + ix + DXk(k);
-              atomicAdd(&es[u], dl);
+              prog |= atomicAdd(&es[u], dl) < 0;  // reached a deficit node
               rs[(k ^ 1) * TPX + u] += dl;  // unique writer: u cannot push back to v this round
             }
           }
@@ -630,10 +647,13 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
       hn[hidx(iy, ix)] = h2;
     }
     cb ^= 1;
-    if (!__syncthreads_or(still)) break;  // tile discharged: nothing left to push
+    if (d.pdbg && t == 0) atomicAdd(&d.pdbg[5], 1ULL);
+    const int flags = __syncthreads_or(still | (prog << 1));
+    blockprog |= flags & 2;
+    if (!(flags & 1)) break;  // tile discharged: nothing left to push
   }
   // store state
-  int act = 0;
+  int act = 0, amin = HINF;
   long long neg1 = 0;
   {
     int h[4];
@@ -644,8 +664,11 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
       h[j] = hb[cb][hidx(iy0 + 8 * j, ix)];
       d.h[gt * TPX + lp] = h[j];
       act |= (ev > 0) & (h[j] < HINF);
+      if (ev > 0) amin = min(amin, h[j]);
       neg1 += ev < 0 ? -(long long)ev : 0;
     }
+    amin = __reduce_min_sync(0xffffffffu, amin);
+    if ((t & 31) == 0 && amin < HINF) atomicMin(&bc[5], amin);
     tile_store_smem<K>(d, gt, es, rs);
     store_hedge(d, gt, h, t);
   }
@@ -687,16 +710,33 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     long long ab = 0;
     for (int i = 0; i < NTH / 32; ++i) ab += red[i];
     const int ph = d.fph[s];
-    const bool first = d.tph[gt] != ph;  // first visit in this phase: transport progress
+    const bool first = d.tph[gt] != ph;  // first visit in this phase
     d.tph[gt] = ph;
     d.tact[gt] = act;
     d.mat[gt] = 1;
     d.tuni[gt] = 0;
     d.tfix[gt] = 0;
     const int v = atomicAdd(&d.fvis[s], 1) + 1;
-    if (ab > 0 || first) atomicMax(&d.fprog[s], v);
+    // progress: flow absorbed by deficit nodes, or excess at a height lower than any seen
+    // so far in the phase (flow moving toward the sink; excess that only sloshes and
+    // climbs does not count), or -- once a certificate attempt has failed, i.e. flow has
+    // far to go -- excess reaching a tile for the first time in the phase
+    const bool lower = bc[5] < HINF && atomicMin(&d.fhmin[s], bc[5]) > bc[5];
+    if (ab > 0 || lower || (first && d.cep[s] > 0)) atomicMax(&d.fprog[s], v);
     atomicAdd(&d.fstat[s * 4 + 0], 1);
-    bc[3] = act;
+    // run again only if this task got somewhere: flow absorbed by deficit nodes or sent
+    // across the border.  A tile whose excess only sloshed and climbed waits for the
+    // next certificate attempt / global relabel instead of spinning on stale labels.
+    bc[3] = act && (c.selfrun == 0 || ab > 0 || sides != 0);
+    if (d.pdbg) {
+      atomicAdd(&d.pdbg[0], 1ULL);
+      if (lower) atomicAdd(&d.pdbg[1], 1ULL);
+      if (ab > 0) atomicAdd(&d.pdbg[2], 1ULL);
+      if (sides) atomicAdd(&d.pdbg[3], 1ULL);
+      if (act) atomicAdd(&d.pdbg[6], 1ULL);
+      if (rcv) atomicAdd(&d.pdbg[7], 1ULL);
+      if (!lower && ab <= 0 && !sides) atomicAdd(&d.pdbg[8], 1ULL);
+    }
   }
 }
 
@@ -746,7 +786,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     nact = __syncthreads_or(nact);
     // push wave: the phase starts on the active tiles nearest the sink; farther ones wait
     // for the next global relabel (most are cut off by then) unless flow reaches them
-    const int hcap = md == M_BFS ? (bc[6] > HINF - c.wave ? HINF : bc[6] + c.wave) : HINF;
+    const int hcap = (md == M_BFS && __ldcg(d.cep + s) == 0) ? (bc[6] > HINF - c.wave ? HINF : bc[6] + c.wave) : HINF;
     if (t == 0) {
       int nm = md, kind = SET_ALL;
       int* st = d.fstat + s * 4;
@@ -765,6 +805,8 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.frel[s] = 0;
           d.fvis[s] = 0;
           d.fprog[s] = 0;
+          d.fdrain[s] = 0;
+          d.fhmin[s] = HINF;
           d.fph[s] += 1;
         } else {
           nm = M_CSEED;  // termination certificate: the preflow is maximum
@@ -812,7 +854,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.fph[s] = 0; d.fvis[s] = 0; d.fprog[s] = 0;
           st[0] = st[1] = st[2] = st[3] = 0;
           d.frel[s] = 0; d.sumct[s] = 0; d.sumneg[s] = 0;
-          d.cep[s] = 0; d.cfail[s] = 0;
+          d.cep[s] = 0; d.cfail[s] = 0; d.fdrain[s] = 0;
           nm = M_INIT;
         } else {
           nm = M_IDLE;
@@ -967,12 +1009,21 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
     int rem = 0;
     if (reqd) {
       if (t == 0) {
-        const int sub = c0 - (bc[3] ? 1 : 0);  // a push task still active keeps one request
-        rem = atomicSub(&d.treq[gt], sub) - sub;
-        if (rem > 0) next_s = (uint32_t)gt;  // requested meanwhile: run again, here
+        const bool drain = md == M_PUSH && __ldcg(d.fdrain + s);
+        if (drain) {
+          // the phase drains: drop the requests (inflow stays flagged in recv1 and is absorbed
+          // by the next closure seed / seed)
+          atomicExch(&d.treq[gt], 0);
+          rem = 0;
+        } else {
+          const int sub = c0 - (bc[3] ? 1 : 0);  // a push task still active keeps one request
+          rem = atomicSub(&d.treq[gt], sub) - sub;
+          if (rem > 0) next_s = (uint32_t)gt;  // requested meanwhile: run again, here
+        }
+        bc[6] = drain;
       }
       __syncthreads();
-      const int bits = bc[1];
+      const int bits = bc[6] ? 0 : bc[1];
       if (t < 8 && ((bits >> t) & 1) && !(t >= 4 && K == 4)) {
         const long long n = side_tile(d, gt, t);
         if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) {

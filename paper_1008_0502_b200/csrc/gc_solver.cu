@@ -33,6 +33,7 @@ struct gc_ctx {
   int vis_mult = 64;              // push tasks per push phase = vis_mult x frame tiles
   int stall = 64;                 // push tasks without progress before a push phase drains
   int wave = 32;                  // push wave width (heights above the lowest active one)
+  int selfrun = 0;                // 1: a push tile re-runs itself only after progress
   int grid = 0;                   // k_solve CTAs of the last launch
   std::string err;
   long long last_launches = 0;
@@ -42,6 +43,7 @@ struct gc_ctx {
   unsigned long long* dtiles = nullptr;  // device counters [12]: tasks [6], ns [6]
   double prof_ms[6] = {0, 0, 0, 0, 0, 0};
   double kernel_ms = 0;
+  unsigned long long dbg[16] = {0};  // development counters (profiling only)
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   size_t evnext = 0;
@@ -102,6 +104,8 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.fprog = w; w += nslot;
   d.cep = w; w += nslot;
   d.cfail = w; w += nslot;
+  d.fdrain = w; w += nslot;
+  d.fhmin = w; w += nslot;
   d.fstat = w; w += 4 * nslot;
   d.gctr = w; w += 4;
   d.done = w; w += 4;
@@ -142,6 +146,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.hostabort = c->habort_dev;
   d.ptiles = c->prof ? c->dtiles : nullptr;
   d.pns = c->prof ? c->dtiles + 6 : nullptr;
+  d.pdbg = c->prof ? c->dtiles + 12 : nullptr;
   return d;
 }
 
@@ -163,8 +168,9 @@ struct Launcher {
 // Profiling counters of the last solve: tasks and summed CTA time per class, plus the
 // device time of each k_solve launch (CUDA events on the launching stream).
 void resolve_profile(gc_ctx* c) {
-  unsigned long long t[12];
+  unsigned long long t[28];
   if (cudaMemcpy(t, c->dtiles, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
+    for (int i = 0; i < 16; ++i) c->dbg[i] += t[12 + i];
     for (int i = 0; i < 6; ++i) {
       c->prof_tiles[i] += (long long)t[i];
       // CTA-time of the class averaged over the persistent grid: the classes (3 = queue
@@ -237,6 +243,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   ctl.vis_budget = c->vis_mult * d.T;
   ctl.stall = c->stall;
   ctl.wave = c->wave;
+  ctl.selfrun = c->selfrun;
   ctl.rounds = c->rounds;
   ctl.nframes = nframes;
   // int4 loads in the init pass when every caller row is 16-byte aligned
@@ -353,6 +360,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (const char* ev = getenv("GC_VIS")) c->vis_mult = atoi(ev);
   if (const char* ev = getenv("GC_STALL")) c->stall = atoi(ev);
   if (const char* ev = getenv("GC_WAVE")) c->wave = atoi(ev);
+  if (const char* ev = getenv("GC_SELFRUN")) c->selfrun = atoi(ev);
   if (const char* ev = getenv("GC_TIMEOUT_S")) c->timeout_s = atof(ev);
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
   if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
@@ -375,8 +383,8 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   c->pool_bytes = nf * fb;
   if (cudaMalloc(&c->pool, c->pool_bytes) != cudaSuccess) { cudaGetLastError(); delete c; return GC_ERR_OOM; }
   if (cudaMallocHost(&c->hpin, 64) != cudaSuccess) { cudaFree(c->pool); delete c; return GC_ERR_OOM; }
-  if (cudaMalloc(&c->dtiles, 128) != cudaSuccess) { cudaFree(c->pool); cudaFreeHost(c->hpin); delete c; return GC_ERR_OOM; }
-  cudaMemset(c->dtiles, 0, 128);
+  if (cudaMalloc(&c->dtiles, 256) != cudaSuccess) { cudaFree(c->pool); cudaFreeHost(c->hpin); delete c; return GC_ERR_OOM; }
+  cudaMemset(c->dtiles, 0, 256);
   if (cudaHostAlloc(&c->habort, 64, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void**)&c->habort_dev, c->habort, 0) != cudaSuccess) {
     cudaGetLastError();
@@ -418,6 +426,15 @@ void gc_get_profile(gc_ctx* c, long long* launches, double* ms, long long* tiles
   }
   if (reset)
     for (int i = 0; i < 6; ++i) { c->prof_n[i] = 0; c->prof_ms[i] = 0; c->prof_tiles[i] = 0; }
+}
+
+// Development counters of the push phase (profiling only; not part of gc.h).
+void gc_debug_counters(gc_ctx* c, unsigned long long* out16, int reset) {
+  if (!c) return;
+  for (int i = 0; i < 16; ++i) {
+    if (out16) out16[i] = c->dbg[i];
+    if (reset) c->dbg[i] = 0;
+  }
 }
 
 double gc_get_kernel_ms(gc_ctx* c, int reset) {

@@ -20,7 +20,7 @@ seed_off = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 kind, H, W, K = ALL[name]
 if kind == "serpentine":
     synth.set_serpentine_params(lane=64, big=1 << 20)
-cs, ct, nb = synth.gen_torch(kind, synth.BASE_SEED + seed_off, 0, n, H, W, K)
+cs, ct, nb = synth.gen_torch(kind, synth.BASE_SEED + seed_off, int(os.environ.get("T0", "0")), n, H, W, K)
 ref = None
 keys = [k for k, _ in knobs]
 for vals in itertools.product(*[v.split(",") for _, v in knobs]):
@@ -42,12 +42,15 @@ for vals in itertools.product(*[v.split(",") for _, v in knobs]):
     g.set_profiling(True); g.profile(reset=True); g.kernel_ms(reset=True)
     g.solve(cs, ct, nb); torch.cuda.synchronize()
     prof = g.profile(reset=True)
+    dbg = gc.debug_counters(g.ctx, reset=True)
     stf = st.float()
     hard = torch.argsort(st[:, 0], descending=True)[:4].tolist()
     print(json.dumps({"cfg": name, "n": n, **env, "ms": round(best, 3), "Mpx_s": round(n * H * W / best / 1e3, 1),
                       "st_mean": [round(x, 1) for x in stf.mean(0).tolist()[:3]], "st_max": st.max(0).values.tolist()[:3],
                       "hard": hard, "cta_ms": {k: round(v[1], 2) for k, v in prof.items()},
-                      "tasks": {k: v[2] for k, v in prof.items()}}), flush=True)
+                      "tasks": {k: v[2] for k, v in prof.items()},
+                      "push_dbg": dict(zip(["real", "lower", "absorbed", "sent", "drained", "rounds", "act_end",
+                                            "recv", "noprog"], dbg[:9]))}), flush=True)
     g.close()
     del g
     for k in env:
