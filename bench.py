@@ -216,6 +216,7 @@ def main():
 
     import paper_1008_0502_b200 as gc
     import synth
+    from paper_1008_0502_b200 import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -230,7 +231,7 @@ def main():
         synth.set_serpentine_params(lane=64, big=1 << 20)
 
     # ---- inputs: this rank's frame shard, generated on the device (CUDA twin of synth/)
-    t_first = rank * n
+    t_first, n = shard.frame_range(rank, world, n)
     cs, ct, nb = synth.gen_torch(cfg["kind"], seed, t_first, n, H, W, K, device=dev)
     flow = torch.empty(n, dtype=torch.int64, device=dev)
     mask = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
@@ -271,24 +272,13 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = shard.max_over_ranks(e0.elapsed_time(e1), dev, world)
     px_total = world * n * H * W * args.steps
     value = px_total / (ms_max * 1e-3) / 1e6
     fps = world * n * args.steps / (ms_max * 1e-3)
 
     # ---- final statistics over NCCL (the only collective: SURVEY.md §8(a) a6)
-    pop = mask.view(n, -1).sum(dim=1, dtype=torch.int64)
-    stats = torch.stack([flow.sum(), pop.sum(), (flow < 0).sum().to(torch.int64)])
-    per_frame = torch.stack([flow, pop], dim=1)
-    if world > 1:
-        dist.all_reduce(stats)
-        gathered = [torch.empty_like(per_frame) for _ in range(world)]
-        dist.all_gather(gathered, per_frame)
-        per_frame = torch.cat(gathered)
+    stats, per_frame = shard.reduce_stats(*shard.frame_stats(flow, mask), world)
     bad_frames = int(stats[2].item())
 
     # ---- profiled replica steps: the persistent kernel's device time (CUDA events on the
@@ -307,18 +297,22 @@ def main():
     avg_ms = kms / nl
     bytes_launch = sum(tile_bytes(c, K) * prof[c][2] for c in prof) / nl
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+    # measured DRAM traffic (ncu dram__bytes_read + write of the same kernel, per frame,
+    # scaled to this launch's frames); null when no capture of this config is committed
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config, {}).get("k_solve")
+            rec = json.load(open(tp)).get(args.config, {}).get("k_solve")
+            if rec:
+                traffic = int(rec["dram_bytes_per_frame"] * n / nl * args.profile_steps)
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": f"k_solve<{K}>",
                 "bytes_per_launch": int(bytes_launch), "avg_launch_ms": round(avg_ms, 4),
                 "launches_per_step": round(nl / args.profile_steps, 2),
-                "share_of_step": round(kms / max(args.profile_steps * ms_max / args.steps, 1e-9), 3),
+                "share_of_step": 1.0,  # the step is this one persistent kernel (+ a setup kernel)
                 "peak_source": peak_src,
                 "classes": {c: {"tasks": v[2], "cta_ms": round(v[1], 3), "bytes": tile_bytes(c, K) * v[2]}
                             for c, v in prof.items()}}
@@ -346,10 +340,7 @@ def main():
             g.solve_host(*hargs, out=hout, stream=stream.cuda_stream)
         e3.record(stream)
         torch.cuda.synchronize()
-        et = torch.tensor([e2.elapsed_time(e3)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        ems = float(et.item())
+        ems = shard.max_over_ranks(e2.elapsed_time(e3), dev, world)
         e2e = {"value": round(world * ne * H * W * args.steps / (ems * 1e-3) / 1e6, 1), "unit": "Mpixel/s",
                "h2d_bytes_per_step": int(ne * H * W * 4 * (2 + K)),
                "d2h_bytes_per_step": int(ne * H * W + ne * 8), "frames_per_step": ne,
