@@ -200,9 +200,16 @@ int persistent_grid(gc_ctx* c, F kernel, size_t dyn_smem = 0) {
   return sms * per;
 }
 
+// Frame slots of a call: as many as the pool holds, but no more than needed to keep the
+// GPU busy -- about 40k tiles in flight, at least 24 frames.  More slots only lengthen the
+// task queue, i.e. the latency of every dependency-chain step (measured: 1080p 8-nbr runs
+// fastest with 15-40 slots, QVGA / VGA level off at 8k-16k tiles in flight).
 int chunk_frames(gc_ctx* c, int H, int W) {
-  const size_t fb = frame_bytes(c->K, tiles_of(H, W));
+  const size_t T = tiles_of(H, W);
+  const size_t fb = frame_bytes(c->K, T);
   size_t n = c->pool_bytes / fb;
+  const size_t want = T >= 40000 / 24 ? 24 : (40000 + T - 1) / T;
+  if (n > want) n = want;
   if (n < 1) n = 1;
   if (c->max_batch > 0 && n > (size_t)c->max_batch) n = c->max_batch;
   const char* env = getenv("GC_CHUNK");
