@@ -933,16 +933,17 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
   const int t = threadIdx.x;
   const bool prof = d.pns != nullptr;
   unsigned long long t_idle = 0;
+  unsigned long long tick = 0;  // thread 0: queue ticket
+  unsigned ntask_local = 0;
   for (;;) {
     if (t == 0 && next_s != QEMPTY) {  // local continuation
       task_s = next_s;
       next_s = QEMPTY;
-      if (atomicAdd(d.ntask, 1ULL) >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
     } else if (t == 0) {
       uint64_t w0 = 0;
       if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0));
-      const unsigned long long tk = atomicAdd(d.qhead, 1ULL);
-      volatile uint32_t* slot = d.q + (tk & d.qmask);
+      tick = atomicAdd(d.qhead, 1ULL);
+      volatile uint32_t* slot = d.q + (tick & d.qmask);
       uint32_t v;
       int ns = 32, spins = 0;
       while ((v = *slot) == QEMPTY) {
@@ -951,10 +952,7 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
         __nanosleep(ns);
         ns = ns < 1024 ? 2 * ns : 1024;
       }
-      if (v != QEXIT) {
-        *slot = QEMPTY;
-        if (atomicAdd(d.ntask, 1ULL) >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
-      }
+      if (v != QEXIT) *slot = QEMPTY;
       if (prof) {
         uint64_t w1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
@@ -962,6 +960,9 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
       }
       task_s = v;
     }
+    if (t == 0 && (++ntask_local & 15) == 0 &&
+        atomicAdd(d.ntask, 16ULL) + 16 >= (unsigned long long)c.max_tasks)  // watchdog
+      *(volatile int*)&d.done[1] = 1;
     __syncthreads();
     const uint32_t v = task_s;
     if (v == QEXIT || *(volatile int*)&d.done[1]) break;
