@@ -502,61 +502,142 @@ __device__ __forceinline__ void tile_store_smem(const Dev& d, size_t gt, const i
 // 2-byte fl word per pixel, the frame's sum c(v,t), the tile's sum max(0,-e) and the
 // range flag.  Thread t owns 4 consecutive pixels of row t/8 (int4 loads when the caller's
 // rows are 16-byte aligned).
+// Caller-layout pointers of the frame a slot holds.
+struct FramePtrs {
+  size_t fr;  // batch frame index
+  const int32_t* cs;
+  const int32_t* ct;
+  const int32_t* nb;
+  const int32_t* wf;
+};
+__device__ __forceinline__ FramePtrs frame_ptrs(const Dev& d, const IO& io, int s, int K) {
+  const size_t plane = (size_t)d.H * d.W;
+  const size_t fr = (size_t)d.sfr[s];  // batch frame held by this slot
+  FramePtrs p;
+  p.fr = fr;
+  p.cs = io.cs + fr * plane;
+  p.ct = io.ct + fr * plane;
+  p.nb = io.nb + fr * plane * K;
+  p.wf = io.wf ? io.wf + fr * plane * (K / 2) : nullptr;
+  return p;
+}
+
+// Init pass, cap loads: thread t owns the 4 consecutive pixels (t/8, 4(t%8)..+3) of the tile.
 template <int K>
-__device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt, bool vec, long long (*red)[NTH / 32]) {
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+__device__ __forceinline__ void init_load(const Dev& d, const FramePtrs& P, int ty, int tx, bool vec, int (&a)[4],
+                                          int (&b)[4], int (&c)[K][4]) {
   const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
-  const size_t fr = (size_t)d.sfr[s];  // batch frame held by this slot
-  const int32_t* cs = io.cs + fr * plane;
-  const int32_t* ct = io.ct + fr * plane;
-  const int32_t* nb = io.nb + fr * plane * K;
-  const int32_t* wf = io.wf ? io.wf + fr * plane * (K / 2) : nullptr;
   const int y = ty * TS + iy, x0 = tx * TS + ix0;
-  int bad = 0, uni = 1;
-  long long sct = 0, neg = 0;
-  int a[4] = {0, 0, 0, 0}, b[4] = {0, 0, 0, 0}, c[K][4];
   const size_t o0 = (size_t)y * W + x0;
-  const bool full = vec && y < H && x0 + 3 < W;
-  if (full) {
-    const int4 va = __ldg(reinterpret_cast<const int4*>(cs + o0));
-    const int4 vb = __ldg(reinterpret_cast<const int4*>(ct + o0));
+  if (vec && y < H && x0 + 3 < W) {
+    const int4 va = __ldg(reinterpret_cast<const int4*>(P.cs + o0));
+    const int4 vb = __ldg(reinterpret_cast<const int4*>(P.ct + o0));
     a[0] = va.x; a[1] = va.y; a[2] = va.z; a[3] = va.w;
     b[0] = vb.x; b[1] = vb.y; b[2] = vb.z; b[3] = vb.w;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const int4 v = __ldg(reinterpret_cast<const int4*>(nb + k * plane + o0));
+      const int4 v = __ldg(reinterpret_cast<const int4*>(P.nb + k * plane + o0));
       c[k][0] = v.x; c[k][1] = v.y; c[k][2] = v.z; c[k][3] = v.w;
     }
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const bool in = y < H && x0 + i < W;
-      a[i] = in ? __ldg(cs + o0 + i) : 0;
-      b[i] = in ? __ldg(ct + o0 + i) : 0;
+      a[i] = in ? __ldg(P.cs + o0 + i) : 0;
+      b[i] = in ? __ldg(P.ct + o0 + i) : 0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) c[k][i] = in ? __ldg(nb + k * plane + o0 + i) : 0;
+      for (int k = 0; k < K; ++k) c[k][i] = in ? __ldg(P.nb + k * plane + o0 + i) : 0;
     }
   }
+}
+
+// Init pass, asynchronous variant (rows 16-byte aligned): each thread copies its 16-byte
+// chunks of the 2 + K planes into its own slots of shared memory with cp.async (zero-fill
+// below the frame), so the next tile's caps stream in while this tile is computed.  Only
+// the issuing thread ever reads its slots back: no barrier is needed between the copy and
+// its use, nor before the slots are refilled.
+template <int K>
+__device__ __forceinline__ void init_prefetch(const Dev& d, const FramePtrs& P, int ty, int tx, int4* stage) {
+  const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
+  const size_t plane = (size_t)d.H * d.W;
+  const int y = ty * TS + iy, x0 = tx * TS + ix0;
+  const bool in = y < d.H && x0 < d.W;  // W % 4 == 0: the whole chunk is in the frame
+  const size_t o0 = in ? (size_t)y * d.W + x0 : 0;
+  const int src = in ? 16 : 0;
+#pragma unroll
+  for (int pl = 0; pl < 2 + K; ++pl) {
+    const int32_t* g = pl == 0 ? P.cs + o0 : (pl == 1 ? P.ct + o0 : P.nb + (size_t)(pl - 2) * plane + o0);
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(stage + pl * NTH + t);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(src) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void init_from_stage(const int4* stage, int (&a)[4], int (&b)[4], int (&c)[K][4]) {
+  const int t = threadIdx.x;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  const int4 va = stage[t], vb = stage[NTH + t];
+  a[0] = va.x; a[1] = va.y; a[2] = va.z; a[3] = va.w;
+  b[0] = vb.x; b[1] = vb.y; b[2] = vb.z; b[3] = vb.w;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int4 v = stage[(2 + k) * NTH + t];
+    c[k][0] = v.x; c[k][1] = v.y; c[k][2] = v.z; c[k][3] = v.w;
+  }
+}
+
+// Init pass, per tile once the caps are in registers: computes e and r (the tile stays
+// un-materialised -- e, r are recomputed if a push ever touches it) and writes only the
+// 2-byte fl word per pixel, zeroes the caller's mask, flags a uniform sink tile, and adds
+// the tile's sum c(v,t) and sum max(0,-e) to the frame (range flag on bad caps).
+template <int K, bool WARM>
+__device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_t gt, const FramePtrs& P,
+                                               const int (&a)[4], const int (&b)[4], const int (&c)[K][4],
+                                               long long (*red)[NTH / 32]) {
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
+  const int H = d.H, W = d.W;
+  const size_t plane = (size_t)H * W;
+  const size_t fr = P.fr;
+  const int32_t* nb = P.nb;
+  const int32_t* wf = P.wf;
+  const int y = ty * TS + iy, x0 = tx * TS + ix0;
+  const size_t o0 = (size_t)y * W + x0;
+  // arcs whose far end is in the frame: all of them for tiles away from the frame border
+  const bool inner = ty > 0 && tx > 0 && (ty + 1) * TS < H && (tx + 1) * TS < W;
+  int acc = 0;  // OR of every in-grid capacity: one is outside [0, GC_CAP_MAX] iff acc & ~CAPMAX
+  int uni = 1;
+  long long sct = 0, neg = 0;
   int fl4[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int x = x0 + i;
     int f = 0;
-    if (y < H && x < W) {
-      bad |= (a[i] < 0) | (a[i] > CAPMAX) | (b[i] < 0) | (b[i] > CAPMAX);
+    if (inner || (y < H && x < W)) {
+      int vm = 0xff;  // valid-arc mask (reading c7: off-grid arcs are ignored)
+      if (!inner) {
+        vm = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int y2 = y + DYk(k), x2 = x + DXk(k);
+          vm |= ((unsigned)y2 < (unsigned)H && (unsigned)x2 < (unsigned)W) << k;
+        }
+      }
+      acc |= a[i] | b[i];
       int ev = a[i] - b[i];  // a1: pre-cancel min(cs,ct) straight s -> v -> t
       sct += b[i];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const int y2 = y + DYk(k), x2 = x + DXk(k);
-        if (y2 < 0 || y2 >= H || x2 < 0 || x2 >= W) continue;  // off-grid: ignored (c7)
-        const int ck = c[k][i];
-        bad |= (ck < 0) | (ck > CAPMAX);
+        const int on = (vm >> k) & 1;
+        const int ck = on ? c[k][i] : 0;
+        acc |= ck;
         int rk = ck;
-        if (wf) {  // a1w: clamp the previous flow to the new capacities
+        if (WARM && on) {  // a1w: clamp the previous flow to the new capacities
+          const int y2 = y + DYk(k), x2 = x + DXk(k);
           const size_t oq = (size_t)y2 * W + x2;
           const int cq = __ldg(nb + (k ^ 1) * plane + oq);
           if ((k & 1) == 0) {
@@ -577,6 +658,7 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
     }
     fl4[i] = f;
   }
+  int bad = (acc & ~CAPMAX) != 0;
   ushort4 w;
   w.x = (unsigned short)fl4[0]; w.y = (unsigned short)fl4[1];
   w.z = (unsigned short)fl4[2]; w.w = (unsigned short)fl4[3];
@@ -591,7 +673,7 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
         if (x0 + i < W) mk[i] = 0;
     }
   }
-  for (int i = t; i < K * 64; i += NTH) d.reach[gt * K * 64 + i] = 0;
+  if (t < K * 16) reinterpret_cast<uint32_t*>(d.reach + gt * K * 64)[t] = 0u;
   bad = __syncthreads_or(bad);
   uni = __syncthreads_and(uni);
   if (uni && t < 128) {  // uniform sink tile: publish its border heights now (h = 1 in frame)
@@ -624,6 +706,40 @@ __device__ __forceinline__ void tile_init(const Dev& d, const IO& io, size_t gt,
     if (bad) d.ferr[s] = 1;
   }
   __syncthreads();
+}
+
+// a1 / a1w: one init task = a group of INIT_G consecutive tiles of a frame; with aligned rows
+// the caps of tile i+1 are copied to shared memory (cp.async) while tile i is computed.
+constexpr int INIT_G = 4;
+
+template <int K>
+constexpr size_t init_stage_bytes() { return sizeof(int4) * (2 + K) * NTH; }
+
+template <int K>
+__device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, long long (*red)[NTH / 32],
+                                          int4* stage) {
+  const int s = (int)(gt0 / d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
+  const int n = min(INIT_G, d.T - tile0);
+  const FramePtrs P = frame_ptrs(d, io, s, K);
+  int a[4], b[4], c[K][4];
+  if (!vec) {
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) {
+      const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
+      init_load<K>(d, P, ty, tx, false, a, b, c);
+      if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, red);
+      else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, red);
+    }
+    return;
+  }
+  init_prefetch<K>(d, P, tile0 / d.TX, tile0 % d.TX, stage);
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    init_from_stage<K>(stage, a, b, c);
+    if (i + 1 < n) init_prefetch<K>(d, P, (tile0 + i + 1) / d.TX, (tile0 + i + 1) % d.TX, stage);
+    if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, red);
+    else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, red);
+  }
 }
 
 }  // namespace gcb

@@ -744,7 +744,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
 // first task set of a phase: NONE = the slot idles; EMPTY = no task (the next transition
 // follows at once)
 enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_CSEED = 5, SET_EMPTY = 6,
-       SET_MASK = 7 };
+       SET_MASK = 7, SET_INITG = 8 };
 
 __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
   const int f = d.sfr[s];
@@ -856,6 +856,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.frel[s] = 0; d.sumct[s] = 0; d.sumneg[s] = 0;
           d.cep[s] = 0; d.cfail[s] = 0; d.fdrain[s] = 0;
           nm = M_INIT;
+          kind = SET_INITG;
         } else {
           nm = M_IDLE;
           kind = SET_NONE;
@@ -875,6 +876,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (i < d.T) {
         const size_t gt = base_gt + i;
         if (kind == SET_ALL) want = 1;
+        else if (kind == SET_INITG) want = (i % INIT_G) == 0;  // one init task per tile group
         else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1
           want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));
           d.flag[gt] = 0;
@@ -927,6 +929,7 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
   extern __shared__ int smem[];
   __shared__ int bc[8];
   __shared__ long long red[NTH / 32];
+  __shared__ long long red2[2][NTH / 32];
   __shared__ uint32_t task_s;
   __shared__ uint32_t next_s;  // continuation kept by this CTA (QEMPTY: none)
   if (threadIdx.x == 0) next_s = QEMPTY;
@@ -982,7 +985,7 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
     __syncthreads();
     int cls = 0;
     switch (md) {
-      case M_INIT: tile_init<K>(d, io, gt, c.vec != 0, reinterpret_cast<long long(*)[NTH / 32]>(smem)); cls = 0; break;
+      case M_INIT: task_init<K>(d, io, gt, c.vec != 0, red2, reinterpret_cast<int4*>(smem)); cls = 0; break;
       case M_SEED: task_seed<K>(d, io, gt, smem, bc); cls = 1; break;
       case M_BFS:
         task_relax<K>(d, gt, smem, bc);
@@ -1062,19 +1065,22 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
   if (prof && t == 0) atomicAdd(&d.pns[3], t_idle);
 }
 
-// Initial slot assignment: slot s holds frame s in M_INIT, every tile of every slot queued.
+// Initial slot assignment: slot s holds frame s in M_INIT, every init tile group of every
+// slot queued.
 __global__ void k_setup(Dev d, int nframes) {
-  const size_t ns = NS(d);
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ns; i += (size_t)gridDim.x * blockDim.x) {
-    d.q[i] = (uint32_t)i;
-    if (i < (size_t)d.nslot) {
-      d.sfr[i] = (int)i;
-      d.fmode[i] = M_INIT;
-      d.fout[i] = d.T;
+  const int G = (d.T + INIT_G - 1) / INIT_G;  // init tasks per frame
+  const size_t ntask = (size_t)d.nslot * G;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ntask; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t s = i / G, g = i - s * G;
+    d.q[i] = (uint32_t)(s * d.T + g * INIT_G);
+    if (g == 0) {
+      d.sfr[s] = (int)s;
+      d.fmode[s] = M_INIT;
+      d.fout[s] = G;
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *d.qtail = ns;
+    *d.qtail = ntask;
     d.gctr[0] = d.nslot;
   }
 }
