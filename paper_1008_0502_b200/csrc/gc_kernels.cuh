@@ -49,6 +49,7 @@ __host__ __device__ constexpr int DXk(int k) {
 
 struct Dev {
   int H, W, TY, TX, T, nslot;
+  int initg;  // tiles per init task
   int hmax;  // relabel cap: heights >= hmax are unreachable (HINF)
   int32_t* e;
   int32_t* h;
@@ -681,10 +682,15 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
     const int py = side == 0 ? 0 : (side == 1 ? 31 : j), px = side == 2 ? 0 : (side == 3 ? 31 : j);
     d.hedge[gt * 128 + t] = (ty * TS + py < H && tx * TS + px < W) ? 1 : HINF;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sct += __shfl_xor_sync(0xffffffffu, sct, o);
-    neg += __shfl_xor_sync(0xffffffffu, neg, o);
+  // warp sums with REDUX on 32-bit halves (per-thread sums are < 2^31, warp sums may not be)
+  {
+    const unsigned long long us = (unsigned long long)sct, un = (unsigned long long)neg;
+    const unsigned s_lo = __reduce_add_sync(0xffffffffu, (unsigned)(us & 0xffffu));
+    const unsigned s_hi = __reduce_add_sync(0xffffffffu, (unsigned)(us >> 16));
+    const unsigned n_lo = __reduce_add_sync(0xffffffffu, (unsigned)(un & 0xffffu));
+    const unsigned n_hi = __reduce_add_sync(0xffffffffu, (unsigned)(un >> 16));
+    sct = (long long)s_lo + ((long long)s_hi << 16);
+    neg = (long long)n_lo + ((long long)n_hi << 16);
   }
   if ((t & 31) == 0) { red[0][t >> 5] = sct; red[1][t >> 5] = neg; }
   __syncthreads();
@@ -708,9 +714,10 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
   __syncthreads();
 }
 
-// a1 / a1w: one init task = a group of INIT_G consecutive tiles of a frame; with aligned rows
-// the caps of tile i+1 are copied to shared memory (cp.async) while tile i is computed.
-constexpr int INIT_G = 4;
+// a1 / a1w: one init task = a group of d.initg consecutive tiles of a frame (more tiles per
+// task on large frames: less per-task overhead; one on small frames: more parallelism);
+// with aligned rows the caps of tile i+1 are copied to shared memory (cp.async) while tile
+// i is computed.
 
 template <int K>
 constexpr size_t init_stage_bytes() { return sizeof(int4) * (2 + K) * NTH; }
@@ -719,7 +726,7 @@ template <int K>
 __device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, long long (*red)[NTH / 32],
                                           int4* stage) {
   const int s = (int)(gt0 / d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
-  const int n = min(INIT_G, d.T - tile0);
+  const int n = min(d.initg, d.T - tile0);
   const FramePtrs P = frame_ptrs(d, io, s, K);
   int a[4], b[4], c[K][4];
   if (!vec) {

@@ -35,6 +35,9 @@
 
 namespace gcb {
 
+#ifndef GC_MINB
+#define GC_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr uint32_t QEMPTY = 0xffffffffu;
 constexpr uint32_t QEXIT = 0xfffffffeu;
 
@@ -61,14 +64,9 @@ __device__ __forceinline__ void q_put(const Dev& d, unsigned long long p, uint32
   *slot = v;
 }
 
-// One thread: enqueue tile gt of frame slot s in a request-driven phase.  The caller has
-// fenced the writes the tile must see.
-__device__ __forceinline__ void request(const Dev& d, size_t gt, int s) {
-  if (atomicAdd(&d.treq[gt], 1) == 0) {
-    atomicAdd(&d.fout[s], 1);
-    q_put(d, atomicAdd(d.qtail, 1ULL), (uint32_t)gt);
-  }
-}
+// Queue entry: the phase a task belongs to (it cannot change while the task is queued) and
+// the tile.
+__device__ __forceinline__ uint32_t qent(int md, size_t gt) { return ((uint32_t)md << 28) | (uint32_t)gt; }
 
 // Neighbour tile of gt on side b (0 N, 1 S, 2 W, 3 E, 4 NW, 5 NE, 6 SW, 7 SE); -1 if off-frame.
 __device__ __forceinline__ long long side_tile(const Dev& d, size_t gt, int b) {
@@ -864,6 +862,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       }
       d.fmode[s] = nm;
       bc[4] = kind;
+      bc[2] = nm;
     }
     __syncthreads();
     const int kind = bc[4];
@@ -876,7 +875,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (i < d.T) {
         const size_t gt = base_gt + i;
         if (kind == SET_ALL) want = 1;
-        else if (kind == SET_INITG) want = (i % INIT_G) == 0;  // one init task per tile group
+        else if (kind == SET_INITG) want = (i % d.initg) == 0;  // one init task per tile group
         else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1
           want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));
           d.flag[gt] = 0;
@@ -909,7 +908,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       }
       __syncthreads();
       const unsigned long long p0 = ((unsigned long long)(uint32_t)bc[7] << 32) | (uint32_t)bc[6];
-      if (want) q_put(d, p0 + li, (uint32_t)(base_gt + i));
+      if (want) q_put(d, p0 + li, qent(bc[2], base_gt + i));
       __syncthreads();
     }
     if (t == 0) {
@@ -925,7 +924,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
 
 // ---------------------------------------------------------------- the persistent kernel
 template <int K>
-__global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
+__global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
   extern __shared__ int smem[];
   __shared__ int bc[8];
   __shared__ long long red[NTH / 32];
@@ -969,9 +968,9 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
     __syncthreads();
     const uint32_t v = task_s;
     if (v == QEXIT || *(volatile int*)&d.done[1]) break;
-    const size_t gt = v;
+    const size_t gt = v & 0x0fffffffu;
     const int s = (int)(gt / d.T);
-    const int md = __ldcg(d.fmode + s);
+    const int md = (int)(v >> 28);
     const bool reqd = md == M_BFS || md == M_PUSH || md == M_CLOS;  // request-driven phase
     int c0 = 0;
     uint64_t w0 = 0;
@@ -1022,7 +1021,7 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
         } else {
           const int sub = c0 - (bc[3] ? 1 : 0);  // a push task still active keeps one request
           rem = atomicSub(&d.treq[gt], sub) - sub;
-          if (rem > 0) next_s = (uint32_t)gt;  // requested meanwhile: run again, here
+          if (rem > 0) next_s = qent(md, gt);  // requested meanwhile: run again, here
         }
         bc[6] = drain;
       }
@@ -1033,7 +1032,7 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
         if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) {
           if (atomicAdd(&d.treq[n], 1) == 0) {
             atomicAdd(&d.fout[s], 1);
-            if (atomicCAS(&next_s, QEMPTY, (uint32_t)n) != QEMPTY) q_put(d, atomicAdd(d.qtail, 1ULL), (uint32_t)n);
+            if (atomicCAS(&next_s, QEMPTY, qent(md, n)) != QEMPTY) q_put(d, atomicAdd(d.qtail, 1ULL), qent(md, n));
           }
         }
       }
@@ -1068,11 +1067,11 @@ __global__ void __launch_bounds__(NTH, 4) k_solve(Dev d, IO io, Ctl c) {
 // Initial slot assignment: slot s holds frame s in M_INIT, every init tile group of every
 // slot queued.
 __global__ void k_setup(Dev d, int nframes) {
-  const int G = (d.T + INIT_G - 1) / INIT_G;  // init tasks per frame
+  const int G = (d.T + d.initg - 1) / d.initg;  // init tasks per frame
   const size_t ntask = (size_t)d.nslot * G;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ntask; i += (size_t)gridDim.x * blockDim.x) {
     const size_t s = i / G, g = i - s * G;
-    d.q[i] = (uint32_t)(s * d.T + g * INIT_G);
+    d.q[i] = qent(M_INIT, s * d.T + g * d.initg);
     if (g == 0) {
       d.sfr[s] = (int)s;
       d.fmode[s] = M_INIT;
