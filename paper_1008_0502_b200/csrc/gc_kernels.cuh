@@ -76,6 +76,8 @@ struct Dev {
                     //        open arc has h = 1)
   int32_t* tph;     // [NS]   push-phase id of the tile's last push task
   int32_t* tminh;   // [NS]   lowest height of an active pixel of the tile (HINF if none)
+  int32_t* tsk;     // [NS]   global relabel (fbe) in which the tile's seed was skipped (its
+                    //        border heights, all 1 in frame, are final for that relabel)
   // per frame slot (state machine): zero-initialised by one memset
   int32_t* fmode;   // [nslot] M_INIT, M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_EXPORT, M_IDLE
   int32_t* sfr;     // [nslot] batch frame index held by the slot
@@ -89,6 +91,7 @@ struct Dev {
   int32_t* cfail;   // [nslot] the running closure attempt reached a node with e < 0
   int32_t* fdrain;  // [nslot] the running push phase drains (no new requests)
   int32_t* fhmin;   // [nslot] lowest height of an active pixel seen in the running push phase
+  int32_t* fbe;     // [nslot] global relabels started (BFS epoch)
   int32_t* fstat;   // [nslot][4] push tasks, global relabels, BFS relax tasks, -
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]
@@ -148,6 +151,21 @@ __device__ __forceinline__ int recv_slot(int k, int uy, int ux) {
   }
 }
 
+// Sender-side view of the receiver slots: the tile (offset dy, dx from the sending tile)
+// that owns slot `sl` of direction k (inverse of recv_slot; unused slots are never written).
+__device__ __forceinline__ void recv_tile_offset(int k, int sl, int& dy, int& dx) {
+  switch (k) {
+    case 0: dy = 0; dx = 1; break;                                           // E
+    case 1: dy = 0; dx = -1; break;                                          // W
+    case 2: dy = 1; dx = 0; break;                                           // S
+    case 3: dy = -1; dx = 0; break;                                          // N
+    case 4: if (sl < 32) { dy = 1; dx = sl == 0 ? 1 : 0; } else { dy = 0; dx = 1; } break;     // SE
+    case 5: if (sl < 32) { dy = -1; dx = sl == 31 ? -1 : 0; } else { dy = 0; dx = -1; } break; // NW
+    case 6: if (sl < 32) { dy = 1; dx = sl == 31 ? -1 : 0; } else { dy = 0; dx = -1; } break;  // SW
+    default: if (sl < 32) { dy = -1; dx = sl == 0 ? 1 : 0; } else { dy = 0; dx = 1; } break;   // NE
+  }
+}
+
 __device__ __forceinline__ int hidx(int iy, int ix) { return (iy + 1) * HS + (ix + 1); }
 __device__ __forceinline__ bool on_border(int iy, int ix) { return iy == 0 || iy == 31 || ix == 0 || ix == 31; }
 
@@ -170,6 +188,32 @@ __device__ __forceinline__ void load_halo(const Dev& d, int s, int ty, int tx, i
     const int nty = ty + dy, ntx = tx + dx;
     int v = HINF;
     if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
+      v = d.hedge[(((size_t)s * d.T + nty * d.TX + ntx) * 4 + (dy < 0 ? 1 : 0)) * 32 + (dx < 0 ? 31 : 0)];
+    hs[hidx(dy < 0 ? -1 : 32, dx < 0 ? -1 : 32)] = v;
+  }
+}
+
+// Halo from the neighbours selected by `sides` (side bits as side_bit: 0 N, 1 S, 2 W, 3 E,
+// 4 NW, 5 NE, 6 SW, 7 SE); INF elsewhere.
+__device__ __forceinline__ void load_halo_sides(const Dev& d, int s, int ty, int tx, int* hs, int t, int sides) {
+  if (t < 128) {
+    const int side = t >> 5, i = t & 31;
+    int nty = ty, ntx = tx, esd, pos, bit;
+    if (side == 0) { nty = ty - 1; esd = 1; pos = hidx(-1, i); bit = 0; }
+    else if (side == 1) { nty = ty + 1; esd = 0; pos = hidx(32, i); bit = 1; }
+    else if (side == 2) { ntx = tx - 1; esd = 3; pos = hidx(i, -1); bit = 2; }
+    else { ntx = tx + 1; esd = 2; pos = hidx(i, 32); bit = 3; }
+    int v = HINF;
+    if (((sides >> bit) & 1) && nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
+      v = d.hedge[(((size_t)s * d.T + nty * d.TX + ntx) * 4 + esd) * 32 + i];
+    hs[pos] = v;
+  } else if (t < 132) {
+    const int c = t - 128;
+    const int dy = (c < 2) ? -1 : 1, dx = (c & 1) ? 1 : -1;
+    const int bit = dy < 0 ? (dx < 0 ? 4 : 5) : (dx < 0 ? 6 : 7);
+    const int nty = ty + dy, ntx = tx + dx;
+    int v = HINF;
+    if (((sides >> bit) & 1) && nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
       v = d.hedge[(((size_t)s * d.T + nty * d.TX + ntx) * 4 + (dy < 0 ? 1 : 0)) * 32 + (dx < 0 ? 31 : 0)];
     hs[hidx(dy < 0 ? -1 : 32, dx < 0 ? -1 : 32)] = v;
   }
@@ -442,24 +486,29 @@ __device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_
   }
 }
 
-// Flow that arrived across the border of receiver pixel (iy, ix) along direction k since
-// the tile last absorbed: sent - got (wrapping uint32 arithmetic: the amount in flight on
-// one arc is below 2^31).  Marks it absorbed.  Sender and receiver each own one counter,
-// so no atomics are needed.
+// Flow that arrived across the tile border since the tile last absorbed, per direction and
+// receiver slot: infl[k][slot] = sent - got (wrapping uint32 arithmetic: the amount in
+// flight on one arc is below 2^31), marking it absorbed.  Sender and receiver each own one
+// counter, so no atomics are needed.  Coalesced: thread i < 16K handles 4
+// consecutive slots of one direction with 16-byte loads.  Block-wide; ends with a barrier.
 template <int K>
-__device__ __forceinline__ int take_inflow(const Dev& d, size_t gt, int k, int iy, int ix) {
-  const int sl = recv_slot(k, iy, ix);
-  const uint32_t snt = __ldcg(SENTp(d, K, gt, k) + sl);
-  uint32_t* g = GOTp(d, K, gt, k) + sl;
-  const uint32_t gv = *g;
-  if (snt == gv) return 0;
-  *g = snt;
-  return (int)(snt - gv);
+__device__ __forceinline__ void gather_inflow(const Dev& d, size_t gt, int* infl) {
+  const int t = threadIdx.x;
+  if (t < 16 * K) {
+    uint4* sp = reinterpret_cast<uint4*>(d.sent + gt * K * 64) + t;
+    uint4* gp = reinterpret_cast<uint4*>(d.got + gt * K * 64) + t;
+    const uint4 sv = __ldcg(sp), gv = *gp;
+    int4 dl;
+    dl.x = (int)(sv.x - gv.x); dl.y = (int)(sv.y - gv.y); dl.z = (int)(sv.z - gv.z); dl.w = (int)(sv.w - gv.w);
+    if (dl.x | dl.y | dl.z | dl.w) *gp = sv;
+    reinterpret_cast<int4*>(infl)[t] = dl;
+  }
+  __syncthreads();
 }
 
-// Absorb inbound border flow into the shared-memory state.
+// Absorb inbound border flow into the shared-memory state (infl: gather_inflow's result).
 template <int K>
-__device__ __forceinline__ void absorb_smem(const Dev& d, size_t gt, int* es, int* rs) {
+__device__ __forceinline__ void absorb_smem(const int* infl, int* es, int* rs) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -469,7 +518,7 @@ __device__ __forceinline__ void absorb_smem(const Dev& d, size_t gt, int* es, in
     for (int k = 0; k < K; ++k) {
       const int wy = iy - DYk(k), wx = ix - DXk(k);
       if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-      const int dl = take_inflow<K>(d, gt, k, iy, ix);
+      const int dl = infl[k * 64 + recv_slot(k, iy, ix)];
       if (dl) {
         es[lp] += dl;
         rs[(k ^ 1) * TPX + lp] += dl;  // residual u -> w grows by the flow w -> u
@@ -711,7 +760,7 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
     d.tmk[gt] = 0;
     if (bad) d.ferr[s] = 1;
   }
-  __syncthreads();
+  // no trailing barrier: the caller alternates `red` between consecutive tiles
 }
 
 // a1 / a1w: one init task = a group of d.initg consecutive tiles of a frame (more tiles per
@@ -723,7 +772,7 @@ template <int K>
 constexpr size_t init_stage_bytes() { return sizeof(int4) * (2 + K) * NTH; }
 
 template <int K>
-__device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, long long (*red)[NTH / 32],
+__device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, long long (*red)[2][NTH / 32],
                                           int4* stage) {
   const int s = (int)(gt0 / d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
   const int n = min(d.initg, d.T - tile0);
@@ -734,8 +783,8 @@ __device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, b
     for (int i = 0; i < n; ++i) {
       const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
       init_load<K>(d, P, ty, tx, false, a, b, c);
-      if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, red);
-      else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, red);
+      if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, red[i & 1]);
+      else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, red[i & 1]);
     }
     return;
   }
@@ -744,8 +793,8 @@ __device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, b
   for (int i = 0; i < n; ++i) {
     init_from_stage<K>(stage, a, b, c);
     if (i + 1 < n) init_prefetch<K>(d, P, (tile0 + i + 1) / d.TX, (tile0 + i + 1) % d.TX, stage);
-    if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, red);
-    else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, red);
+    if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, red[i & 1]);
+    else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, red[i & 1]);
   }
 }
 

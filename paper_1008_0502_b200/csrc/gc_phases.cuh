@@ -109,10 +109,11 @@ __device__ __forceinline__ int border_bits(int iy, int ix) {
 // Flow still in flight into the tile: materialise e, r pixel at a time (from the stored
 // state or the caps), absorb the inbound border flow, store; returns the new fl words.
 template <int K>
-__device__ __forceinline__ void absorb_pixelwise(const Dev& d, const IO& io, size_t gt, int (&fl)[4]) {
+__device__ __forceinline__ void absorb_pixelwise(const Dev& d, const IO& io, size_t gt, int (&fl)[4], int* infl) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  gather_inflow<K>(d, gt, infl);
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j, lp = iy * TS + ix;
@@ -123,7 +124,7 @@ __device__ __forceinline__ void absorb_pixelwise(const Dev& d, const IO& io, siz
       for (int k = 0; k < K; ++k) {
         const int wy = iy - DYk(k), wx = ix - DXk(k);
         if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-        const int dl = take_inflow<K>(d, gt, k, iy, ix);
+        const int dl = infl[k * 64 + recv_slot(k, iy, ix)];
         if (dl) { e += dl; r[k ^ 1] += dl; }
       }
     }
@@ -155,18 +156,30 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   if (t == 0) {
     bc[0] = __ldcg(d.recv1 + gt);
     bc[2] = __ldcg(d.tuni + gt);
+    bc[6] = __ldcg(d.fbe + s);
+    bc[7] = 0;
   }
   __syncthreads();
   const int rcv = bc[0];
   if (bc[2] && !rcv) return;  // untouched uniform sink tile: h = 1, hedge published
   int fl[4];
-  if (rcv) absorb_pixelwise<K>(d, io, gt, fl);
+  if (rcv) absorb_pixelwise<K>(d, io, gt, fl, hs + 2048);
   else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
   }
+  // halo: the border heights of the neighbours whose seed was skipped in this relabel
+  // (uniform sink tiles: final), INF elsewhere -- the BFS phase brings in the others
+  const int tile_ = (int)(gt - (size_t)s * d.T);
+  const int ty_ = tile_ / d.TX, tx_ = tile_ - ty_ * d.TX;
+  if (t < 8) {
+    const long long n = side_tile(d, gt, t);
+    const int ok = n >= 0 && !(t >= 4 && K == 4) && __ldcg(d.tsk + n) == bc[6];
+    if (ok) atomicOr(&bc[7], 1 << t);
+  }
   for (int i = t; i < HS * HS; i += NTH) hs[i] = HINF;
   __syncthreads();
+  load_halo_sides(d, s, ty_, tx_, hs, t, bc[7]);
   int h[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -198,19 +211,11 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   fix = __syncthreads_and(fix);
   uni = __syncthreads_and(uni);
   if ((t & 31) == 0 && bits) atomicOr(&bc[1], bits);
-  // a uniform sink neighbour (seed skipped) cannot flag this tile: flag it here
-  int self = 0;
-  if (t < 8 && !(t >= 4 && K == 4)) {
-    const long long n = side_tile(d, gt, t);
-    self = n >= 0 && __ldcg(d.tuni + n);
-  }
-  self = __syncthreads_or(self);
   if (t == 0) {
     d.tact[gt] = act;
     d.tminh[gt] = bc[5];
     d.tfix[gt] = fix;
     d.tuni[gt] = uni;
-    if (self && !fix) d.flag[gt] = 1;
   }
   flag_sides(d, gt, bc[1], K);
 }
@@ -354,7 +359,7 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   __syncthreads();
   if (bc[2]) return;  // range error (mask stays 0, F = -1) or the attempt already failed
   int fl[4];
-  if (bc[0]) absorb_pixelwise<K>(d, io, gt, fl);
+  if (bc[0]) absorb_pixelwise<K>(d, io, gt, fl, reinterpret_cast<int*>(ms) + 2048);
   else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
@@ -561,7 +566,9 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
   }
   if (rcv) {
     if (t == 0) d.recv1[gt] = 0;
-    absorb_smem<K>(d, gt, es, rs);
+    gather_inflow<K>(d, gt, &oacc[0][0]);  // oacc is free until the rounds: borrow it
+    absorb_smem<K>(&oacc[0][0], es, rs);
+    __syncthreads();
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -670,26 +677,20 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     tile_store_smem<K>(d, gt, es, rs);
     store_hedge(d, gt, h, t);
   }
-  // border pushes: add to the receivers' cumulative counters (unique writer per slot)
+  // border pushes: add to the receivers' cumulative counters (unique writer per slot),
+  // one slot per thread (coalesced per direction)
   int sides = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j;
-    if (!on_border(iy, ix)) continue;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (!crosses(k, iy, ix)) continue;
-      const int y2 = iy + DYk(k), x2 = ix + DXk(k);
-      const int sl = recv_slot(k, y2 & 31, x2 & 31);
-      const int dl = oacc[k][sl];
-      if (dl) {
-        const int dy = y2 < 0 ? -1 : (y2 > 31 ? 1 : 0), dx = x2 < 0 ? -1 : (x2 > 31 ? 1 : 0);
-        const size_t rgt = (size_t)s * d.T + (ty + dy) * d.TX + (tx + dx);
-        uint32_t* p = SENTp(d, K, rgt, k) + sl;
-        *p = *p + (uint32_t)dl;
-        d.recv1[rgt] = 1;
-        sides |= 1 << side_bit(dy, dx);
-      }
+  for (int i = t; i < K * 64; i += NTH) {
+    const int dl = (&oacc[0][0])[i];
+    if (dl) {
+      const int k = i >> 6, sl = i & 63;
+      int dy, dx;
+      recv_tile_offset(k, sl, dy, dx);
+      const size_t rgt = (size_t)s * d.T + (ty + dy) * d.TX + (tx + dx);
+      uint32_t* p = SENTp(d, K, rgt, k) + sl;
+      *p = __ldcg(p) + (uint32_t)dl;
+      d.recv1[rgt] = 1;
+      sides |= 1 << side_bit(dy, dx);
     }
   }
   act = __syncthreads_or(act);
@@ -852,7 +853,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.fph[s] = 0; d.fvis[s] = 0; d.fprog[s] = 0;
           st[0] = st[1] = st[2] = st[3] = 0;
           d.frel[s] = 0; d.sumct[s] = 0; d.sumneg[s] = 0;
-          d.cep[s] = 0; d.cfail[s] = 0; d.fdrain[s] = 0;
+          d.cep[s] = 0; d.cfail[s] = 0; d.fdrain[s] = 0; d.fbe[s] = 0;
           nm = M_INIT;
           kind = SET_INITG;
         } else {
@@ -860,6 +861,8 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           kind = SET_NONE;
         }
       }
+      if (nm == M_SEED) d.fbe[s] += 1;  // a new global relabel
+      bc[3] = d.fbe[s];
       d.fmode[s] = nm;
       bc[4] = kind;
       bc[2] = nm;
@@ -878,6 +881,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         else if (kind == SET_INITG) want = (i % d.initg) == 0;  // one init task per tile group
         else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1
           want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));
+          if (!want) d.tsk[gt] = bc[3];
           d.flag[gt] = 0;
         } else if (kind == SET_CSEED) {  // untouched uniform sink tiles are never in the closure
           want = !(__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt) && !__ldcg(d.recv1 + gt));
@@ -928,7 +932,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
   extern __shared__ int smem[];
   __shared__ int bc[8];
   __shared__ long long red[NTH / 32];
-  __shared__ long long red2[2][NTH / 32];
+  __shared__ long long red2[2][2][NTH / 32];
   __shared__ uint32_t task_s;
   __shared__ uint32_t next_s;  // continuation kept by this CTA (QEMPTY: none)
   if (threadIdx.x == 0) next_s = QEMPTY;

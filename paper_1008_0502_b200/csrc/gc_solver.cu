@@ -66,10 +66,10 @@ size_t frame_bytes(int K, size_t T) {
   b += T * 128 * 4;               // hedge
   b += 2 * T * K * 64 * 4;        // sent, got
   b += T * K * 64;                // reach
-  b += T * 8 + 11 * T * 4;        // neg0 + tile flags
+  b += T * 8 + 12 * T * 4;        // neg0 + tile flags
   b += T * TPX;                   // m
   b += 2 * T * 4 * 2;             // queue (capacity >= 2 x tiles in flight)
-  b += 4 * 16 + 8 * 4;            // frame words
+  b += 4 * 24 + 8 * 4;            // frame words
   return b + 16 * 256;            // alignment slack
 }
 
@@ -94,7 +94,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
   // per-frame words and the queue counters first: contiguous, so one memset clears them
-  char* fw = take((size_t)nslot * (4 * 16 + 8 * 4) + 64 * 4);  // 11 int + 3 u64 per slot
+  char* fw = take((size_t)nslot * (4 * 24 + 8 * 4) + 64 * 4);  // <= 24 int + 4 u64 per slot
   int32_t* w = (int32_t*)fw;
   d.fmode = w; w += nslot;
   d.sfr = w; w += nslot;
@@ -107,6 +107,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.cfail = w; w += nslot;
   d.fdrain = w; w += nslot;
   d.fhmin = w; w += nslot;
+  d.fbe = w; w += nslot;
   d.fstat = w; w += 4 * nslot;
   d.gctr = w; w += 4;
   d.done = w; w += 4;
@@ -141,6 +142,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.tfix = (int32_t*)take(ns * 4);
   d.tph = (int32_t*)take(ns * 4);
   d.tminh = (int32_t*)take(ns * 4);
+  d.tsk = (int32_t*)take(ns * 4);
   d.tcs = (int32_t*)take(ns * 4);
   d.tmk = (int32_t*)take(ns * 4);
   d.m = (uint8_t*)take(ns * TPX);
