@@ -601,15 +601,20 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
       int ee = es[lp];
       const int hv = hc[hidx(iy, ix)];
       if (ee > 0 && hv < HINF) {
+        int rk[K], hu[K];  // all loads first (independent), then the sequential pushes
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          rk[k] = rs[k * TPX + lp];
+          hu[k] = hc[hidx(iy + DYk(k), ix + DXk(k))];
+        }
         int sent = 0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const int rk = rs[k * TPX + lp];
-          if (ee > 0 && rk > 0 && hc[hidx(iy + DYk(k), ix + DXk(k))] == hv - 1) {
-            const int dl = min(ee, rk);
+          if (ee > 0 && rk[k] > 0 && hu[k] == hv - 1) {
+            const int dl = min(ee, rk[k]);
             ee -= dl;
             sent += dl;
-            rs[k * TPX + lp] = rk - dl;
+            rs[k * TPX + lp] = rk[k] - dl;
             if (crosses(k, iy, ix)) {
               oacc[k][recv_slot(k, (iy + DYk(k)) & 31, (ix + DXk(k)) & 31)] += dl;
               prog = 1;
@@ -635,12 +640,17 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
       if (es[lp] > 0 && hv < HINF) {
         int mn = HINF;
         bool adm = false;
+        int rk[K], hu[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if (rs[k * TPX + lp] > 0) {
-            const int hu = hc[hidx(iy + DYk(k), ix + DXk(k))];
-            adm |= (hu == hv - 1);
-            mn = min(mn, hu);
+          rk[k] = rs[k * TPX + lp];
+          hu[k] = hc[hidx(iy + DYk(k), ix + DXk(k))];
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (rk[k] > 0) {
+            adm |= (hu[k] == hv - 1);
+            mn = min(mn, hu[k]);
           }
         }
         if (!adm) {
