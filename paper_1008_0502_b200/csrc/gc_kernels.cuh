@@ -430,128 +430,6 @@ __device__ __forceinline__ void px_er(const Dev& d, const IO& io, size_t gt, int
 
 // ---- shared-memory tile state (push kernel): es[TPX], rs[K][TPX]; pixel-at-a-time so
 // no register arrays stay live.
-template <int K>
-__device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_t gt, int* es, int* rs) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  if (d.mat[gt]) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int lp = (iy0 + 8 * j) * TS + ix;
-      es[lp] = d.e[gt * TPX + lp];
-#pragma unroll
-      for (int k = 0; k < K; ++k) rs[k * TPX + lp] = Rp(d, K, gt, k)[lp];
-    }
-    return;
-  }
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const int H = d.H, W = d.W;
-  const size_t plane = (size_t)H * W;
-  const size_t f = (size_t)d.sfr[s];
-  const int32_t* cs = io.cs + f * plane;
-  const int32_t* ct = io.ct + f * plane;
-  const int32_t* nb = io.nb + f * plane * K;
-  const int32_t* wf = io.wf ? io.wf + f * plane * (K / 2) : nullptr;
-#pragma unroll 1
-  for (int j = 0; j < 4; ++j) {
-    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix, lp = (iy0 + 8 * j) * TS + ix;
-    int ev = 0;
-    const bool in = y < H && x < W;
-    const size_t o = (size_t)y * W + x;
-    if (in) ev = __ldg(cs + o) - __ldg(ct + o);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int y2 = y + DYk(k), x2 = x + DXk(k);
-      int rk = 0;
-      if (in && y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) {
-        const int c = __ldg(nb + k * plane + o);
-        rk = c;
-        if (wf) {  // a1w: identical clamp to tile_from_caps / tile_init
-          const size_t oq = (size_t)y2 * W + x2;
-          const int cq = __ldg(nb + (k ^ 1) * plane + oq);
-          if ((k & 1) == 0) {
-            const int fv = max(-cq, min(c, __ldg(wf + (k >> 1) * plane + o)));
-            rk = c - fv;
-            ev -= fv;
-          } else {
-            const int fv = max(-c, min(cq, __ldg(wf + ((k ^ 1) >> 1) * plane + oq)));
-            rk = c + fv;
-            ev += fv;
-          }
-        }
-      }
-      rs[k * TPX + lp] = rk;
-    }
-    es[lp] = ev;
-  }
-}
-
-// Flow that arrived across the tile border since the tile last absorbed, per direction and
-// receiver slot: infl[k][slot] = sent - got (wrapping uint32 arithmetic: the amount in
-// flight on one arc is below 2^31), marking it absorbed.  Sender and receiver each own one
-// counter, so no atomics are needed (DESIGN.md §3).  Coalesced: thread i < 16K handles 4
-// consecutive slots of one direction with 16-byte loads.  Block-wide; ends with a barrier.
-template <int K>
-__device__ __forceinline__ void gather_inflow(const Dev& d, size_t gt, int* infl) {
-  const int t = threadIdx.x;
-  if (t < 16 * K) {
-    uint4* sp = reinterpret_cast<uint4*>(d.sent + gt * K * 64) + t;
-    uint4* gp = reinterpret_cast<uint4*>(d.got + gt * K * 64) + t;
-    const uint4 sv = __ldcg(sp), gv = *gp;
-    int4 dl;
-    dl.x = (int)(sv.x - gv.x); dl.y = (int)(sv.y - gv.y); dl.z = (int)(sv.z - gv.z); dl.w = (int)(sv.w - gv.w);
-    if (dl.x | dl.y | dl.z | dl.w) *gp = sv;
-    reinterpret_cast<int4*>(infl)[t] = dl;
-  }
-  __syncthreads();
-}
-
-// Absorb inbound border flow into the shared-memory state (infl: gather_inflow's result).
-template <int K>
-__device__ __forceinline__ void absorb_smem(const int* infl, int* es, int* rs) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int iy = iy0 + 8 * j, lp = iy * TS + ix;
-    if (!on_border(iy, ix)) continue;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int wy = iy - DYk(k), wx = ix - DXk(k);
-      if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
-      const int dl = infl[k * 64 + recv_slot(k, iy, ix)];
-      if (dl) {
-        es[lp] += dl;
-        rs[(k ^ 1) * TPX + lp] += dl;  // residual u -> w grows by the flow w -> u
-      }
-    }
-  }
-}
-
-template <int K>
-__device__ __forceinline__ void tile_store_smem(const Dev& d, size_t gt, const int* es, const int* rs) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int lp = (iy0 + 8 * j) * TS + ix;
-    const int ev = es[lp];
-    d.e[gt * TPX + lp] = ev;
-    int f = (ev > 0 ? FL_POS : 0) | (ev < 0 ? FL_NEG : 0);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int rk = rs[k * TPX + lp];
-      Rp(d, K, gt, k)[lp] = rk;
-      f |= (rk > 0) << k;
-    }
-    d.fl[gt * TPX + lp] = (uint16_t)f;
-  }
-}
-
-// ------------------------------------------------------------------------------ a1
-// Init: a streaming pass over the caps.  Computes e and r in registers (the tile stays
-// un-materialised -- e, r are recomputed if a push ever touches it) and writes only the
-// 2-byte fl word per pixel, the frame's sum c(v,t), the tile's sum max(0,-e) and the
-// range flag.  Thread t owns 4 consecutive pixels of row t/8 (int4 loads when the caller's
-// rows are 16-byte aligned).
 // Caller-layout pointers of the frame a slot holds.
 struct FramePtrs {
   size_t fr;  // batch frame index
@@ -603,6 +481,161 @@ __device__ __forceinline__ void init_load(const Dev& d, const FramePtrs& P, int 
   }
 }
 
+// e, r of a tile into shared memory (es[TPX], rs[K][TPX]): from the materialised state, else
+// recomputed from the caps (+ clamped warm flows).  16-byte accesses, thread t owning the 4
+// consecutive pixels 4t..4t+3, whenever the layout allows.  Block-wide; ends with a barrier.
+template <int K>
+__device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_t gt, int* es, int* rs, bool vec) {
+  const int t = threadIdx.x;
+  if (d.mat[gt]) {
+    reinterpret_cast<int4*>(es)[t] = reinterpret_cast<const int4*>(d.e + gt * TPX)[t];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      reinterpret_cast<int4*>(rs + k * TPX)[t] = reinterpret_cast<const int4*>(Rp(d, K, gt, k))[t];
+    __syncthreads();
+    return;
+  }
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  const int H = d.H, W = d.W;
+  const int ix = t & 31, iy0 = t >> 5;
+  if (vec && !io.wf) {  // cold, aligned rows: the init pass's loads (row t/8, columns 4(t%8)..+3)
+    const FramePtrs P = frame_ptrs(d, io, s, K);
+    int a[4], b[4], c[K][4];
+    init_load<K>(d, P, ty, tx, true, a, b, c);
+    const int y = ty * TS + (t >> 3), x0 = tx * TS + (t & 7) * 4;
+    const bool inner = ty > 0 && tx > 0 && (ty + 1) * TS < H && (tx + 1) * TS < W;
+    int ev[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int x = x0 + i;
+      const bool in = y < H && x < W;
+      int vm = in ? 0xff : 0;
+      if (in && !inner) {
+        vm = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          vm |= ((unsigned)(y + DYk(k)) < (unsigned)H && (unsigned)(x + DXk(k)) < (unsigned)W) << k;
+      }
+      ev[i] = in ? a[i] - b[i] : 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) c[k][i] = ((vm >> k) & 1) ? c[k][i] : 0;
+    }
+    reinterpret_cast<int4*>(es)[t] = make_int4(ev[0], ev[1], ev[2], ev[3]);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      reinterpret_cast<int4*>(rs + k * TPX)[t] = make_int4(c[k][0], c[k][1], c[k][2], c[k][3]);
+    __syncthreads();
+    return;
+  }
+  const size_t plane = (size_t)H * W;
+  const size_t f = (size_t)d.sfr[s];
+  const int32_t* cs = io.cs + f * plane;
+  const int32_t* ct = io.ct + f * plane;
+  const int32_t* nb = io.nb + f * plane * K;
+  const int32_t* wf = io.wf ? io.wf + f * plane * (K / 2) : nullptr;
+#pragma unroll 1
+  for (int j = 0; j < 4; ++j) {
+    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix, lp = (iy0 + 8 * j) * TS + ix;
+    int ev = 0;
+    const bool in = y < H && x < W;
+    const size_t o = (size_t)y * W + x;
+    if (in) ev = __ldg(cs + o) - __ldg(ct + o);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int y2 = y + DYk(k), x2 = x + DXk(k);
+      int rk = 0;
+      if (in && y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) {
+        const int c = __ldg(nb + k * plane + o);
+        rk = c;
+        if (wf) {  // a1w: identical clamp to tile_from_caps / tile_init
+          const size_t oq = (size_t)y2 * W + x2;
+          const int cq = __ldg(nb + (k ^ 1) * plane + oq);
+          if ((k & 1) == 0) {
+            const int fv = max(-cq, min(c, __ldg(wf + (k >> 1) * plane + o)));
+            rk = c - fv;
+            ev -= fv;
+          } else {
+            const int fv = max(-c, min(cq, __ldg(wf + ((k ^ 1) >> 1) * plane + oq)));
+            rk = c + fv;
+            ev += fv;
+          }
+        }
+      }
+      rs[k * TPX + lp] = rk;
+    }
+    es[lp] = ev;
+  }
+  __syncthreads();
+}
+
+// Flow that arrived across the tile border since the tile last absorbed, per direction and
+// receiver slot: infl[k][slot] = sent - got (wrapping uint32 arithmetic: the amount in
+// flight on one arc is below 2^31), marking it absorbed.  Sender and receiver each own one
+// counter, so no atomics are needed (DESIGN.md §3).  Coalesced: thread i < 16K handles 4
+// consecutive slots of one direction with 16-byte loads.  Block-wide; ends with a barrier.
+template <int K>
+__device__ __forceinline__ void gather_inflow(const Dev& d, size_t gt, int* infl) {
+  const int t = threadIdx.x;
+  if (t < 16 * K) {
+    uint4* sp = reinterpret_cast<uint4*>(d.sent + gt * K * 64) + t;
+    uint4* gp = reinterpret_cast<uint4*>(d.got + gt * K * 64) + t;
+    const uint4 sv = __ldcg(sp), gv = *gp;
+    int4 dl;
+    dl.x = (int)(sv.x - gv.x); dl.y = (int)(sv.y - gv.y); dl.z = (int)(sv.z - gv.z); dl.w = (int)(sv.w - gv.w);
+    if (dl.x | dl.y | dl.z | dl.w) *gp = sv;
+    reinterpret_cast<int4*>(infl)[t] = dl;
+  }
+  __syncthreads();
+}
+
+// Absorb inbound border flow into the shared-memory state (infl: gather_inflow's result).
+template <int K>
+__device__ __forceinline__ void absorb_smem(const int* infl, int* es, int* rs) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int iy = iy0 + 8 * j, lp = iy * TS + ix;
+    if (!on_border(iy, ix)) continue;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int wy = iy - DYk(k), wx = ix - DXk(k);
+      if ((unsigned)wy < 32u && (unsigned)wx < 32u) continue;
+      const int dl = infl[k * 64 + recv_slot(k, iy, ix)];
+      if (dl) {
+        es[lp] += dl;
+        rs[(k ^ 1) * TPX + lp] += dl;  // residual u -> w grows by the flow w -> u
+      }
+    }
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void tile_store_smem(const Dev& d, size_t gt, const int* es, const int* rs) {
+  const int t = threadIdx.x;  // pixels 4t..4t+3, 16-byte accesses
+  const int4 ev = reinterpret_cast<const int4*>(es)[t];
+  reinterpret_cast<int4*>(d.e + gt * TPX)[t] = ev;
+  int f0 = (ev.x > 0 ? FL_POS : 0) | (ev.x < 0 ? FL_NEG : 0);
+  int f1 = (ev.y > 0 ? FL_POS : 0) | (ev.y < 0 ? FL_NEG : 0);
+  int f2 = (ev.z > 0 ? FL_POS : 0) | (ev.z < 0 ? FL_NEG : 0);
+  int f3 = (ev.w > 0 ? FL_POS : 0) | (ev.w < 0 ? FL_NEG : 0);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int4 rk = reinterpret_cast<const int4*>(rs + k * TPX)[t];
+    reinterpret_cast<int4*>(Rp(d, K, gt, k))[t] = rk;
+    f0 |= (rk.x > 0) << k; f1 |= (rk.y > 0) << k; f2 |= (rk.z > 0) << k; f3 |= (rk.w > 0) << k;
+  }
+  ushort4 w;
+  w.x = (unsigned short)f0; w.y = (unsigned short)f1; w.z = (unsigned short)f2; w.w = (unsigned short)f3;
+  reinterpret_cast<ushort4*>(d.fl + gt * TPX)[t] = w;
+}
+
+// ------------------------------------------------------------------------------ a1
+// Init: a streaming pass over the caps.  Computes e and r in registers (the tile stays
+// un-materialised -- e, r are recomputed if a push ever touches it) and writes only the
+// 2-byte fl word per pixel, the frame's sum c(v,t), the tile's sum max(0,-e) and the
+// range flag.  Thread t owns 4 consecutive pixels of row t/8 (int4 loads when the caller's
+// rows are 16-byte aligned).
 // Init pass, asynchronous variant (rows 16-byte aligned): each thread copies its 16-byte
 // chunks of the 2 + K planes into its own slots of shared memory with cp.async (zero-fill
 // below the frame), so the next tile's caps stream in while this tile is computed.  Only

@@ -557,7 +557,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     return;
   }
   const int rcv = bc[2], uni = bc[4];
-  tile_load_smem<K>(d, io, gt, es, rs);
+  tile_load_smem<K>(d, io, gt, es, rs, c.vec != 0);
   long long neg0 = 0;  // deficit of the tile before the task (flow absorbed = progress)
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
