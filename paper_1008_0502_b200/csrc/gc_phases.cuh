@@ -1025,28 +1025,28 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
     __syncthreads();
     int rem = 0;
     if (reqd) {
+      // concurrently: thread 0 settles the tile's own requests, threads 1..8 request the
+      // neighbours; no requests while a push phase drains (inflow stays flagged in recv1
+      // and is absorbed by the next closure seed / seed)
+      const bool drain = md == M_PUSH && __ldcg(d.fdrain + s);
       if (t == 0) {
-        const bool drain = md == M_PUSH && __ldcg(d.fdrain + s);
         if (drain) {
-          // the phase drains: drop the requests (inflow stays flagged in recv1 and is absorbed
-          // by the next closure seed / seed)
           atomicExch(&d.treq[gt], 0);
-          rem = 0;
         } else {
           const int sub = c0 - (bc[3] ? 1 : 0);  // a push task still active keeps one request
           rem = atomicSub(&d.treq[gt], sub) - sub;
-          if (rem > 0) next_s = qent(md, gt);  // requested meanwhile: run again, here
+          if (rem > 0 && atomicCAS(&next_s, QEMPTY, qent(md, gt)) != QEMPTY)  // run again
+            q_put(d, atomicAdd(d.qtail, 1ULL), qent(md, gt));
         }
-        bc[6] = drain;
-      }
-      __syncthreads();
-      const int bits = bc[6] ? 0 : bc[1];
-      if (t < 8 && ((bits >> t) & 1) && !(t >= 4 && K == 4)) {
-        const long long n = side_tile(d, gt, t);
-        if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) {
-          if (atomicAdd(&d.treq[n], 1) == 0) {
-            atomicAdd(&d.fout[s], 1);
-            if (atomicCAS(&next_s, QEMPTY, qent(md, n)) != QEMPTY) q_put(d, atomicAdd(d.qtail, 1ULL), qent(md, n));
+      } else if (t <= 8 && !drain) {
+        const int b = t - 1;
+        if (((bc[1] >> b) & 1) && !(b >= 4 && K == 4)) {
+          const long long n = side_tile(d, gt, b);
+          if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) {
+            if (atomicAdd(&d.treq[n], 1) == 0) {
+              atomicAdd(&d.fout[s], 1);
+              if (atomicCAS(&next_s, QEMPTY, qent(md, n)) != QEMPTY) q_put(d, atomicAdd(d.qtail, 1ULL), qent(md, n));
+            }
           }
         }
       }
