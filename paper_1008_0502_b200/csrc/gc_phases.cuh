@@ -546,7 +546,9 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     bc[0] = cond || __ldcg(d.fdrain + s);
     if (cond) d.fdrain[s] = 1;  // no more requests in this phase
     bc[1] = 0;
-    bc[2] = __ldcg(d.recv1 + gt);
+    // inbound flow: take the flag (acquire: the senders set it after their counters)
+    bc[2] = bc[0] ? 0 : atomicExch(&d.recv1[gt], 0);
+    fence_gpu();
     bc[3] = 0;
     bc[4] = __ldcg(d.tuni + gt);
     bc[5] = HINF;
@@ -565,7 +567,6 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     neg0 += ev < 0 ? -(long long)ev : 0;
   }
   if (rcv) {
-    if (t == 0) d.recv1[gt] = 0;
     gather_inflow<K>(d, gt, &oacc[0][0]);  // oacc is free until the rounds: borrow it
     absorb_smem<K>(&oacc[0][0], es, rs);
     __syncthreads();
@@ -699,12 +700,13 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
       const size_t rgt = (size_t)s * d.T + (ty + dy) * d.TX + (tx + dx);
       uint32_t* p = SENTp(d, K, rgt, k) + sl;
       *p = __ldcg(p) + (uint32_t)dl;
-      d.recv1[rgt] = 1;
       sides |= 1 << side_bit(dy, dx);
     }
   }
+  fence_gpu();  // the counters are visible before the receivers' recv1 flags (release)
   act = __syncthreads_or(act);
   sides = block_or_bits(sides, bc);
+  if (t < 8 && ((sides >> t) & 1)) d.recv1[side_tile(d, gt, t)] = 1;
   // progress counters: relabels of this phase, tasks, flow absorbed by deficit nodes
   long long absorbed = neg0 - neg1;
 #pragma unroll

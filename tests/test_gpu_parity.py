@@ -258,3 +258,44 @@ def test_two_contexts_interleaved(torch, gc):
     check_against_oracle(*c4, Fa.cpu().numpy(), ma.cpu().numpy())
     check_against_oracle(*c8, Fb.cpu().numpy(), mb.cpu().numpy())
     a.close(); b.close()
+
+
+def cut_torch(torch, cs, ct, nb, mask):
+    """cut(S) of SURVEY.md §8(c), S = mask, written out in plain PyTorch on the device:
+    sum_{v not in S} cs + sum_{v in S} ct + sum over in-grid arcs p -> q, p in S, q not in S."""
+    S = mask.bool()
+    n, K, H, W = nb.shape
+    val = torch.where(S, ct, cs).to(torch.int64).sum(dim=(1, 2))
+    for k in range(K):
+        dy, dx = DY[k], DX[k]
+        y0, y1 = max(0, -dy), H - max(0, dy)
+        x0, x1 = max(0, -dx), W - max(0, dx)
+        p = S[:, y0:y1, x0:x1]
+        q = S[:, y0 + dy:y1 + dy, x0 + dx:x1 + dx]
+        val += (nb[:, k, y0:y1, x0:x1].to(torch.int64) * (p & ~q)).sum(dim=(1, 2))
+    return val
+
+
+def test_c4_batch_flow_is_cut_of_mask(torch, gc):
+    """C4 in the bench's launch configuration (many frames in flight, continuous batching):
+    every frame's F equals the capacity of the cut its mask defines (max-flow = min-cut,
+    checked on all 256 frames without the oracle), masks equal the oracle's on a stride,
+    and a second solve returns the same F and masks (no race leaks into the results)."""
+    n = 256
+    cs, ct, nb = synth.gen_torch("blob", synth.BASE_SEED + 3, 0, n, 1080, 1920, 8)
+    g = solver(gc, 8)
+    F, mask = g.solve(cs, ct, nb)
+    torch.cuda.synchronize()
+    cut = cut_torch(torch, cs, ct, nb, mask)
+    bad = torch.nonzero(cut != F).flatten().tolist()
+    assert not bad, f"F != cut(mask) on frames {bad[:10]}"
+    for _ in range(2):
+        F2, mask2 = g.solve(cs, ct, nb)
+        bad = torch.nonzero(cut_torch(torch, cs, ct, nb, mask2) != F2).flatten().tolist()
+        assert not bad, f"F != cut(mask) on frames {bad[:10]} (repeat solve)"
+        assert torch.equal(F, F2) and torch.equal(mask, mask2)
+    hc, ht, hn = synth.gen_host("blob", synth.BASE_SEED + 3, 0, 3, 1080, 1920, 8)
+    Fo, mo = oracle.solve_batch(hc, ht, hn, "bk")
+    np.testing.assert_array_equal(F[:3].cpu().numpy(), Fo)
+    np.testing.assert_array_equal(mask[:3].cpu().numpy(), mo)
+    del cs, ct, nb
