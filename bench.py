@@ -314,7 +314,7 @@ def main():
                 "launches_per_step": round(nl / args.profile_steps, 2),
                 "share_of_step": 1.0,  # the step is this one persistent kernel (+ a setup kernel)
                 "peak_source": peak_src,
-                "classes": {c: {"tasks": v[2], "cta_ms": round(v[1], 3), "bytes": tile_bytes(c, K) * v[2]}
+                "classes": {c: {"tiles": v[2], "cta_ms": round(v[1], 3), "bytes": tile_bytes(c, K) * v[2]}
                             for c, v in prof.items()}}
     comp = compulsory_bytes_per_px(K) * n * H * W * world * args.steps / (ms_max * 1e-3) / 1e9
 

@@ -118,7 +118,8 @@ long long gc_last_launches(const gc_ctx* ctx);
 void gc_set_profiling(gc_ctx* ctx, int enable);
 /* Fills launches[6] (k_solve launches, the same in every class), ms[6] (CTA time spent in
  * the class, averaged over the CTAs of the persistent grid, so the six add up to the
- * kernel's duration) and tiles[6] (tile tasks of the class), accumulated since the last
+ * kernel's duration) and tiles[6] (32x32 tiles the class processed; an init task covers a
+ * group of tiles), accumulated since the last
  * reset; any pointer may be NULL; resets the counters if reset != 0. */
 void gc_get_profile(gc_ctx* ctx, long long* launches, double* ms, long long* tiles, int reset);
 /* Device time (ms, CUDA events) of the k_solve launches since the last reset (profiling on). */

@@ -1062,7 +1062,9 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
         uint64_t w1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
         atomicAdd(&d.pns[cls], (unsigned long long)(w1 - w0));
-        atomicAdd(&d.ptiles[cls], 1ULL);
+        // tiles processed (an init task covers a group of tiles)
+        const int tl = (int)(gt - (size_t)s * d.T);
+        atomicAdd(&d.ptiles[cls], md == M_INIT ? (unsigned long long)min(d.initg, d.T - tl) : 1ULL);
       }
     }
     __syncthreads();
