@@ -343,6 +343,22 @@ __device__ __forceinline__ int block_or_bits(int bits, int* bc) {
   return bc[1];
 }
 
+// The caller's mask bytes of the tile's in-frame pixels with wr[j] set: 1 iff in the closure.
+// Written during the attempt itself: if it fails, every tile that got closure pixels (tmk)
+// is closure-seeded again in the next attempt, which rewrites all its bytes.
+__device__ __forceinline__ void mask_write(const Dev& d, const IO& io, size_t gt, const int (&mm)[4],
+                                           const int (&wr)[4]) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int ty = tile / d.TX, tx = tile - ty * d.TX;
+  uint8_t* mask = io.mask + (size_t)d.sfr[s] * d.H * d.W;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
+    if (wr[j] && y < d.H && x < d.W) mask[(size_t)y * d.W + x] = (uint8_t)mm[j];
+  }
+}
+
 // ---------------------------------------------------------------- a4: closure seed (one tile)
 // Absorbs flow still in flight, closes {e > 0} inside the tile, writes the tile's m,
 // marks reach across the border (flagging the receivers for the closure phase), checks the
@@ -390,6 +406,10 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   }
   fail = __syncthreads_or(fail);
   any = __syncthreads_or(any);
+  {
+    const int all[4] = {1, 1, 1, 1};
+    mask_write(d, io, gt, mm, all);
+  }
   const int sides = block_or_bits(closure_send<K>(d, gt, mm, os, ep), bc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
@@ -456,9 +476,13 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
   any = __syncthreads_or(any);
   fail = __syncthreads_or(fail);
   if (any || !valid) {
+    int wr[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (nw[j] || !valid) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = mm[j] ? (uint8_t)ep : (uint8_t)0;
+    for (int j = 0; j < 4; ++j) {
+      wr[j] = nw[j] || !valid;
+      if (wr[j]) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = mm[j] ? (uint8_t)ep : (uint8_t)0;
+    }
+    mask_write(d, io, gt, mm, wr);
   }
   if (t == 0) {
     if (!valid) d.tcs[gt] = ep;
@@ -845,14 +869,11 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         } else if (md == M_CSEED) {
           nm = M_CLOS;
           kind = SET_FLAG;
-        } else {
-          nm = M_MASK;
-          kind = SET_MASK;
+        } else {  // certified: the mask is written
           d.cfail[s] = 0;
+          if (io.fstate && !d.ferr[s]) nm = M_EXPORT;
+          else finished = true;
         }
-      } else if (md == M_MASK) {
-        if (io.fstate && !d.ferr[s]) nm = M_EXPORT;
-        else finished = true;
       } else if (md == M_EXPORT) {
         finished = true;
       }
@@ -896,7 +917,8 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           if (!want) d.tsk[gt] = bc[3];
           d.flag[gt] = 0;
         } else if (kind == SET_CSEED) {  // untouched uniform sink tiles are never in the closure
-          want = !(__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt) && !__ldcg(d.recv1 + gt));
+          want = !(__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt) && !__ldcg(d.recv1 + gt)) ||
+                 __ldcg(d.tmk + gt) != 0;  // mask bytes of a failed attempt are rewritten
           d.flag[gt] = 0;
         } else if (kind == SET_MASK) {
           want = __ldcg(d.tmk + gt) == __ldcg(d.cep + s) % 255 + 1;
