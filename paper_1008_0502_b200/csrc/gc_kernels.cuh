@@ -92,6 +92,7 @@ struct Dev {
   int32_t* fdrain;  // [nslot] the running push phase drains (no new requests)
   int32_t* fhmin;   // [nslot] lowest height of an active pixel seen in the running push phase
   int32_t* fbe;     // [nslot] global relabels started (BFS epoch)
+  int32_t* fcap;    // [nslot] height cap of the running push phase (higher pixels are frozen)
   int32_t* fstat;   // [nslot][4] push tasks, global relabels, BFS relax tasks, -
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]

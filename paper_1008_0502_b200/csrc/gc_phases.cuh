@@ -576,13 +576,14 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     bc[3] = 0;
     bc[4] = __ldcg(d.tuni + gt);
     bc[5] = HINF;
+    bc[7] = __ldcg(d.fcap + s);  // pixels higher than this are frozen in this phase
   }
   __syncthreads();
   if (bc[0]) {
     if (d.pdbg && t == 0) atomicAdd(&d.pdbg[4], 1ULL);
     return;
   }
-  const int rcv = bc[2], uni = bc[4];
+  const int rcv = bc[2], uni = bc[4], hcap = bc[7];
   tile_load_smem<K>(d, io, gt, es, rs, c.vec != 0);
   long long neg0 = 0;  // deficit of the tile before the task (flow absorbed = progress)
 #pragma unroll
@@ -625,7 +626,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
       const int iy = iy0 + 8 * j, lp = iy * TS + ix;
       int ee = es[lp];
       const int hv = hc[hidx(iy, ix)];
-      if (ee > 0 && hv < HINF) {
+      if (ee > 0 && hv <= hcap) {
         int rk[K], hu[K];  // all loads first (independent), then the sequential pushes
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -662,7 +663,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
       const int iy = iy0 + 8 * j, lp = iy * TS + ix;
       const int hv = hc[hidx(iy, ix)];
       int h2 = hv;
-      if (es[lp] > 0 && hv < HINF) {
+      if (es[lp] > 0 && hv <= hcap) {
         int mn = HINF;
         bool adm = false;
         int rk[K], hu[K];
@@ -682,7 +683,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
           h2 = (mn >= hmax - 1) ? HINF : mn + 1;
           ++nrel;
         }
-        still |= h2 < HINF;
+        still |= h2 <= hcap;
       }
       hn[hidx(iy, ix)] = h2;
     }
@@ -703,7 +704,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
       const int ev = es[lp];
       h[j] = hb[cb][hidx(iy0 + 8 * j, ix)];
       d.h[gt * TPX + lp] = h[j];
-      act |= (ev > 0) & (h[j] < HINF);
+      act |= (ev > 0) & (h[j] <= hcap);
       if (ev > 0) amin = min(amin, h[j]);
       neg1 += ev < 0 ? -(long long)ev : 0;
     }
@@ -821,7 +822,12 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     nact = __syncthreads_or(nact);
     // push wave: the phase starts on the active tiles nearest the sink; farther ones wait
     // for the next global relabel (most are cut off by then) unless flow reaches them
-    const int hcap = (md == M_BFS && __ldcg(d.cep + s) == 0) ? (bc[6] > HINF - c.wave ? HINF : bc[6] + c.wave) : HINF;
+    // and pixels above the cap do not take part in the phase at all (frozen): in a typical
+    // frame only the excess next to the object boundary has anywhere to go, and the closure
+    // certificate proves the rest trapped.  The cap doubles with every failed attempt.
+    const int cepn = __ldcg(d.cep + s);
+    const long long capw = cepn == 0 ? (long long)c.wave : (long long)max(c.wave, 1) << min(cepn, 20);
+    const int hcap = md == M_BFS ? (int)min((long long)HINF - 1, (long long)bc[6] + capw) : HINF - 1;
     if (t == 0) {
       int nm = md, kind = SET_ALL;
       int* st = d.fstat + s * 4;
@@ -842,6 +848,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.fprog[s] = 0;
           d.fdrain[s] = 0;
           d.fhmin[s] = HINF;
+          d.fcap[s] = hcap;
           d.fph[s] += 1;
         } else {
           nm = M_CSEED;  // termination certificate: the preflow is maximum

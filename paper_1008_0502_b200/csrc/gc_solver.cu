@@ -32,7 +32,8 @@ struct gc_ctx {
   double timeout_s = 300.0;       // wall-clock bound of one k_solve launch
   int vis_mult = 64;              // push tasks per push phase = vis_mult x frame tiles
   int stall = 64;                 // push tasks without progress before a push phase drains
-  int wave = 32;                  // push wave width (heights above the lowest active one)
+  int wave = 0;                   // push cap: heights above the lowest active one + wave freeze
+                                  // (doubled from 1 per failed certificate attempt)
   int selfrun = 0;                // 1: a push tile re-runs itself only after progress
   int grid = 0;                   // k_solve CTAs of the last launch
   std::string err;
@@ -108,6 +109,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.fdrain = w; w += nslot;
   d.fhmin = w; w += nslot;
   d.fbe = w; w += nslot;
+  d.fcap = w; w += nslot;
   d.fstat = w; w += 4 * nslot;
   d.gctr = w; w += 4;
   d.done = w; w += 4;
