@@ -125,7 +125,7 @@ struct IO {
 
 __device__ __forceinline__ size_t NS(const Dev& d) { return (size_t)d.nslot * d.T; }
 __device__ __forceinline__ int32_t* Rp(const Dev& d, int K, size_t gt, int k) {
-  const size_t s = gt / d.T, tile = gt - s * d.T;
+  const size_t s = (unsigned)gt / (unsigned)d.T, tile = gt - s * d.T;
   return d.r + ((s * K + k) * d.T + tile) * TPX;
 }
 __device__ __forceinline__ uint32_t* SENTp(const Dev& d, int K, size_t gt, int k) { return d.sent + (gt * K + k) * 64; }
@@ -324,7 +324,7 @@ __device__ __forceinline__ void get_er(const Dev& d, const IO& io, size_t gt, in
   if (d.mat[gt]) {
     load_er<K>(d, gt, e, r);
   } else {
-    const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+    const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
     const int ty = tile / d.TX, tx = tile - ty * d.TX;
     int bad = 0;
     long long sct = 0;
@@ -395,7 +395,7 @@ __device__ __forceinline__ void px_er(const Dev& d, const IO& io, size_t gt, int
     for (int k = 0; k < K; ++k) r[k] = Rp(d, K, gt, k)[lp];
     return;
   }
-  const int s = (int)(gt / d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T);
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const size_t f = (size_t)d.sfr[s];
@@ -496,7 +496,7 @@ __device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_
     __syncthreads();
     return;
   }
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int H = d.H, W = d.W;
   const int ix = t & 31, iy0 = t >> 5;
@@ -637,51 +637,24 @@ __device__ __forceinline__ void tile_store_smem(const Dev& d, size_t gt, const i
 // 2-byte fl word per pixel, the frame's sum c(v,t), the tile's sum max(0,-e) and the
 // range flag.  Thread t owns 4 consecutive pixels of row t/8 (int4 loads when the caller's
 // rows are 16-byte aligned).
-// Init pass, asynchronous variant (rows 16-byte aligned): each thread copies its 16-byte
-// chunks of the 2 + K planes into its own slots of shared memory with cp.async (zero-fill
-// below the frame), so the next tile's caps stream in while this tile is computed.  Only
-// the issuing thread ever reads its slots back: no barrier is needed between the copy and
-// its use, nor before the slots are refilled.
-template <int K>
-__device__ __forceinline__ void init_prefetch(const Dev& d, const FramePtrs& P, int ty, int tx, int4* stage) {
-  const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
-  const size_t plane = (size_t)d.H * d.W;
-  const int y = ty * TS + iy, x0 = tx * TS + ix0;
-  const bool in = y < d.H && x0 < d.W;  // W % 4 == 0: the whole chunk is in the frame
-  const size_t o0 = in ? (size_t)y * d.W + x0 : 0;
-  const int src = in ? 16 : 0;
-#pragma unroll
-  for (int pl = 0; pl < 2 + K; ++pl) {
-    const int32_t* g = pl == 0 ? P.cs + o0 : (pl == 1 ? P.ct + o0 : P.nb + (size_t)(pl - 2) * plane + o0);
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(stage + pl * NTH + t);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(src) : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-template <int K>
-__device__ __forceinline__ void init_from_stage(const int4* stage, int (&a)[4], int (&b)[4], int (&c)[K][4]) {
-  const int t = threadIdx.x;
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  const int4 va = stage[t], vb = stage[NTH + t];
-  a[0] = va.x; a[1] = va.y; a[2] = va.z; a[3] = va.w;
-  b[0] = vb.x; b[1] = vb.y; b[2] = vb.z; b[3] = vb.w;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const int4 v = stage[(2 + k) * NTH + t];
-    c[k][0] = v.x; c[k][1] = v.y; c[k][2] = v.z; c[k][3] = v.w;
-  }
-}
-
 // Init pass, per tile once the caps are in registers: computes e and r (the tile stays
 // un-materialised -- e, r are recomputed if a push ever touches it) and writes only the
 // 2-byte fl word per pixel, zeroes the caller's mask, flags a uniform sink tile, and adds
 // the tile's sum c(v,t) and sum max(0,-e) to the frame (range flag on bad caps).
+constexpr int INIT_GMAX = 64;  // tiles per init task, at most
+
+// Per-warp partial results of one init tile (summed by the group's finalisation).
+struct InitPart {
+  long long sct[NTH / 32];  // sum c(v,t)
+  long long neg[NTH / 32];  // sum max(0,-e)
+  int fl[NTH / 32];         // bit 0: capacity out of range, bit 1: not a uniform sink tile
+};
+
 template <int K, bool WARM>
 __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_t gt, const FramePtrs& P,
                                                const int (&a)[4], const int (&b)[4], const int (&c)[K][4],
-                                               long long (*red)[NTH / 32]) {
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+                                               InitPart* part) {
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
   const int H = d.H, W = d.W;
@@ -758,28 +731,33 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
     }
   }
   if (t < K * 16) reinterpret_cast<uint32_t*>(d.reach + gt * K * 64)[t] = 0u;
-  bad = __syncthreads_or(bad);
-  uni = __syncthreads_and(uni);
-  if (uni && t < 128) {  // uniform sink tile: publish its border heights now (h = 1 in frame)
-    const int side = t >> 5, j = t & 31;
-    const int py = side == 0 ? 0 : (side == 1 ? 31 : j), px = side == 2 ? 0 : (side == 3 ? 31 : j);
-    d.hedge[gt * 128 + t] = (ty * TS + py < H && tx * TS + px < W) ? 1 : HINF;
+  // warp partials (no barrier: warps run ahead to the next tile's loads); sums with REDUX on
+  // 32-bit halves (per-thread sums are < 2^31, warp sums may not be)
+  const unsigned long long us = (unsigned long long)sct, un = (unsigned long long)neg;
+  const unsigned s_lo = __reduce_add_sync(0xffffffffu, (unsigned)(us & 0xffffu));
+  const unsigned s_hi = __reduce_add_sync(0xffffffffu, (unsigned)(us >> 16));
+  const unsigned n_lo = __reduce_add_sync(0xffffffffu, (unsigned)(un & 0xffffu));
+  const unsigned n_hi = __reduce_add_sync(0xffffffffu, (unsigned)(un >> 16));
+  const int wfl = __reduce_or_sync(0xffffffffu, bad | ((!uni) << 1));
+  if ((t & 31) == 0) {
+    part->sct[t >> 5] = (long long)s_lo + ((long long)s_hi << 16);
+    part->neg[t >> 5] = (long long)n_lo + ((long long)n_hi << 16);
+    part->fl[t >> 5] = wfl;
   }
-  // warp sums with REDUX on 32-bit halves (per-thread sums are < 2^31, warp sums may not be)
-  {
-    const unsigned long long us = (unsigned long long)sct, un = (unsigned long long)neg;
-    const unsigned s_lo = __reduce_add_sync(0xffffffffu, (unsigned)(us & 0xffffu));
-    const unsigned s_hi = __reduce_add_sync(0xffffffffu, (unsigned)(us >> 16));
-    const unsigned n_lo = __reduce_add_sync(0xffffffffu, (unsigned)(un & 0xffffu));
-    const unsigned n_hi = __reduce_add_sync(0xffffffffu, (unsigned)(un >> 16));
-    sct = (long long)s_lo + ((long long)s_hi << 16);
-    neg = (long long)n_lo + ((long long)n_hi << 16);
-  }
-  if ((t & 31) == 0) { red[0][t >> 5] = sct; red[1][t >> 5] = neg; }
-  __syncthreads();
-  if (t == 0) {
+}
+
+// Per-tile results of an init group, after a barrier: tile words, frame sums, range flag,
+// and the border heights of uniform sink tiles (h = 1 in frame).
+__device__ __forceinline__ void init_finalize(const Dev& d, size_t gt0, int n, const InitPart* part, int* uni_s) {
+  const int t = threadIdx.x;
+  const int s = (int)((unsigned)gt0 / (unsigned)d.T);
+  if (t < n) {
+    const size_t gt = gt0 + t;
     long long sa = 0, sb = 0;
-    for (int i = 0; i < NTH / 32; ++i) { sa += red[0][i]; sb += red[1][i]; }
+    int f = 0;
+#pragma unroll
+    for (int w = 0; w < NTH / 32; ++w) { sa += part[t].sct[w]; sb += part[t].neg[w]; f |= part[t].fl[w]; }
+    const int uni = !(f & 2);
     if (sa) atomicAdd(&d.sumct[s], (unsigned long long)sa);
     if (sb) atomicAdd(&d.sumneg[s], (unsigned long long)sb);  // corrected by the closure seed if e changes
     d.neg0[gt] = sb;
@@ -792,44 +770,43 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
     d.tph[gt] = -1;
     d.tcs[gt] = 0;
     d.tmk[gt] = 0;
-    if (bad) d.ferr[s] = 1;
+    if (f & 1) d.ferr[s] = 1;
+    uni_s[t] = uni;
   }
-  // no trailing barrier: the caller alternates `red` between consecutive tiles
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (!uni_s[j] || t >= 128) continue;
+    const int tile = (int)(gt0 + j - (size_t)s * d.T);
+    const int ty = tile / d.TX, tx = tile - ty * d.TX;
+    const int side = t >> 5, i = t & 31;
+    const int py = side == 0 ? 0 : (side == 1 ? 31 : i), px = side == 2 ? 0 : (side == 3 ? 31 : i);
+    d.hedge[(gt0 + j) * 128 + t] = (ty * TS + py < d.H && tx * TS + px < d.W) ? 1 : HINF;
+  }
 }
 
 // a1 / a1w: one init task = a group of d.initg consecutive tiles of a frame (more tiles per
-// task on large frames: less per-task overhead; one on small frames: more parallelism);
-// with aligned rows the caps of tile i+1 are copied to shared memory (cp.async) while tile
-// i is computed.
+// task on large frames: less per-task overhead; one on small frames: more parallelism).
+// No barrier inside the group: each warp streams its rows of tile after tile (16-byte loads
+// straight to registers) and leaves per-warp partials; one barrier and a finalisation at
+// the end publish the per-tile results.
 
 template <int K>
-constexpr size_t init_stage_bytes() { return sizeof(int4) * (2 + K) * NTH; }
-
-template <int K>
-__device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, long long (*red)[2][NTH / 32],
-                                          int4* stage) {
-  const int s = (int)(gt0 / d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
+__device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, int* smem) {
+  const int s = (int)((unsigned)gt0 / (unsigned)d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
   const int n = min(d.initg, d.T - tile0);
   const FramePtrs P = frame_ptrs(d, io, s, K);
+  InitPart* part = reinterpret_cast<InitPart*>(smem);        // [n]
+  int* uni_s = reinterpret_cast<int*>(part + INIT_GMAX);     // [n]
   int a[4], b[4], c[K][4];
-  if (!vec) {
-#pragma unroll 1
-    for (int i = 0; i < n; ++i) {
-      const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
-      init_load<K>(d, P, ty, tx, false, a, b, c);
-      if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, red[i & 1]);
-      else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, red[i & 1]);
-    }
-    return;
-  }
-  init_prefetch<K>(d, P, tile0 / d.TX, tile0 % d.TX, stage);
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
-    init_from_stage<K>(stage, a, b, c);
-    if (i + 1 < n) init_prefetch<K>(d, P, (tile0 + i + 1) / d.TX, (tile0 + i + 1) % d.TX, stage);
-    if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, red[i & 1]);
-    else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, red[i & 1]);
+    const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
+    init_load<K>(d, P, ty, tx, vec, a, b, c);
+    if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, part + i);
+    else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, part + i);
   }
+  __syncthreads();
+  init_finalize(d, gt0, n, part, uni_s);
 }
 
 }  // namespace gcb

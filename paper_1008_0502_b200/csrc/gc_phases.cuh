@@ -72,7 +72,7 @@ __device__ __forceinline__ uint32_t qent(int md, size_t gt) { return ((uint32_t)
 __device__ __forceinline__ long long side_tile(const Dev& d, size_t gt, int b) {
   const int dy = (b == 0 || b == 4 || b == 5) ? -1 : ((b == 1 || b == 6 || b == 7) ? 1 : 0);
   const int dx = (b == 2 || b == 4 || b == 6) ? -1 : ((b == 3 || b == 5 || b == 7) ? 1 : 0);
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX + dy, tx = tile % d.TX + dx;
   if (ty < 0 || ty >= d.TY || tx < 0 || tx >= d.TX) return -1;
   return (long long)s * d.T + ty * d.TX + tx;
@@ -111,7 +111,7 @@ __device__ __forceinline__ int border_bits(int iy, int ix) {
 template <int K>
 __device__ __forceinline__ void absorb_pixelwise(const Dev& d, const IO& io, size_t gt, int (&fl)[4], int* infl) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   gather_inflow<K>(d, gt, infl);
 #pragma unroll 1
@@ -152,7 +152,7 @@ __device__ __forceinline__ void absorb_pixelwise(const Dev& d, const IO& io, siz
 template <int K>
 __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt, int* hs, int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T);
   if (t == 0) {
     bc[0] = __ldcg(d.recv1 + gt);
     bc[2] = __ldcg(d.tuni + gt);
@@ -226,7 +226,7 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
 template <int K>
 __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   if (t == 0) bc[1] = 0;
   int fl[4], h[4], h0[4];
@@ -310,7 +310,7 @@ template <int K>
 __device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os,
                                             int ep) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   int sides = 0;
 #pragma unroll
@@ -349,7 +349,7 @@ __device__ __forceinline__ int block_or_bits(int bits, int* bc) {
 __device__ __forceinline__ void mask_write(const Dev& d, const IO& io, size_t gt, const int (&mm)[4],
                                            const int (&wr)[4]) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   uint8_t* mask = io.mask + (size_t)d.sfr[s] * d.H * d.W;
 #pragma unroll
@@ -367,7 +367,7 @@ template <int K>
 __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
                                            long long* red, int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T);
   if (t == 0) {
     bc[0] = __ldcg(d.recv1 + gt);
     bc[2] = __ldcg(d.ferr + s) || __ldcg(d.cfail + s) > 0;
@@ -436,7 +436,7 @@ template <int K>
 __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
                                             int* bc) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T);
   if (t == 0) {
     bc[1] = 0;
     bc[2] = __ldcg(d.cfail + s) > 0;
@@ -497,7 +497,7 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
 template <int K>
 __device__ __forceinline__ void task_mask(const Dev& d, const IO& io, size_t gt) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int ep = closure_epoch(d, s);
   uint8_t* mask = io.mask + (size_t)d.sfr[s] * d.H * d.W;
@@ -512,7 +512,7 @@ __device__ __forceinline__ void task_mask(const Dev& d, const IO& io, size_t gt)
 // Forward-arc flows f = c - r of this solve (the next frame's warm start).
 template <int K>
 __device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t gt) {
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int H = d.H, W = d.W;
@@ -559,7 +559,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
   int* rs = es + TPX;                                             // residuals [K][TPX]
   int(*oacc)[64] = reinterpret_cast<int(*)[64]>(rs + K * TPX);    // border pushes by slot
   const int hmax = d.hmax;
-  const int s = (int)(gt / d.T), tile = (int)(gt - (size_t)s * d.T);
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   if (t == 0) {
     // phase budget spent or no progress lately: the frame drains to the next global relabel
@@ -973,7 +973,6 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
   extern __shared__ int smem[];
   __shared__ int bc[8];
   __shared__ long long red[NTH / 32];
-  __shared__ long long red2[2][2][NTH / 32];
   __shared__ uint32_t task_s;
   __shared__ uint32_t next_s;  // continuation kept by this CTA (QEMPTY: none)
   if (threadIdx.x == 0) next_s = QEMPTY;
@@ -1014,7 +1013,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
     const uint32_t v = task_s;
     if (v == QEXIT || *(volatile int*)&d.done[1]) break;
     const size_t gt = v & 0x0fffffffu;
-    const int s = (int)(gt / d.T);
+    const int s = (int)((unsigned)gt / (unsigned)d.T);
     const int md = (int)(v >> 28);
     const bool reqd = md == M_BFS || md == M_PUSH || md == M_CLOS;  // request-driven phase
     int c0 = 0;
@@ -1029,7 +1028,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
     __syncthreads();
     int cls = 0;
     switch (md) {
-      case M_INIT: task_init<K>(d, io, gt, c.vec != 0, red2, reinterpret_cast<int4*>(smem)); cls = 0; break;
+      case M_INIT: task_init<K>(d, io, gt, c.vec != 0, smem); cls = 0; break;
       case M_SEED: task_seed<K>(d, io, gt, smem, bc); cls = 1; break;
       case M_BFS:
         task_relax<K>(d, gt, smem, bc);

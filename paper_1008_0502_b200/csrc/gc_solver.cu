@@ -90,7 +90,8 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.TY = (H + TS - 1) / TS; d.TX = (W + TS - 1) / TS; d.T = d.TY * d.TX;
   d.nslot = nslot;
   d.hmax = d.T * TPX + 2;
-  d.initg = d.T / 128 < 1 ? 1 : (d.T / 128 > 16 ? 16 : d.T / 128);
+  d.initg = d.T / 32 < 1 ? 1 : (d.T / 32 > 32 ? 32 : d.T / 32);
+  if (const char* ev = getenv("GC_INITG")) d.initg = atoi(ev) > 0 && atoi(ev) <= INIT_GMAX ? atoi(ev) : d.initg;
   const size_t T = d.T, ns = (size_t)nslot * T, K = c->K;
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
