@@ -110,7 +110,7 @@ struct Dev {
   unsigned long long* pdbg;    // [16] development counters (profiling only)
 };
 
-enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_MASK = 6, M_EXPORT = 7, M_IDLE = 8 };
+enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_EXPORT = 7, M_IDLE = 8 };
 
 struct IO {
   const int32_t* cs;

@@ -12,12 +12,14 @@
 //               neighbour tiles (asynchronous Bellman-Ford over tiles, exact at
 //               quiescence)                                                            (a2)
 //               then: no active node left -> M_CSEED, else -> M_PUSH
-//   M_PUSH   -- active tiles and tiles with inbound flow: push/relabel rounds in shared
-//               memory (a3); a tile that stays active requests itself, border flow
-//               requests the receiver; ends at quiescence or when the phase's relabel /
-//               task budget (Goldberg's global-relabel heuristic) is spent -> M_SEED
-//   M_CSEED  -- all tiles: canonical mask seed, writes the caller's mask                (a4)
-//   M_CLOS   -- mask closure across tile borders until nothing changes                (a4)
+//   M_PUSH   -- active tiles under the phase's height cap and tiles with inbound flow:
+//               push/relabel rounds in shared memory (a3); a tile that stays active
+//               requests itself, border flow requests the receiver; ends at quiescence or
+//               when the phase's budgets are spent -> M_CSEED (certificate attempt)
+//   M_CSEED  -- touched tiles: closure of the excess nodes inside the tile (the canonical
+//               mask and the termination certificate), written to the caller's mask   (a4)
+//   M_CLOS   -- closure across tile borders until nothing changes; reaching a node with
+//               e < 0 fails the attempt (-> M_SEED), else the frame is solved          (a4)
 //   M_EXPORT -- all tiles: forward-arc flows for the caller's warm-start state         (a5)
 //   then the flow value is written and the slot takes the next frame (M_INIT) or idles.
 //
@@ -492,22 +494,6 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
   if (any && !fail) block_or_bits(closure_send<K>(d, gt, nw, os, ep), bc);  // sides to request, in bc[1]
 }
 
-// ---------------------------------------------------------------- a4: mask (one tile)
-// After a certified closure: the caller's mask (zero-filled by init) gets the ones.
-template <int K>
-__device__ __forceinline__ void task_mask(const Dev& d, const IO& io, size_t gt) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  const int ep = closure_epoch(d, s);
-  uint8_t* mask = io.mask + (size_t)d.sfr[s] * d.H * d.W;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
-    if (y < d.H && x < d.W && d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] == ep) mask[(size_t)y * d.W + x] = 1;
-  }
-}
-
 // ---------------------------------------------------------------- a5: export (one tile)
 // Forward-arc flows f = c - r of this solve (the next frame's warm start).
 template <int K>
@@ -780,7 +766,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
 // first task set of a phase: NONE = the slot idles; EMPTY = no task (the next transition
 // follows at once)
 enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_CSEED = 5, SET_EMPTY = 6,
-       SET_MASK = 7, SET_INITG = 8 };
+       SET_INITG = 8 };
 
 __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
   const int f = d.sfr[s];
@@ -927,10 +913,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           want = !(__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt) && !__ldcg(d.recv1 + gt)) ||
                  __ldcg(d.tmk + gt) != 0;  // mask bytes of a failed attempt are rewritten
           d.flag[gt] = 0;
-        } else if (kind == SET_MASK) {
-          want = __ldcg(d.tmk + gt) == __ldcg(d.cep + s) % 255 + 1;
-        }
-        else if (kind == SET_FLAG) {
+        } else if (kind == SET_FLAG) {
           want = __ldcg(d.flag + gt);
           if (want) d.flag[gt] = 0;
           if (md == M_SEED && __ldcg(d.tfix + gt)) want = 0;  // a relax cannot change it
@@ -1044,7 +1027,6 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
         task_crelax<K>(d, io, gt, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, bc);
         cls = 4;
         break;
-      case M_MASK: task_mask<K>(d, io, gt); cls = 4; break;
       default: task_export<K>(d, io, gt); cls = 5; break;
     }
     // release this task's writes, then request the neighbour tiles it changed.  One
