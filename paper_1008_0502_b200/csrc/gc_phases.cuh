@@ -989,9 +989,10 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
       }
       task_s = v;
     }
-    if (t == 0 && (++ntask_local & 15) == 0 &&
-        atomicAdd(d.ntask, 16ULL) + 16 >= (unsigned long long)c.max_tasks)  // watchdog
-      *(volatile int*)&d.done[1] = 1;
+    if (t == 0 && (++ntask_local & 15) == 0) {  // watchdogs: task budget, host stop request
+      if (atomicAdd(d.ntask, 16ULL) + 16 >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
+      if ((ntask_local & 255) == 0 && *d.hostabort) *(volatile int*)&d.done[1] = 1;
+    }
     __syncthreads();
     const uint32_t v = task_s;
     if (v == QEXIT || *(volatile int*)&d.done[1]) break;

@@ -299,3 +299,50 @@ def test_c4_batch_flow_is_cut_of_mask(torch, gc):
     np.testing.assert_array_equal(F[:3].cpu().numpy(), Fo)
     np.testing.assert_array_equal(mask[:3].cpu().numpy(), mo)
     del cs, ct, nb
+
+
+@pytest.mark.parametrize("kind,H,W,K,n,so", [("blob", 240, 320, 4, 300, 1), ("blob", 480, 640, 4, 120, 2),
+                                             ("blob", 1080, 1920, 4, 32, 3)])
+def test_batch_flow_is_cut_of_mask(torch, gc, kind, H, W, K, n, so):
+    """C2 / C3 shapes (and a 4-neighbour 1080p batch): F == cut(mask) on every frame of the
+    batch, identical results on a repeat solve, the oracle on the first frames."""
+    cs, ct, nb = synth.gen_torch(kind, synth.BASE_SEED + so, 0, n, H, W, K)
+    g = solver(gc, K)
+    F, mask = g.solve(cs, ct, nb)
+    torch.cuda.synchronize()
+    bad = torch.nonzero(cut_torch(torch, cs, ct, nb, mask) != F).flatten().tolist()
+    assert not bad, f"F != cut(mask) on frames {bad[:10]}"
+    F2, mask2 = g.solve(cs, ct, nb)
+    assert torch.equal(F, F2) and torch.equal(mask, mask2)
+    m = 2
+    hc, ht, hn = synth.gen_host(kind, synth.BASE_SEED + so, 0, m, H, W, K)
+    Fo, mo = oracle.solve_batch(hc, ht, hn, "bk")
+    np.testing.assert_array_equal(F[:m].cpu().numpy(), Fo)
+    np.testing.assert_array_equal(mask[:m].cpu().numpy(), mo)
+
+
+def test_host_watchdog_stops_the_kernel(torch, gc, monkeypatch):
+    """The host wall-clock bound (GC_TIMEOUT_S) asks the persistent kernel to stop through the
+    mapped host word: an adversarial frame that needs tens of seconds returns GC_ERR_NOCONV
+    with F = -1 after ~0.3 s, and the next solve on a fresh context is correct (the GPU is
+    left usable)."""
+    synth.set_serpentine_params(lane=64, big=1 << 20)
+    try:
+        scs, sct, snb = synth.gen_torch("serpentine", synth.BASE_SEED + 4, 0, 1, 1080, 1920, 4)
+    finally:
+        synth.set_serpentine_params()
+    monkeypatch.setenv("GC_TIMEOUT_S", "0.3")
+    g = gc.GridCut(neighborhood=4, max_h=1080, max_w=1920)
+    monkeypatch.delenv("GC_TIMEOUT_S")
+    import time
+    t0 = time.time()
+    F, m = g.solve(scs, sct, snb, allow=(5,))
+    assert time.time() - t0 < 10
+    assert g.last_status == 5 and int(F[0]) == -1
+    assert "timed out" in gc.gc_last_error(g.ctx)
+    g.close()
+    cs, ct, nb = synth.gen_host("blob", 11, 0, 8, 240, 320, 4)
+    g2 = gc.GridCut(neighborhood=4, max_h=240, max_w=320)
+    F2, m2 = g2.solve(*to_dev(torch, cs, ct, nb))
+    check_against_oracle(cs, ct, nb, F2.cpu().numpy(), m2.cpu().numpy(), "bk", frames=[0, 7])
+    g2.close()
