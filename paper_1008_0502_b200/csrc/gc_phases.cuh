@@ -66,9 +66,13 @@ __device__ __forceinline__ void q_put(const Dev& d, unsigned long long p, uint32
   *slot = v;
 }
 
-// Queue entry: the phase a task belongs to (it cannot change while the task is queued) and
-// the tile.
-__device__ __forceinline__ uint32_t qent(int md, size_t gt) { return ((uint32_t)md << 28) | (uint32_t)gt; }
+// Queue entry: the phase a task belongs to (it cannot change while the task is queued),
+// the number of consecutive tiles it covers (1..16; bulk seed / closure-seed tasks take
+// groups of tiles), and the first tile (< 2^24).
+__device__ __forceinline__ uint32_t qent(int md, size_t gt, int cnt = 1) {
+  return ((uint32_t)md << 28) | ((uint32_t)(cnt - 1) << 24) | (uint32_t)gt;
+}
+constexpr int BULK_G = 8;  // tiles per seed / closure-seed task
 
 // Neighbour tile of gt on side b (0 N, 1 S, 2 W, 3 E, 4 NW, 5 NE, 6 SW, 7 SE); -1 if off-frame.
 __device__ __forceinline__ long long side_tile(const Dev& d, size_t gt, int b) {
@@ -372,10 +376,13 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   const int s = (int)((unsigned)gt / (unsigned)d.T);
   if (t == 0) {
     bc[0] = __ldcg(d.recv1 + gt);
-    bc[2] = __ldcg(d.ferr + s) || __ldcg(d.cfail + s) > 0;
+    // range error (mask stays 0, F = -1), the attempt already failed, or (a tile of the
+    // group outside the task set) an untouched uniform sink tile that never had closure pixels
+    bc[2] = __ldcg(d.ferr + s) || __ldcg(d.cfail + s) > 0 ||
+            (__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt) && !bc[0] && __ldcg(d.tmk + gt) == 0);
   }
   __syncthreads();
-  if (bc[2]) return;  // range error (mask stays 0, F = -1) or the attempt already failed
+  if (bc[2]) return;
   int fl[4];
   if (bc[0]) absorb_pixelwise<K>(d, io, gt, fl, reinterpret_cast<int*>(ms) + 2048);
   else {
@@ -921,6 +928,16 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         else want = __ldcg(d.tact + gt) && __ldcg(d.tminh + gt) <= hcap;
         if (want && (kind == SET_FLAG || kind == SET_TACT)) d.treq[gt] = 1;
       }
+      // seed / closure-seed tasks take groups of BULK_G consecutive tiles (the task skips
+      // the tiles of its group that are not in the set): the group leader enqueues
+      const bool grouped = kind == SET_SEED || kind == SET_CSEED;
+      int gcnt = 1;
+      if (grouped) {
+        const unsigned bal = __ballot_sync(0xffffffffu, want);
+        const int lane = t & 31, lead = lane & ~(BULK_G - 1);
+        want = (lane == lead) && ((bal >> lead) & ((1u << BULK_G) - 1));
+        gcnt = min(BULK_G, d.T - i);
+      }
       if (t == 0) bc[5] = 0;
       __syncthreads();
       int li = want ? atomicAdd(&bc[5], 1) : 0;
@@ -936,7 +953,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       }
       __syncthreads();
       const unsigned long long p0 = ((unsigned long long)(uint32_t)bc[7] << 32) | (uint32_t)bc[6];
-      if (want) q_put(d, p0 + li, qent(bc[2], base_gt + i));
+      if (want) q_put(d, p0 + li, qent(bc[2], base_gt + i, gcnt));
       __syncthreads();
     }
     if (t == 0) {
@@ -996,9 +1013,10 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
     __syncthreads();
     const uint32_t v = task_s;
     if (v == QEXIT || *(volatile int*)&d.done[1]) break;
-    const size_t gt = v & 0x0fffffffu;
+    const size_t gt = v & 0x00ffffffu;
     const int s = (int)((unsigned)gt / (unsigned)d.T);
     const int md = (int)(v >> 28);
+    const int gcnt = (int)((v >> 24) & 15) + 1;
     const bool reqd = md == M_BFS || md == M_PUSH || md == M_CLOS;  // request-driven phase
     int c0 = 0;
     uint64_t w0 = 0;
@@ -1013,7 +1031,13 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
     int cls = 0;
     switch (md) {
       case M_INIT: task_init<K>(d, io, gt, c.vec != 0, smem); cls = 0; break;
-      case M_SEED: task_seed<K>(d, io, gt, smem, bc); cls = 1; break;
+      case M_SEED:
+        for (int j = 0; j < gcnt; ++j) {
+          if (j) __syncthreads();
+          task_seed<K>(d, io, gt + j, smem, bc);
+        }
+        cls = 1;
+        break;
       case M_BFS:
         task_relax<K>(d, gt, smem, bc);
         if (t == 0) atomicAdd(&d.fstat[s * 4 + 2], 1);
@@ -1021,7 +1045,10 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
         break;
       case M_PUSH: task_push<K>(d, io, gt, c, smem, bc, red); cls = 2; break;
       case M_CSEED:
-        task_cseed<K>(d, io, gt, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, red, bc);
+        for (int j = 0; j < gcnt; ++j) {
+          if (j) __syncthreads();
+          task_cseed<K>(d, io, gt + j, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, red, bc);
+        }
         cls = 4;
         break;
       case M_CLOS:
@@ -1075,7 +1102,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
         atomicAdd(&d.pns[cls], (unsigned long long)(w1 - w0));
         // tiles processed (an init task covers a group of tiles)
         const int tl = (int)(gt - (size_t)s * d.T);
-        atomicAdd(&d.ptiles[cls], md == M_INIT ? (unsigned long long)min(d.initg, d.T - tl) : 1ULL);
+        atomicAdd(&d.ptiles[cls], md == M_INIT ? (unsigned long long)min(d.initg, d.T - tl) : (unsigned long long)gcnt);
       }
     }
     __syncthreads();

@@ -218,6 +218,7 @@ int chunk_frames(gc_ctx* c, int H, int W) {
   if (n > want) n = want;
   if (n < 1) n = 1;
   if (c->max_batch > 0 && n > (size_t)c->max_batch) n = c->max_batch;
+  if (n * T >= (1u << 24)) n = ((1u << 24) - 1) / T;  // queue entries hold 24-bit tile ids
   const char* env = getenv("GC_CHUNK");
   if (env && atoi(env) > 0 && (size_t)atoi(env) < n) n = atoi(env);
   return (int)n;
