@@ -93,6 +93,7 @@ struct Dev {
   int32_t* fhmin;   // [nslot] lowest height of an active pixel seen in the running push phase
   int32_t* fbe;     // [nslot] global relabels started (BFS epoch)
   int32_t* fcap;    // [nslot] height cap of the running push phase (higher pixels are frozen)
+  int32_t* fbnd;    // [nslot] distance bound of the running global relabel (HINF: exact)
   int32_t* fstat;   // [nslot][4] push tasks, global relabels, BFS relax tasks, -
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]
@@ -332,11 +333,12 @@ __device__ __forceinline__ void get_er(const Dev& d, const IO& io, size_t gt, in
   }
 }
 
-// Tile-local BFS fixpoint: h(v) = min(h(v), 1 + min{h(v+d_k) : arc k open}) until stable.
+// Tile-local BFS fixpoint: h(v) = min(h(v), 1 + min{h(v+d_k) : arc k open}) until stable,
+// for distances up to `bnd` (a bounded global relabel; HINF: exact distances everywhere).
 // hs holds the halo'd heights (halo fixed); updates are written in place (monotone, so a
 // racing reader sees an old or a new upper bound -- both valid).
 template <int K>
-__device__ __forceinline__ void bfs_fixpoint(volatile int* hs, const int (&fl)[4], int (&h)[4]) {
+__device__ __forceinline__ void bfs_fixpoint(volatile int* hs, const int (&fl)[4], int (&h)[4], int bnd) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   for (;;) {
     int changed = 0;
@@ -348,7 +350,7 @@ __device__ __forceinline__ void bfs_fixpoint(volatile int* hs, const int (&fl)[4
 #pragma unroll
         for (int k = 0; k < K; ++k)
           if ((fl[j] >> k) & 1) mn = min(mn, hs[hidx(iy + DYk(k), ix + DXk(k))]);
-        if (mn < HINF && mn + 1 < h[j]) {
+        if (mn < bnd && mn + 1 < h[j]) {  // distances beyond the relabel's bound stay HINF
           h[j] = mn + 1;
           hs[hidx(iy, ix)] = h[j];
           changed = 1;
@@ -357,31 +359,6 @@ __device__ __forceinline__ void bfs_fixpoint(volatile int* hs, const int (&fl)[4
     }
     if (!__syncthreads_or(changed)) break;
   }
-}
-
-// Seed heights from fl (h = 1 where the node still has residual capacity to t) and relax to
-// the tile-local fixpoint with an INF halo; stores h, hedge; returns "tile has an active node".
-template <int K>
-__device__ __forceinline__ int bfs_seed_tile(const Dev& d, size_t gt, int* hs, const int (&fl)[4]) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  for (int i = t; i < HS * HS; i += NTH) hs[i] = HINF;
-  __syncthreads();
-  int h[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    h[j] = (fl[j] & FL_NEG) ? 1 : HINF;
-    hs[hidx(iy0 + 8 * j, ix)] = h[j];
-  }
-  __syncthreads();
-  bfs_fixpoint<K>(hs, fl, h);
-  int act = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
-    act |= (fl[j] & FL_POS) && h[j] < HINF;
-  }
-  store_hedge(d, gt, h, t);
-  return __syncthreads_or(act);
 }
 
 // One pixel's current e and r: from the materialised state, else recomputed from the caps

@@ -164,6 +164,7 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
     bc[2] = __ldcg(d.tuni + gt);
     bc[6] = __ldcg(d.fbe + s);
     bc[7] = 0;
+    bc[4] = __ldcg(d.fbnd + s);
   }
   __syncthreads();
   const int rcv = bc[0];
@@ -193,7 +194,7 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
     hs[hidx(iy0 + 8 * j, ix)] = h[j];
   }
   __syncthreads();
-  bfs_fixpoint<K>(hs, fl, h);
+  bfs_fixpoint<K>(hs, fl, h, bc[4]);
   int act = 0, fix = 1, uni = 1, bits = 0, mnh = HINF;
   const int tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
@@ -234,7 +235,7 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  if (t == 0) bc[1] = 0;
+  if (t == 0) { bc[1] = 0; bc[4] = __ldcg(d.fbnd + s); }
   int fl[4], h[4], h0[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -245,7 +246,7 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
   }
   load_halo(d, s, ty, tx, hs, t);
   __syncthreads();
-  bfs_fixpoint<K>(hs, fl, h);
+  bfs_fixpoint<K>(hs, fl, h, bc[4]);
   int any = 0, bits = 0, act = 0, fix = 1, mnh = HINF;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -820,7 +821,8 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     // certificate proves the rest trapped.  The cap doubles with every failed attempt.
     const int cepn = __ldcg(d.cep + s);
     const long long capw = cepn == 0 ? (long long)c.wave : (long long)max(c.wave, 1) << min(cepn, 20);
-    const int hcap = md == M_BFS ? (int)min((long long)HINF - 1, (long long)bc[6] + capw) : HINF - 1;
+    const int hcap = md == M_BFS ? (int)min((long long)min(HINF - 1, __ldcg(d.fbnd + s)), (long long)bc[6] + capw)
+                                 : HINF - 1;
     if (t == 0) {
       int nm = md, kind = SET_ALL;
       int* st = d.fstat + s * 4;
@@ -844,9 +846,11 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.fcap[s] = hcap;
           d.fph[s] += 1;
         } else {
-          nm = M_CSEED;  // termination certificate: the preflow is maximum
+          nm = M_CSEED;
           kind = SET_CSEED;
-          d.cfail[s] = -1;  // this closure cannot fail (marker)
+          // an exact relabel without an active node is the termination certificate: the
+          // closure cannot fail (marker); after a bounded one it is an ordinary attempt
+          d.cfail[s] = d.fbnd[s] >= HINF ? -1 : 0;
         }
       } else if (md == M_PUSH) {
         // try to certify at once: the closure of the excess nodes; if it reaches a node with
@@ -894,7 +898,11 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           kind = SET_NONE;
         }
       }
-      if (nm == M_SEED) d.fbe[s] += 1;  // a new global relabel
+      if (nm == M_SEED) {  // a new global relabel, bounded: distances up to 2 + 2^(attempts+1)
+        d.fbe[s] += 1;     // (HINF once that exceeds any distance in the frame)
+        const int ce = d.cep[s];
+        d.fbnd[s] = (ce >= 24 || (2ll << ce) >= d.hmax) ? HINF : 2 + (2 << ce);
+      }
       bc[3] = d.fbe[s];
       d.fmode[s] = nm;
       bc[4] = kind;
