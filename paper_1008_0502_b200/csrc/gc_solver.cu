@@ -215,7 +215,8 @@ int chunk_frames(gc_ctx* c, int H, int W) {
   const size_t T = tiles_of(H, W);
   const size_t fb = frame_bytes(c->K, T);
   size_t n = c->pool_bytes / fb;
-  const size_t want = T >= 40000 / 24 ? 24 : (40000 + T - 1) / T;
+  size_t want = T >= 40000 / 24 ? 24 : (40000 + T - 1) / T;
+  if (const char* ev = getenv("GC_SLOTS")) want = atoi(ev) > 0 ? atoi(ev) : want;  // tuning knob
   if (n > want) n = want;
   if (n < 1) n = 1;
   if (c->max_batch > 0 && n > (size_t)c->max_batch) n = c->max_batch;
