@@ -191,6 +191,94 @@ def run_reference(args, cfg):
     print(json.dumps(out), flush=True)
 
 
+def run_warm(args, cfg):
+    """Sequence mode for C3 (BASELINE.json configs[2]): S sequences of L frames; the frames
+    at time t of all sequences are one batch, warm-started from the flows the batch at t-1
+    exported (Kohli-Torr-style reuse).  The same schedule is also run cold.  One
+    step = the L batches of a sequence set; value = warm throughput."""
+    import torch
+
+    import paper_1008_0502_b200 as gc
+    import synth
+    from paper_1008_0502_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    H, W, K = cfg["H"], cfg["W"], cfg["K"]
+    S, L = args.seqs, args.seq_len
+    seed = synth.BASE_SEED + cfg["seed_off"]
+    t0, _ = shard.frame_range(rank, world, S * L)  # each rank takes its own S sequences
+    cs, ct, nb = synth.gen_torch(cfg["kind"], seed, t0, S * L, H, W, K, device=dev, seq_len=L)
+    # [sequence][time] -> [time][sequence]: the batch of time t is contiguous
+    order = torch.arange(S * L, device=dev).view(S, L).t().reshape(-1)
+    cs, ct, nb = cs[order].contiguous(), ct[order].contiguous(), nb[order].contiguous()
+    g = gc.GridCut(neighborhood=K, max_h=H, max_w=W)
+    flow = torch.empty(S, dtype=torch.int64, device=dev)
+    mask = torch.empty((S, H, W), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def sweep(warm):
+        prev, launches = None, 0
+        Fs = []
+        for t in range(L):
+            sl = slice(t * S, (t + 1) * S)
+            res = g.solve(cs[sl], ct[sl], nb[sl], warm_flow=prev if warm else None, flow_state=warm, out=(flow, mask))
+            if warm:
+                prev = res[2]
+            Fs.append(flow.clone())
+            launches += g.launches()
+        return torch.stack(Fs), launches
+
+    for _ in range(args.warmup):
+        sweep(True)
+        sweep(False)
+    torch.cuda.synchronize()
+
+    def timed(warm):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        launches = 0
+        e0.record(stream)
+        for _ in range(args.steps):
+            F, nl = sweep(warm)
+            launches += nl
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return shard.max_over_ranks(e0.elapsed_time(e1), dev, world), F, launches
+
+    clk = ClockSampler(None)
+    clk.start()
+    time.sleep(0.3)
+    ms_w, Fw, lw = timed(True)
+    ms_c, Fc, _ = timed(False)
+    clocks = clk.stop()
+    assert torch.equal(Fw, Fc), "warm-started flow values differ from cold ones"
+    px = world * S * L * H * W * args.steps
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(px / (ms_w * 1e-3) / 1e6, 1), "unit": "Mpixel/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_w / args.steps, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+               "data": "synthetic (seeded saliency-blob sequences, synth/; generated on device before timing)",
+               "config": {"workload": f"{cfg['workload']}: {S} sequences x {L} frames, frame t warm-started from "
+                                      f"t-1 (batch = the {S} frames of one time step)",
+                          "H": H, "W": W, "K": K, "sequences_per_rank": S, "seq_len": L,
+                          "parallelism": f"sequence-sharded dp{world}"},
+               "fps": round(world * S * L * args.steps / (ms_w * 1e-3), 1),
+               "cold_same_schedule": {"value": round(px / (ms_c * 1e-3) / 1e6, 1), "unit": "Mpixel/s",
+                                      "ms_per_step": round(ms_c / args.steps, 3)},
+               "warm_speedup": round(ms_c / ms_w, 3), "warm_equals_cold": True,
+               "gpu_launches": int(lw), "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,12 +291,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-frames", type=int, default=32)
     ap.add_argument("--profile-steps", type=int, default=1)
+    ap.add_argument("--warm", action="store_true",
+                    help="sequence mode (C3): S sequences x L frames, frame t warm-started from t-1")
+    ap.add_argument("--seqs", type=int, default=8)
+    ap.add_argument("--seq-len", type=int, default=120)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.frames:
         cfg["frames"] = args.frames
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.warm:
+        return run_warm(args, cfg)
 
     import numpy as np
     import torch

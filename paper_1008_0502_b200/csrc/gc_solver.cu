@@ -290,15 +290,19 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   }
   if (!ck(c, cudaGetLastError(), "k_solve launch")) return GC_ERR_CUDA;
   cudaMemcpyAsync(c->hpin, d.gctr, 32, cudaMemcpyDeviceToHost, st);  // gctr[4], done[4]
-  // wait; past the timeout ask the kernel to stop (it polls the mapped word while idle)
+  // wait (spinning for the first 2 ms: small calls are latency-bound, a sleep costs ~60 us);
+  // past the timeout ask the kernel to stop (it polls the mapped word)
   const double t0 = now_s();
   for (;;) {
     const cudaError_t q = cudaStreamQuery(st);
     if (q == cudaSuccess) break;
     if (q != cudaErrorNotReady) { ck(c, q, "k_solve"); return GC_ERR_CUDA; }
-    if (!*c->habort && now_s() - t0 > c->timeout_s) *(volatile int32_t*)c->habort = 1;
-    struct timespec ts = {0, 20000};
-    nanosleep(&ts, nullptr);
+    const double el = now_s() - t0;
+    if (!*c->habort && el > c->timeout_s) *(volatile int32_t*)c->habort = 1;
+    if (el > 2e-3) {
+      struct timespec ts = {0, 20000};
+      nanosleep(&ts, nullptr);
+    }
   }
   const bool aborted = c->hpin[5] != 0 || c->hpin[1] < nframes;
   if (aborted && getenv("GC_DEBUG")) {  // development aid: where did each slot stop?
