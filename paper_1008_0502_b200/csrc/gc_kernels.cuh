@@ -168,6 +168,20 @@ __device__ __forceinline__ void recv_tile_offset(int k, int sl, int& dy, int& dx
   }
 }
 
+// Receiver pixel (in the receiver tile) of slot `sl` of direction k (inverse of recv_slot).
+__device__ __forceinline__ void recv_pixel(int k, int sl, int& uy, int& ux) {
+  switch (k) {
+    case 0: uy = sl; ux = 0; break;
+    case 1: uy = sl; ux = 31; break;
+    case 2: uy = 0; ux = sl; break;
+    case 3: uy = 31; ux = sl; break;
+    case 4: if (sl < 32) { uy = 0; ux = sl; } else { uy = sl - 32; ux = 0; } break;
+    case 5: if (sl < 32) { uy = 31; ux = sl; } else { uy = sl - 32; ux = 31; } break;
+    case 6: if (sl < 32) { uy = 0; ux = sl; } else { uy = sl - 32; ux = 31; } break;
+    default: if (sl < 32) { uy = 31; ux = sl; } else { uy = sl - 32; ux = 0; } break;
+  }
+}
+
 __device__ __forceinline__ int hidx(int iy, int ix) { return (iy + 1) * HS + (ix + 1); }
 __device__ __forceinline__ bool on_border(int iy, int ix) { return iy == 0 || iy == 31 || ix == 0 || ix == 31; }
 

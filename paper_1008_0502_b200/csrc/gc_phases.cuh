@@ -708,24 +708,33 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     store_hedge(d, gt, h, t);
   }
   // border pushes: add to the receivers' cumulative counters (unique writer per slot),
-  // one slot per thread (coalesced per direction)
+  // one slot per thread (coalesced per direction).  The receiver is flagged (recv1: the flow
+  // is absorbed at its next task, seed or closure seed at the latest) and requested only if
+  // a receiving pixel can pass the flow on in this phase: 1 < h <= cap by our halo (a sink
+  // node just absorbs it; a node above the cap is frozen).
   int sides = 0;
   for (int i = t; i < K * 64; i += NTH) {
     const int dl = (&oacc[0][0])[i];
     if (dl) {
       const int k = i >> 6, sl = i & 63;
-      int dy, dx;
+      int dy, dx, uy, ux;
       recv_tile_offset(k, sl, dy, dx);
+      recv_pixel(k, sl, uy, ux);
       const size_t rgt = (size_t)s * d.T + (ty + dy) * d.TX + (tx + dx);
       uint32_t* p = SENTp(d, K, rgt, k) + sl;
       *p = __ldcg(p) + (uint32_t)dl;
-      sides |= 1 << side_bit(dy, dx);
+      const int b = side_bit(dy, dx);
+      const int hu = hb[cb][hidx(uy + 32 * dy, ux + 32 * dx)];
+      sides |= (1 << b) | ((hu > 1 && hu <= hcap) << (8 + b));
     }
   }
   fence_gpu();  // the counters are visible before the receivers' recv1 flags (release)
   act = __syncthreads_or(act);
-  sides = block_or_bits(sides, bc);
+  const int sb2 = block_or_bits(sides, bc);
+  sides = sb2 & 255;
   if (t < 8 && ((sides >> t) & 1)) d.recv1[side_tile(d, gt, t)] = 1;
+  __syncthreads();
+  if (t == 0) bc[1] = (sb2 >> 8) & 255;  // the receivers to request (task completion)
   // progress counters: relabels of this phase, tasks, flow absorbed by deficit nodes
   long long absorbed = neg0 - neg1;
 #pragma unroll
