@@ -761,6 +761,7 @@ __device__ __forceinline__ void init_finalize(const Dev& d, size_t gt0, int n, c
     d.tph[gt] = -1;
     d.tcs[gt] = 0;
     d.tmk[gt] = 0;
+    d.tsk[gt] = 0;  // relabel epochs restart at 1 per frame: a stale stamp would alias
     if (f & 1) d.ferr[s] = 1;
     uni_s[t] = uni;
   }
