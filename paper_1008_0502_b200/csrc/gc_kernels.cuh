@@ -235,6 +235,30 @@ __device__ __forceinline__ void load_halo_sides(const Dev& d, int s, int ty, int
   }
 }
 
+// fl words of the 34x34 halo ring (the neighbours' border pixels; 0 off-frame), hidx layout.
+__device__ __forceinline__ void load_fl_halo(const Dev& d, int s, int ty, int tx, uint16_t* flh, int t) {
+  if (t < 128) {
+    const int side = t >> 5, i = t & 31;
+    int nty = ty, ntx = tx, py, px, pos;
+    if (side == 0) { nty = ty - 1; py = 31; px = i; pos = hidx(-1, i); }
+    else if (side == 1) { nty = ty + 1; py = 0; px = i; pos = hidx(32, i); }
+    else if (side == 2) { ntx = tx - 1; py = i; px = 31; pos = hidx(i, -1); }
+    else { ntx = tx + 1; py = i; px = 0; pos = hidx(i, 32); }
+    uint16_t v = 0;
+    if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
+      v = d.fl[((size_t)s * d.T + nty * d.TX + ntx) * TPX + py * TS + px];
+    flh[pos] = v;
+  } else if (t < 132) {
+    const int c = t - 128;
+    const int dy = (c < 2) ? -1 : 1, dx = (c & 1) ? 1 : -1;
+    const int nty = ty + dy, ntx = tx + dx;
+    uint16_t v = 0;
+    if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
+      v = d.fl[((size_t)s * d.T + nty * d.TX + ntx) * TPX + (dy < 0 ? 31 : 0) * TS + (dx < 0 ? 31 : 0)];
+    flh[hidx(dy < 0 ? -1 : 32, dx < 0 ? -1 : 32)] = v;
+  }
+}
+
 __device__ __forceinline__ void store_hedge(const Dev& d, size_t gt, const int (&h)[4], int t) {
   const int ix = t & 31, iy0 = t >> 5;
   int32_t* he = d.hedge + gt * 128;

@@ -315,7 +315,7 @@ __device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uin
 // (side_bit) of the neighbour tiles that were marked.
 template <int K>
 __device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os,
-                                            int ep) {
+                                            int ep, const uint16_t* flh) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
@@ -329,6 +329,7 @@ __device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (
     for (int k = 0; k < K; ++k) {
       if (!crosses(k, iy, ix) || !((ob >> k) & 1)) continue;
       const int y2 = iy + DYk(k), x2 = ix + DXk(k);
+      if (flh[hidx(y2, x2)] & FL_POS) continue;  // an excess node: in the closure anyway
       const int dy = y2 < 0 ? -1 : (y2 > 31 ? 1 : 0), dx = x2 < 0 ? -1 : (x2 > 31 ? 1 : 0);
       const int rty = ty + dy, rtx = tx + dx;
       if (rty < 0 || rty >= d.TY || rtx < 0 || rtx >= d.TX) continue;
@@ -416,11 +417,21 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   }
   fail = __syncthreads_or(fail);
   any = __syncthreads_or(any);
+  if (d.pdbg) {  // development: closure-seed tiles, tiles entirely in the closure
+    const int full = __syncthreads_and(mm[0] & mm[1] & mm[2] & mm[3]);
+    if (t == 0) { atomicAdd(&d.pdbg[9], 1ULL); if (full) atomicAdd(&d.pdbg[10], 1ULL); }
+  }
   {
     const int all[4] = {1, 1, 1, 1};
     mask_write(d, io, gt, mm, all);
   }
-  const int sides = block_or_bits(closure_send<K>(d, gt, mm, os, ep), bc);
+  uint16_t* flh = reinterpret_cast<uint16_t*>(ms + 12288);  // the neighbours' border fl words
+  {
+    const int tile = (int)(gt - (size_t)s * d.T);
+    load_fl_halo(d, s, tile / d.TX, tile % d.TX, flh, t);
+  }
+  __syncthreads();
+  const int sides = block_or_bits(closure_send<K>(d, gt, mm, os, ep, flh), bc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
   if ((t & 31) == 0) red[t >> 5] = neg;
@@ -485,6 +496,7 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
   }
   any = __syncthreads_or(any);
   fail = __syncthreads_or(fail);
+  if (d.pdbg && t == 0) { atomicAdd(&d.pdbg[11], 1ULL); if (any) atomicAdd(&d.pdbg[12], 1ULL); }
   if (any || !valid) {
     int wr[4];
 #pragma unroll
@@ -499,7 +511,12 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
     if (any) d.tmk[gt] = ep;
     if (fail) atomicAdd(&d.cfail[s], 2);
   }
-  if (any && !fail) block_or_bits(closure_send<K>(d, gt, nw, os, ep), bc);  // sides to request, in bc[1]
+  if (any && !fail) {
+    uint16_t* flh = reinterpret_cast<uint16_t*>(ms + 12288);
+    load_fl_halo(d, s, (int)(gt - (size_t)s * d.T) / d.TX, (int)(gt - (size_t)s * d.T) % d.TX, flh, t);
+    __syncthreads();
+    block_or_bits(closure_send<K>(d, gt, nw, os, ep, flh), bc);  // sides to request, in bc[1]
+  }
 }
 
 // ---------------------------------------------------------------- a5: export (one tile)

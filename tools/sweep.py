@@ -50,7 +50,7 @@ for vals in itertools.product(*[v.split(",") for _, v in knobs]):
                       "hard": hard, "cta_ms": {k: round(v[1], 2) for k, v in prof.items()},
                       "tasks": {k: v[2] for k, v in prof.items()},
                       "push_dbg": dict(zip(["real", "lower", "absorbed", "sent", "drained", "rounds", "act_end",
-                                            "recv", "noprog"], dbg[:9]))}), flush=True)
+                                            "recv", "noprog", "cseed_tiles", "cseed_full", "clos_tasks", "clos_new"], dbg[:13]))}), flush=True)
     g.close()
     del g
     for k in env:
