@@ -20,7 +20,8 @@ __all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "g
            "STATUS", "lib_path"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libgc.so")
+# GC_LIB_PATH: development A/B of two builds of the same library (tools/ab.sh)
+lib_path = os.environ.get("GC_LIB_PATH") or os.path.join(_HERE, "libgc.so")
 CAP_MAX = (1 << 26) - 1
 STATUS = {0: "GC_OK", 1: "GC_ERR_ARG", 2: "GC_ERR_RANGE", 3: "GC_ERR_OOM", 4: "GC_ERR_CUDA", 5: "GC_ERR_NOCONV"}
 PROFILE_CLASSES = ("init", "bfs", "push", "sched", "closure", "export")

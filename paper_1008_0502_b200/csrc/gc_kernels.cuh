@@ -656,7 +656,7 @@ __device__ __forceinline__ void tile_store_smem(const Dev& d, size_t gt, const i
 // un-materialised -- e, r are recomputed if a push ever touches it) and writes only the
 // 2-byte fl word per pixel, zeroes the caller's mask, flags a uniform sink tile, and adds
 // the tile's sum c(v,t) and sum max(0,-e) to the frame (range flag on bad caps).
-constexpr int INIT_GMAX = 64;  // tiles per init task, at most
+constexpr int INIT_GMAX = 32;  // tiles per init task, at most
 
 // Per-warp partial results of one init tile (summed by the group's finalisation).
 struct InitPart {
@@ -806,6 +806,36 @@ __device__ __forceinline__ void init_finalize(const Dev& d, size_t gt0, int n, c
 // straight to registers) and leaves per-warp partials; one barrier and a finalisation at
 // the end publish the per-tile results.
 
+// 16-byte global -> shared copy that bypasses registers (LDGSTS); src_bytes 0 zero-fills.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Prefetch of one tile's caps into this thread's own shared slots pf[j * NTH + t]
+// (j = 0: cs, 1: ct, 2 + k: c_k), the same pixels init_load reads; zero outside the frame.
+template <int K>
+__device__ __forceinline__ void init_prefetch(const Dev& d, const FramePtrs& P, int ty, int tx, int4* pf) {
+  const int t = threadIdx.x;
+  const int y = ty * TS + (t >> 3), x0 = tx * TS + (t & 7) * 4;
+  const bool in = y < d.H && x0 < d.W;  // W % 4 == 0 on this path
+  const size_t plane = (size_t)d.H * d.W;
+  const size_t o0 = in ? (size_t)y * d.W + x0 : 0;
+  const int nbytes = in ? 16 : 0;
+  cp_async16(pf + t, P.cs + o0, nbytes);
+  cp_async16(pf + NTH + t, P.ct + o0, nbytes);
+#pragma unroll
+  for (int k = 0; k < K; ++k) cp_async16(pf + (2 + k) * NTH + t, P.nb + k * plane + o0, nbytes);
+  cp_async_commit();
+}
+
+template <int K>
+constexpr size_t init_smem_bytes() {
+  return INIT_GMAX * sizeof(InitPart) + INIT_GMAX * sizeof(int) + (2 + K) * NTH * 16;
+}
+
 template <int K>
 __device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, int* smem) {
   const int s = (int)((unsigned)gt0 / (unsigned)d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
@@ -814,12 +844,40 @@ __device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, b
   InitPart* part = reinterpret_cast<InitPart*>(smem);        // [n]
   int* uni_s = reinterpret_cast<int*>(part + INIT_GMAX);     // [n]
   int a[4], b[4], c[K][4];
+  if (vec && !P.wf) {
+    // cold frames, aligned rows: tile i + 1's caps stream into shared memory (cp.async,
+    // each thread its own slots, so no barrier) while tile i is computed from registers
+    int4* pf = reinterpret_cast<int4*>(uni_s + INIT_GMAX);  // [(2 + K) * NTH]
+    const int t = threadIdx.x;
+    init_prefetch<K>(d, P, tile0 / d.TX, tile0 % d.TX, pf);
 #pragma unroll 1
-  for (int i = 0; i < n; ++i) {
-    const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
-    init_load<K>(d, P, ty, tx, vec, a, b, c);
-    if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, part + i);
-    else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, part + i);
+    for (int i = 0; i < n; ++i) {
+      cp_async_wait_all();
+      {
+        int4 v = pf[t];
+        a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+        v = pf[NTH + t];
+        b[0] = v.x; b[1] = v.y; b[2] = v.z; b[3] = v.w;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          v = pf[(2 + k) * NTH + t];
+          c[k][0] = v.x; c[k][1] = v.y; c[k][2] = v.z; c[k][3] = v.w;
+        }
+      }
+      if (i + 1 < n) {
+        const int tile = tile0 + i + 1;
+        init_prefetch<K>(d, P, tile / d.TX, tile % d.TX, pf);
+      }
+      tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, part + i);
+    }
+  } else {
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) {
+      const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
+      init_load<K>(d, P, ty, tx, vec, a, b, c);
+      if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, part + i);
+      else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, part + i);
+    }
   }
   __syncthreads();
   init_finalize(d, gt0, n, part, uni_s);

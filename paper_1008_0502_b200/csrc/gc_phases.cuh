@@ -559,6 +559,8 @@ __device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t g
 // relabel restores valid labels and certifies termination.
 template <int K>
 constexpr size_t push_smem_bytes() { return sizeof(int) * (2 * HS * HS + TPX + K * TPX + K * 64); }
+static_assert(init_smem_bytes<4>() <= push_smem_bytes<4>() && init_smem_bytes<8>() <= push_smem_bytes<8>(),
+              "the init pass's prefetch buffer must fit the push tile's shared memory");
 
 // Returns the sides whose tiles received border flow in bc[1] and "still active" in bc[3].
 template <int K>
@@ -1004,7 +1006,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
 // ---------------------------------------------------------------- the persistent kernel
 template <int K>
 __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
-  extern __shared__ int smem[];
+  extern __shared__ __align__(16) int smem[];
   __shared__ int bc[8];
   __shared__ long long red[NTH / 32];
   __shared__ uint32_t task_s;
