@@ -98,11 +98,17 @@ struct Dev {
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]
   unsigned long long* sumneg; // [nslot]
-  // work queue: ring of tile ids, ticketed by two 64-bit counters
+  // work queues: rings of task entries, ticketed by two 64-bit counters each.
+  // q holds the latency-critical tasks (relabel, push, closure: dependency chains), qi the
+  // init groups (HBM streaming); an idle CTA serves q first.
   uint32_t* q;
   uint32_t qmask;
-  unsigned long long* qhead;
+  unsigned long long* qhead;   // qhead, qtail adjacent and 16-byte aligned (read as one)
   unsigned long long* qtail;
+  uint32_t* qi;
+  uint32_t qimask;
+  unsigned long long* qihead;  // likewise
+  unsigned long long* qitail;
   int32_t* done;    // [0] every frame finished, [1] aborted
   unsigned long long* ntask;  // tasks executed (watchdog)
   const volatile int32_t* hostabort;  // mapped host word: the host asks the kernel to stop

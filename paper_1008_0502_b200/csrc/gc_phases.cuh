@@ -42,12 +42,15 @@ namespace gcb {
 #endif
 constexpr uint32_t QEMPTY = 0xffffffffu;
 constexpr uint32_t QEXIT = 0xfffffffeu;
+constexpr uint32_t QNOP = 0xfffffffdu;  // releases a CTA waiting on the init ring (no task)
 
 struct Ctl {
   long long relabel_budget;  // relabels per push phase (alpha x frame pixels)
   long long max_tasks;       // watchdog: tasks per launch before GC_ERR_NOCONV
   int vis_budget;            // push tasks per push phase
   int stall;                 // push tasks without progress before the phase drains
+  int stallx;                // the stall bound doubles with every failed certificate attempt
+                             // beyond the first stallx (hard frames: long transport)
   int wave;                  // push phase starts on active tiles with min height <= lowest + wave
   int selfrun;               // 0: an active tile always runs again; 1: only after progress
   int rounds;                // push/relabel rounds per push task
@@ -63,6 +66,11 @@ __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" 
 __device__ __forceinline__ void q_put(const Dev& d, unsigned long long p, uint32_t v) {
   volatile uint32_t* slot = d.q + (p & d.qmask);
   while (*slot != QEMPTY) __nanosleep(32);  // previous lap not consumed yet (capacity 2x: never in practice)
+  *slot = v;
+}
+__device__ __forceinline__ void qi_put(const Dev& d, unsigned long long p, uint32_t v) {
+  volatile uint32_t* slot = d.qi + (p & d.qimask);
+  while (*slot != QEMPTY) __nanosleep(32);
   *slot = v;
 }
 
@@ -579,7 +587,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     const int vis = __ldcg(d.fvis + s);
     const int cep = __ldcg(d.cep + s);  // failed certificate attempts: longer phases
     const bool cond = ((long long)__ldcg(d.frel + s) > (c.relabel_budget << min(cep, 10))) || (vis >= c.vis_budget) ||
-                      (vis - __ldcg(d.fprog + s) > c.stall);
+                      (vis - __ldcg(d.fprog + s) > (c.stall << min(max(cep - c.stallx, 0), 24)));
     bc[0] = cond || __ldcg(d.fdrain + s);
     if (cond) d.fdrain[s] = 1;  // no more requests in this phase
     bc[1] = 0;
@@ -924,6 +932,10 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         } else {
           nm = M_IDLE;
           kind = SET_NONE;
+          if (nf == c.nframes) {  // no init group will be queued any more: release every CTA
+            const unsigned long long p0 = atomicAdd(d.qitail, (unsigned long long)gridDim.x);  // parked on qi
+            for (unsigned i = 0; i < gridDim.x; ++i) qi_put(d, p0 + i, QNOP);
+          }
         }
       }
       if (nm == M_SEED) {  // a new global relabel, bounded: distances up to 2 + 2^(attempts+1)
@@ -983,13 +995,16 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (cnt == 0) continue;
       if (t == 0) {
         atomicAdd(&d.fout[s], cnt);
-        const unsigned long long p0 = atomicAdd(d.qtail, (unsigned long long)cnt);
+        const unsigned long long p0 = atomicAdd(kind == SET_INITG ? d.qitail : d.qtail, (unsigned long long)cnt);
         bc[6] = (int)(p0 & 0xffffffffu);
         bc[7] = (int)(p0 >> 32);
       }
       __syncthreads();
       const unsigned long long p0 = ((unsigned long long)(uint32_t)bc[7] << 32) | (uint32_t)bc[6];
-      if (want) q_put(d, p0 + li, qent(bc[2], base_gt + i, gcnt));
+      if (want) {
+        if (kind == SET_INITG) qi_put(d, p0 + li, qent(bc[2], base_gt + i, gcnt));
+        else q_put(d, p0 + li, qent(bc[2], base_gt + i, gcnt));
+      }
       __syncthreads();
     }
     if (t == 0) {
@@ -1024,17 +1039,34 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
     } else if (t == 0) {
       uint64_t w0 = 0;
       if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0));
-      tick = atomicAdd(d.qhead, 1ULL);
-      volatile uint32_t* slot = d.q + (tick & d.qmask);
-      uint32_t v;
+      // latency-critical tasks first, then init groups.  A ticket is taken only when the ring
+      // looked non-empty; a CTA that lost the race waits for the ring's next entry (chain
+      // tasks arrive every few ns; the init ring is released by QNOP entries at the end).
+      // Both rings empty: wait on a ticket of q (the next chain task is picked up at once).
+      uint32_t v = QEMPTY;
       int ns = 32, spins = 0;
-      while ((v = *slot) == QEMPTY) {
-        if (*(volatile int*)&d.done[0] || *(volatile int*)&d.done[1]) { v = QEXIT; break; }
-        if ((++spins & 255) == 0 && *d.hostabort) { *(volatile int*)&d.done[1] = 1; v = QEXIT; break; }
-        __nanosleep(ns);
-        ns = ns < 1024 ? 2 * ns : 1024;
+      volatile uint32_t* slot;
+      {
+        unsigned long long qh, qt, qih, qit;  // one 16-byte load per ring: head, tail
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qh), "=l"(qt) : "l"(d.qhead));
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qih), "=l"(qit) : "l"(d.qihead));
+        if (qt <= qh && qit > qih) {
+          tick = atomicAdd(d.qihead, 1ULL);
+          slot = d.qi + (tick & d.qimask);
+        } else {
+          tick = atomicAdd(d.qhead, 1ULL);
+          slot = d.q + (tick & d.qmask);
+        }
       }
-      if (v != QEXIT) *slot = QEMPTY;
+      {
+        while ((v = *slot) == QEMPTY) {
+          if (*(volatile int*)&d.done[0] || *(volatile int*)&d.done[1]) { v = QEXIT; break; }
+          if ((++spins & 255) == 0 && *d.hostabort) { *(volatile int*)&d.done[1] = 1; v = QEXIT; break; }
+          __nanosleep(ns);
+          ns = ns < 1024 ? 2 * ns : 1024;
+        }
+        if (v != QEXIT) *slot = QEMPTY;
+      }
       if (prof) {
         uint64_t w1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
@@ -1049,6 +1081,10 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
     __syncthreads();
     const uint32_t v = task_s;
     if (v == QEXIT || *(volatile int*)&d.done[1]) break;
+    if (v == QNOP) {
+      __syncthreads();  // every thread has read task_s before thread 0 takes the next one
+      continue;
+    }
     const size_t gt = v & 0x00ffffffu;
     const int s = (int)((unsigned)gt / (unsigned)d.T);
     const int md = (int)(v >> 28);
@@ -1163,7 +1199,7 @@ __global__ void k_setup(Dev d, int nframes) {
   const size_t ntask = (size_t)d.nslot * G;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ntask; i += (size_t)gridDim.x * blockDim.x) {
     const size_t s = i / G, g = i - s * G;
-    d.q[i] = qent(M_INIT, s * d.T + g * d.initg);
+    d.qi[i] = qent(M_INIT, s * d.T + g * d.initg);
     if (g == 0) {
       d.sfr[s] = (int)s;
       d.fmode[s] = M_INIT;
@@ -1171,7 +1207,7 @@ __global__ void k_setup(Dev d, int nframes) {
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *d.qtail = ntask;
+    *d.qitail = ntask;
     d.gctr[0] = d.nslot;
   }
 }
@@ -1182,7 +1218,10 @@ __global__ void k_abort(Dev d, IO io, int nframes) {
     if (d.fmode[s] == M_IDLE) continue;
     const int f = d.sfr[s];
     io.flow[f] = -1;
-    if (io.stats) io.stats[f * 4 + 3] = 5;
+    if (io.stats) {  // the counters so far (push tasks, global relabels, BFS relax tasks)
+      for (int i = 0; i < 3; ++i) io.stats[f * 4 + i] = d.fstat[s * 4 + i];
+      io.stats[f * 4 + 3] = 5;
+    }
   }
   const int first = d.gctr[0];
   for (int f = first + blockIdx.x * blockDim.x + threadIdx.x; f < nframes; f += gridDim.x * blockDim.x) {

@@ -32,6 +32,7 @@ struct gc_ctx {
   double timeout_s = 300.0;       // wall-clock bound of one k_solve launch
   int vis_mult = 64;              // push tasks per push phase = vis_mult x frame tiles
   int stall = 64;                 // push tasks without progress before a push phase drains
+  int stallx = 1 << 20;           // ... doubled per failed certificate attempt beyond stallx
   int wave = 0;                   // push cap: heights above the lowest active one + wave freeze
                                   // (doubled from 1 per failed certificate attempt)
   int selfrun = 0;                // 1: a push tile re-runs itself only after progress
@@ -115,12 +116,15 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.fstat = w; w += 4 * nslot;
   d.gctr = w; w += 4;
   d.done = w; w += 4;
-  unsigned long long* u = (unsigned long long*)align_up((size_t)w, 8);
+  unsigned long long* u = (unsigned long long*)align_up((size_t)w, 16);
   d.frel = u; u += nslot;
   d.sumct = u; u += nslot;
   d.sumneg = u; u += nslot;
+  u = (unsigned long long*)align_up((size_t)u, 16);
   d.qhead = u; u += 1;
   d.qtail = u; u += 1;
+  d.qihead = u; u += 1;
+  d.qitail = u; u += 1;
   d.ntask = u; u += 1;
   c->words_bytes = (char*)u - fw;
   d.treq = (int32_t*)take(ns * 4);
@@ -130,7 +134,11 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   const size_t qcap = pow2_at_least(2 * ns + 1024);
   d.q = (uint32_t*)take(qcap * 4);
   d.qmask = (uint32_t)(qcap - 1);
-  *q_bytes = qcap * 4;
+  // init ring: every slot's init groups once, plus one release entry per CTA (k_solve)
+  const size_t qicap = pow2_at_least(2 * ((size_t)nslot * ((T + d.initg - 1) / d.initg) + 4096) + 1024);
+  d.qi = (uint32_t*)take(qicap * 4);
+  d.qimask = (uint32_t)(qicap - 1);
+  *q_bytes = (char*)(d.qi + qicap) - (char*)d.q;
   d.e = (int32_t*)take(ns * TPX * 4);
   d.h = (int32_t*)take(ns * TPX * 4);
   d.r = (int32_t*)take(ns * K * TPX * 4);
@@ -258,6 +266,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   ctl.relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
   ctl.vis_budget = c->vis_mult * d.T;
   ctl.stall = c->stall;
+  ctl.stallx = c->stallx;
   ctl.wave = c->wave;
   ctl.selfrun = c->selfrun;
   ctl.rounds = c->rounds;
@@ -379,6 +388,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (const char* ev = getenv("GC_ALPHA")) c->alpha = atof(ev);          // tuning knobs
   if (const char* ev = getenv("GC_VIS")) c->vis_mult = atoi(ev);
   if (const char* ev = getenv("GC_STALL")) c->stall = atoi(ev);
+  if (const char* ev = getenv("GC_STALLX")) c->stallx = atoi(ev);
   if (const char* ev = getenv("GC_WAVE")) c->wave = atoi(ev);
   if (const char* ev = getenv("GC_SELFRUN")) c->selfrun = atoi(ev);
   if (const char* ev = getenv("GC_TIMEOUT_S")) c->timeout_s = atof(ev);
