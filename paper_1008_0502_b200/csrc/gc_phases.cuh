@@ -68,6 +68,20 @@ __device__ __forceinline__ void q_put(const Dev& d, unsigned long long p, uint32
   while (*slot != QEMPTY) __nanosleep(32);  // previous lap not consumed yet (capacity 2x: never in practice)
   *slot = v;
 }
+// Chain tasks of hard frames (URGENT_RELABELS global relabels or more) go to the urgent
+// ring, served first: a hard frame is a dependency chain that would otherwise end the call
+// late, waiting behind the easy frames' tasks.
+constexpr int URGENT_RELABELS = 4;
+__device__ __forceinline__ bool urgent_slot(const Dev& d, int s) { return __ldcg(d.fbe + s) >= URGENT_RELABELS; }
+__device__ __forceinline__ void qu_put(const Dev& d, unsigned long long p, uint32_t v) {
+  volatile uint32_t* slot = d.qu + (p & d.qmask);
+  while (*slot != QEMPTY) __nanosleep(32);
+  *slot = v;
+}
+__device__ __forceinline__ void chain_put(const Dev& d, int s, uint32_t v) {
+  if (urgent_slot(d, s)) qu_put(d, atomicAdd(d.qutail, 1ULL), v);
+  else q_put(d, atomicAdd(d.qtail, 1ULL), v);
+}
 __device__ __forceinline__ void qi_put(const Dev& d, unsigned long long p, uint32_t v) {
   volatile uint32_t* slot = d.qi + (p & d.qimask);
   while (*slot != QEMPTY) __nanosleep(32);
@@ -995,15 +1009,20 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (cnt == 0) continue;
       if (t == 0) {
         atomicAdd(&d.fout[s], cnt);
-        const unsigned long long p0 = atomicAdd(kind == SET_INITG ? d.qitail : d.qtail, (unsigned long long)cnt);
+        const bool urg = kind != SET_INITG && urgent_slot(d, s);
+        bc[2] = (bc[2] & 0xffff) | (urg << 16);
+        const unsigned long long p0 =
+            atomicAdd(kind == SET_INITG ? d.qitail : (urg ? d.qutail : d.qtail), (unsigned long long)cnt);
         bc[6] = (int)(p0 & 0xffffffffu);
         bc[7] = (int)(p0 >> 32);
       }
       __syncthreads();
       const unsigned long long p0 = ((unsigned long long)(uint32_t)bc[7] << 32) | (uint32_t)bc[6];
       if (want) {
-        if (kind == SET_INITG) qi_put(d, p0 + li, qent(bc[2], base_gt + i, gcnt));
-        else q_put(d, p0 + li, qent(bc[2], base_gt + i, gcnt));
+        const uint32_t ent = qent(bc[2] & 0xffff, base_gt + i, gcnt);
+        if (kind == SET_INITG) qi_put(d, p0 + li, ent);
+        else if (bc[2] >> 16) qu_put(d, p0 + li, ent);
+        else q_put(d, p0 + li, ent);
       }
       __syncthreads();
     }
@@ -1047,10 +1066,14 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
       int ns = 32, spins = 0;
       volatile uint32_t* slot;
       {
-        unsigned long long qh, qt, qih, qit;  // one 16-byte load per ring: head, tail
+        unsigned long long qh, qt, qih, qit, quh, qut;  // one 16-byte load per ring: head, tail
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(quh), "=l"(qut) : "l"(d.quhead));
         asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qh), "=l"(qt) : "l"(d.qhead));
         asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qih), "=l"(qit) : "l"(d.qihead));
-        if (qt <= qh && qit > qih) {
+        if (qut > quh) {
+          tick = atomicAdd(d.quhead, 1ULL);
+          slot = d.qu + (tick & d.qmask);
+        } else if (qt <= qh && qit > qih) {
           tick = atomicAdd(d.qihead, 1ULL);
           slot = d.qi + (tick & d.qimask);
         } else {
@@ -1148,7 +1171,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
           const int sub = c0 - (bc[3] ? 1 : 0);  // a push task still active keeps one request
           rem = atomicSub(&d.treq[gt], sub) - sub;
           if (rem > 0 && atomicCAS(&next_s, QEMPTY, qent(md, gt)) != QEMPTY)  // run again
-            q_put(d, atomicAdd(d.qtail, 1ULL), qent(md, gt));
+            chain_put(d, s, qent(md, gt));
         }
       } else if (t <= 8 && !drain) {
         const int b = t - 1;
@@ -1157,7 +1180,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
           if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) {
             if (atomicAdd(&d.treq[n], 1) == 0) {
               atomicAdd(&d.fout[s], 1);
-              if (atomicCAS(&next_s, QEMPTY, qent(md, n)) != QEMPTY) q_put(d, atomicAdd(d.qtail, 1ULL), qent(md, n));
+              if (atomicCAS(&next_s, QEMPTY, qent(md, n)) != QEMPTY) chain_put(d, s, qent(md, n));
             }
           }
         }

@@ -32,7 +32,7 @@ struct gc_ctx {
   double timeout_s = 300.0;       // wall-clock bound of one k_solve launch
   int vis_mult = 64;              // push tasks per push phase = vis_mult x frame tiles
   int stall = 64;                 // push tasks without progress before a push phase drains
-  int stallx = 1 << 20;           // ... doubled per failed certificate attempt beyond stallx
+  int stallx = 8;                 // ... doubled per failed certificate attempt beyond stallx
   int wave = 0;                   // push cap: heights above the lowest active one + wave freeze
                                   // (doubled from 1 per failed certificate attempt)
   int selfrun = 0;                // 1: a push tile re-runs itself only after progress
@@ -125,6 +125,8 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.qtail = u; u += 1;
   d.qihead = u; u += 1;
   d.qitail = u; u += 1;
+  d.quhead = u; u += 1;
+  d.qutail = u; u += 1;
   d.ntask = u; u += 1;
   c->words_bytes = (char*)u - fw;
   d.treq = (int32_t*)take(ns * 4);
@@ -134,6 +136,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   const size_t qcap = pow2_at_least(2 * ns + 1024);
   d.q = (uint32_t*)take(qcap * 4);
   d.qmask = (uint32_t)(qcap - 1);
+  d.qu = (uint32_t*)take(qcap * 4);
   // init ring: every slot's init groups once, plus one release entry per CTA (k_solve)
   const size_t qicap = pow2_at_least(2 * ((size_t)nslot * ((T + d.initg - 1) / d.initg) + 4096) + 1024);
   d.qi = (uint32_t*)take(qicap * 4);

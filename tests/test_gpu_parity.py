@@ -346,3 +346,82 @@ def test_host_watchdog_stops_the_kernel(torch, gc, monkeypatch):
     F2, m2 = g2.solve(*to_dev(torch, cs, ct, nb))
     check_against_oracle(cs, ct, nb, F2.cpu().numpy(), m2.cpu().numpy(), "bk", frames=[0, 7])
     g2.close()
+
+
+def residual_closure_host(cs, ct, nb, f):
+    """Pixels reachable from s in the residual graph of the exported flow f:
+    the closure of {e > 0} (s -> v keeps residual capacity e(v)) under n-link arcs with
+    r_k(p) = c_k(p) - f(p -> p + d_k) > 0.  Plain scipy BFS (library routine), no solver code."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import breadth_first_order
+    K, H, W = nb.shape
+    N = H * W
+    idx = np.arange(N, dtype=np.int64).reshape(H, W)
+    e = cs.astype(np.int64) - ct.astype(np.int64)
+    flow = {}  # flow on arc p -> p + d_k for every k, from the forward-arc flows
+    for j in range(K // 2):
+        k = 2 * j
+        fk = np.zeros((H, W), np.int64)
+        y0, y1 = max(0, -DY[k]), H - max(0, DY[k])
+        x0, x1 = max(0, -DX[k]), W - max(0, DX[k])
+        fk[y0:y1, x0:x1] = f[j, y0:y1, x0:x1]
+        flow[k] = fk
+        rv = np.zeros((H, W), np.int64)  # reverse arc q -> p carries -f(p -> q), stored at q
+        rv[y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]] = -fk[y0:y1, x0:x1]
+        flow[k ^ 1] = rv
+        e[y0:y1, x0:x1] -= fk[y0:y1, x0:x1]
+        e[y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]] += fk[y0:y1, x0:x1]
+    rows, cols = [], []
+    for k in range(K):
+        y0, y1 = max(0, -DY[k]), H - max(0, DY[k])
+        x0, x1 = max(0, -DX[k]), W - max(0, DX[k])
+        r = nb[k, y0:y1, x0:x1].astype(np.int64) - flow[k][y0:y1, x0:x1]
+        open_ = r > 0
+        rows.append(idx[y0:y1, x0:x1][open_])
+        cols.append(idx[y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]][open_])
+    src = np.flatnonzero(e.ravel() > 0)  # super-source N -> every excess node
+    rows.append(np.full(src.size, N, np.int64))
+    cols.append(src)
+    r_ = np.concatenate(rows)
+    c_ = np.concatenate(cols)
+    G = sp.csr_matrix((np.ones(r_.size, np.int8), (r_, c_)), shape=(N + 1, N + 1))
+    order = breadth_first_order(G, N, directed=True, return_predecessors=False)
+    m = np.zeros(N + 1, np.uint8)
+    m[order] = 1
+    return m[:N].reshape(H, W)
+
+
+def test_c5_4k_serpentine_certified(torch, gc):
+    """C5 at its full size (3840x2160 serpentine, 64-px lanes, bimodal {1, 2^20} n-links):
+    the CPU oracle needs hours on this frame, so the result is certified without it
+    (SURVEY.md §8(c) "flow certificate"): the exported flow is arc-feasible, F(f) == F ==
+    cut(mask) (so F is the maximum flow and the mask a minimum cut), and the mask equals the
+    residual closure of the excess nodes recomputed on the host (the canonical cut)."""
+    synth.set_serpentine_params(lane=64, big=1 << 20)
+    try:
+        hc, ht, hn = synth.gen_host("serpentine", synth.BASE_SEED + 4, 0, 1, 2160, 3840, 4)
+    finally:
+        synth.set_serpentine_params()
+    g = gc.GridCut(neighborhood=4, max_h=2160, max_w=3840)
+    cs, ct, nb = to_dev(torch, hc, ht, hn)
+    F, mask, fs = g.solve(cs, ct, nb, flow_state=True)
+    torch.cuda.synchronize()
+    Fg = int(F[0])
+    assert int(cut_torch(torch, cs, ct, nb, mask)[0]) == Fg
+    ok, Ff = cut_cert(hc[0], ht[0], hn[0], fs[0].cpu().numpy())
+    assert ok and Ff == Fg
+    np.testing.assert_array_equal(mask[0].cpu().numpy(), residual_closure_host(hc[0], ht[0], hn[0], fs[0].cpu().numpy()))
+    g.close()
+
+
+def test_serpentine_lane64_parity(torch, gc):
+    """C5's lane geometry (64-px lanes) at a size the oracle finishes in seconds: bit-exact
+    F and mask against Boykov-Kolmogorov, two frames in flight."""
+    synth.set_serpentine_params(lane=64, big=1 << 20)
+    try:
+        cs, ct, nb = synth.gen_host("serpentine", synth.BASE_SEED + 4, 0, 2, 256, 384, 4)
+    finally:
+        synth.set_serpentine_params()
+    g = solver(gc, 4)
+    F, mask = g.solve(*to_dev(torch, cs, ct, nb))
+    check_against_oracle(cs, ct, nb, F.cpu().numpy(), mask.cpu().numpy(), "bk")
