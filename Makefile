@@ -1,7 +1,8 @@
 # Builds every native artefact in-tree (they travel to the GPU box with gpurun).
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude $(GC_DEFS)
+GC_DEFS ?= -DGC_SEED_BLOCK -DGC_CSEED_BLOCK
 PKG := paper_1008_0502_b200
 
 all: $(PKG)/libgc.so synth/libsynth.so oracle/liboracle.so

@@ -105,9 +105,6 @@ struct Dev {
   uint32_t qmask;
   unsigned long long* qhead;   // qhead, qtail adjacent and 16-byte aligned (read as one)
   unsigned long long* qtail;
-  uint32_t* qu;                // urgent chain tasks (hard frames), same capacity as q
-  unsigned long long* quhead;  // likewise
-  unsigned long long* qutail;
   uint32_t* qi;
   uint32_t qimask;
   unsigned long long* qihead;  // likewise

@@ -125,8 +125,6 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.qtail = u; u += 1;
   d.qihead = u; u += 1;
   d.qitail = u; u += 1;
-  d.quhead = u; u += 1;
-  d.qutail = u; u += 1;
   d.ntask = u; u += 1;
   c->words_bytes = (char*)u - fw;
   d.treq = (int32_t*)take(ns * 4);
@@ -136,7 +134,6 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   const size_t qcap = pow2_at_least(2 * ns + 1024);
   d.q = (uint32_t*)take(qcap * 4);
   d.qmask = (uint32_t)(qcap - 1);
-  d.qu = (uint32_t*)take(qcap * 4);
   // init ring: every slot's init groups once, plus one release entry per CTA (k_solve)
   const size_t qicap = pow2_at_least(2 * ((size_t)nslot * ((T + d.initg - 1) / d.initg) + 4096) + 1024);
   d.qi = (uint32_t*)take(qicap * 4);
@@ -251,7 +248,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   size_t sg_bytes = 0, q_bytes = 0;
   Dev d = carve(c, nslot, H, W, &sg_bytes, &q_bytes);
   static int g_solve[9] = {0};
-  const size_t smem = push_smem_bytes<K>();
+  const size_t smem = solve_smem_bytes<K>();
   if (!g_solve[K]) {
     cudaFuncSetAttribute(k_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     g_solve[K] = persistent_grid(c, k_solve<K>, smem);
