@@ -1,13 +1,12 @@
 # Builds every native artefact in-tree (they travel to the GPU box with gpurun).
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude $(GC_DEFS)
-GC_DEFS ?= -DGC_SEED_BLOCK -DGC_CSEED_BLOCK
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
 PKG := paper_1008_0502_b200
 
 all: $(PKG)/libgc.so synth/libsynth.so oracle/liboracle.so
 
-$(PKG)/libgc.so: $(PKG)/csrc/gc_solver.cu $(wildcard $(PKG)/csrc/*.cuh) include/gc.h
+$(PKG)/libgc.so: $(PKG)/csrc/gc_solver.cu $(wildcard $(PKG)/csrc/*.cuh) include/gc.h Makefile
 	$(NVCC) $(NVFLAGS) -Xptxas -v -Xptxas -dlcm=cg -shared -cudart static -o $@ $(PKG)/csrc/gc_solver.cu 2> build_gc_ptxas.log || (cat build_gc_ptxas.log; false)
 
 synth/libsynth.so: synth/synth_host.c synth/synth_cuda.cu synth/synth.h

@@ -236,155 +236,6 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   flag_sides(d, gt, bc[1], K);
 }
 
-// ---------------------------------------------------------------- a2: seed, a group of tiles
-// The same result as task_seed for each tile of a group of up to 8 consecutive tiles, one
-// tile per warp (lane l owns column l): the tiles' global round trips overlap instead of
-// running tile after tile behind block barriers.  Tiles with inbound flow in flight
-// (recv1) take the block-wide task_seed (it materialises e, r to absorb the flow).
-constexpr int SEEDW_BYTES = 4 * TPX + 4 * 132 + TPX;  // per warp: heights, halo ring, arc bits
-constexpr size_t seed_group_smem_bytes() { return (size_t)8 * SEEDW_BYTES; }
-
-__device__ __forceinline__ int halo_at(const volatile int* halo, int y2, int x2) {
-  // halo: [0,32) N row, [32,64) S row, [64,96) W column, [96,128) E column, 128.. NW NE SW SE
-  if (y2 < 0) return x2 < 0 ? halo[128] : (x2 > 31 ? halo[129] : halo[x2]);
-  if (y2 > 31) return x2 < 0 ? halo[130] : (x2 > 31 ? halo[131] : halo[32 + x2]);
-  return x2 < 0 ? halo[64 + y2] : halo[96 + y2];
-}
-
-template <int K>
-__device__ __forceinline__ void seed_warp_tile(const Dev& d, size_t gt, int fbe, int bnd, volatile int* hw,
-                                               volatile int* halo, volatile uint8_t* os) {
-  const int l = threadIdx.x & 31;
-  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  // untouched uniform sink tile: h = 1, hedge published at init
-  if (__shfl_sync(0xffffffffu, l == 0 ? __ldcg(d.tuni + gt) : 0, 0)) return;
-  // neighbours whose seed was skipped in this relabel: their border heights are final
-  int okb = 0;
-  if (l < 8 && !(l >= 4 && K == 4)) {
-    const long long n = side_tile(d, gt, l);
-    okb = n >= 0 && __ldcg(d.tsk + n) == fbe;
-  }
-  const unsigned sk = __ballot_sync(0xffffffffu, okb);
-  unsigned pos = 0, negb = 0;
-  const uint16_t* flp = d.fl + gt * TPX + l;
-#pragma unroll 8
-  for (int iy = 0; iy < 32; ++iy) {
-    const int f = flp[iy * TS];
-    os[iy * TS + l] = (uint8_t)(f & 0xff);
-    pos |= (unsigned)((f & FL_POS) != 0) << iy;
-    negb |= (unsigned)((f & FL_NEG) != 0) << iy;
-    hw[iy * TS + l] = (f & FL_NEG) ? 1 : HINF;
-  }
-  {  // halo ring: hedge of the skipped neighbours, INF elsewhere (side bits as side_bit)
-    const size_t sT = (size_t)s * d.T;
-    int v;
-    v = HINF; if ((sk >> 0) & 1) v = d.hedge[((sT + (ty - 1) * d.TX + tx) * 4 + 1) * 32 + l]; halo[l] = v;
-    v = HINF; if ((sk >> 1) & 1) v = d.hedge[((sT + (ty + 1) * d.TX + tx) * 4 + 0) * 32 + l]; halo[32 + l] = v;
-    v = HINF; if ((sk >> 2) & 1) v = d.hedge[((sT + ty * d.TX + tx - 1) * 4 + 3) * 32 + l]; halo[64 + l] = v;
-    v = HINF; if ((sk >> 3) & 1) v = d.hedge[((sT + ty * d.TX + tx + 1) * 4 + 2) * 32 + l]; halo[96 + l] = v;
-    if (l < 4) {
-      const int dy = l < 2 ? -1 : 1, dx = (l & 1) ? 1 : -1;
-      const int bit = dy < 0 ? (dx < 0 ? 4 : 5) : (dx < 0 ? 6 : 7);
-      v = HINF;
-      if ((sk >> bit) & 1)
-        v = d.hedge[((sT + (ty + dy) * d.TX + tx + dx) * 4 + (dy < 0 ? 1 : 0)) * 32 + (dx < 0 ? 31 : 0)];
-      halo[128 + l] = v;
-    }
-  }
-  __syncwarp();
-  // BFS fixpoint h(v) = min(h(v), 1 + min{h(v + d_k) : arc k open}) for distances below the
-  // relabel's bound; sweeps alternate down / up the column
-  for (int sw = 0;; ++sw) {
-    int changed = 0;
-    for (int i = 0; i < 32; ++i) {
-      const int iy = (sw & 1) ? 31 - i : i;
-      const int hv = hw[iy * TS + l];
-      if (hv <= 1) continue;
-      const int ob = os[iy * TS + l];
-      if (!ob) continue;
-      int mn = HINF;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        if (!((ob >> k) & 1)) continue;
-        const int y2 = iy + DYk(k), x2 = l + DXk(k);
-        const int hu = ((unsigned)y2 < 32u && (unsigned)x2 < 32u) ? hw[y2 * TS + x2] : halo_at(halo, y2, x2);
-        mn = min(mn, hu);
-      }
-      if (mn < bnd && mn + 1 < hv) {
-        hw[iy * TS + l] = mn + 1;
-        changed = 1;
-      }
-    }
-    __syncwarp();
-    if (!__any_sync(0xffffffffu, changed)) break;
-  }
-  int act = 0, fix = 1, uni = 1, bits = 0, mnh = HINF;
-  {
-    int32_t* hp = d.h + gt * TPX + l;
-    const int x = tx * TS + l;
-#pragma unroll 8
-    for (int iy = 0; iy < 32; ++iy) {
-      const int h = hw[iy * TS + l];
-      hp[iy * TS] = h;
-      const int p = (pos >> iy) & 1;
-      act |= p && h < HINF;
-      if (p) mnh = min(mnh, h);
-      fix &= (h == 1) || !os[iy * TS + l];
-      const bool in = ty * TS + iy < d.H && x < d.W;
-      uni &= !in || ((negb >> iy) & 1);
-      if ((iy == 0 || iy == 31 || l == 0 || l == 31) && h < HINF) bits |= border_bits(iy, l);
-    }
-  }
-  {  // border heights: top row, bottom row, left column, right column
-    int32_t* he = d.hedge + gt * 128;
-    he[l] = hw[l];
-    he[32 + l] = hw[31 * TS + l];
-    he[64 + l] = hw[l * TS];
-    he[96 + l] = hw[l * TS + 31];
-  }
-  act = __any_sync(0xffffffffu, act);
-  fix = __all_sync(0xffffffffu, fix);
-  uni = __all_sync(0xffffffffu, uni);
-  bits = __reduce_or_sync(0xffffffffu, bits);
-  mnh = __reduce_min_sync(0xffffffffu, mnh);
-  if (l == 0) {
-    d.tact[gt] = act;
-    d.tminh[gt] = mnh;
-    d.tfix[gt] = fix;
-    d.tuni[gt] = uni;
-  }
-  if (l < 8 && ((bits >> l) & 1) && !(l >= 4 && K == 4)) {
-    const long long n = side_tile(d, gt, l);
-    if (n >= 0) d.flag[n] = 1;
-  }
-}
-
-template <int K>
-__device__ __noinline__ void task_seed_group(const Dev& d, const IO& io, size_t gt0, int n, int* smem, int* bc) {
-  const int t = threadIdx.x, w = t >> 5;
-  const int s = (int)((unsigned)gt0 / (unsigned)d.T);
-  if (t == 0) {
-    bc[0] = 0;
-    bc[6] = __ldcg(d.fbe + s);
-    bc[4] = __ldcg(d.fbnd + s);
-  }
-  __syncthreads();
-  if (t < n && __ldcg(d.recv1 + gt0 + t)) atomicOr(&bc[0], 1 << t);
-  __syncthreads();
-  const int rcv = bc[0], fbe = bc[6], bnd = bc[4];
-  if (w < n && !((rcv >> w) & 1)) {
-    uint8_t* base = reinterpret_cast<uint8_t*>(smem) + w * SEEDW_BYTES;
-    seed_warp_tile<K>(d, gt0 + w, fbe, bnd, reinterpret_cast<int*>(base), reinterpret_cast<int*>(base + 4 * TPX),
-                      base + 4 * TPX + 4 * 132);
-  }
-  for (int j = 0; j < n; ++j) {  // tiles with inbound flow: block-wide (absorbs it first)
-    if (!((rcv >> j) & 1)) continue;
-    __syncthreads();
-    task_seed<K>(d, io, gt0 + j, smem, bc);
-  }
-}
-
 // ---------------------------------------------------------------- a2: relax (one tile)
 // Returns (in bc[1]) the sides whose tiles must be requested: their halo reads a changed
 // border height.
@@ -609,165 +460,6 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   flag_sides(d, gt, sides, K);
 }
 
-// ---------------------------------------------------------------- a4: closure seed, a group of tiles
-// The same result as task_cseed for each tile of a group of up to 8 consecutive tiles, one
-// tile per warp: the tiles' dependent global round trips (tile words, fl, e, the border
-// halo) overlap instead of running tile after tile behind block barriers.  Lane l owns
-// column l of its tile (rows 0..31: coalesced 64-byte rows).  Tiles with inbound flow
-// still in flight (recv1) take the block-wide task_cseed (it materialises e, r to absorb).
-template <int K>
-__device__ __forceinline__ void cseed_warp_tile(const Dev& d, const IO& io, size_t gt, int ep, volatile uint8_t* ms,
-                                                volatile uint8_t* os) {
-  const int l = threadIdx.x & 31;
-  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
-  const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  int mat = 0, skip = 0;
-  if (l == 0) {
-    mat = __ldcg(d.mat + gt);
-    // (a tile of the group outside the task set) an untouched uniform sink tile that never
-    // had closure pixels
-    skip = __ldcg(d.tuni + gt) && !mat && __ldcg(d.tmk + gt) == 0;
-  }
-  mat = __shfl_sync(0xffffffffu, mat, 0);
-  if (__shfl_sync(0xffffffffu, skip, 0)) return;
-  const uint16_t* flp = d.fl + gt * TPX + l;
-  unsigned pos = 0, negb = 0;
-  long long neg = 0;
-#pragma unroll 8
-  for (int iy = 0; iy < 32; ++iy) {
-    const int f = flp[iy * TS];
-    os[iy * TS + l] = (uint8_t)(f & 0xff);
-    ms[iy * TS + l] = (f & FL_POS) ? 1 : 0;
-    pos |= (unsigned)((f & FL_POS) != 0) << iy;
-    negb |= (unsigned)((f & FL_NEG) != 0) << iy;
-  }
-  if (mat) {
-    const int32_t* ep_ = d.e + gt * TPX + l;
-#pragma unroll 8
-    for (int iy = 0; iy < 32; ++iy) {
-      const int ev = ep_[iy * TS];
-      neg += ev < 0 ? -(long long)ev : 0;
-    }
-  }
-  __syncwarp();
-  // closure fixpoint inside the tile: sweeps alternate down / up the column (vertical arcs
-  // propagate within a sweep), horizontal neighbours through shared memory
-  unsigned mc = pos;
-  for (int sw = 0;; ++sw) {
-    int changed = 0;
-    for (int i = 0; i < 32; ++i) {
-      const int iy = (sw & 1) ? 31 - i : i;
-      if ((mc >> iy) & 1) continue;
-      int got = 0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int wy = iy - DYk(k), wx = l - DXk(k);
-        if ((unsigned)wy < 32u && (unsigned)wx < 32u) {
-          const int w = wy * TS + wx;
-          got |= ms[w] & (os[w] >> k) & 1;
-        }
-      }
-      if (got) {
-        mc |= 1u << iy;
-        ms[iy * TS + l] = 1;
-        changed = 1;
-      }
-    }
-    __syncwarp();
-    if (!__any_sync(0xffffffffu, changed)) break;
-  }
-  const int fail = __any_sync(0xffffffffu, (mc & negb) != 0);
-  const int any = __any_sync(0xffffffffu, mc != 0);
-  if (d.pdbg && l == 0) {
-    atomicAdd(&d.pdbg[9], 1ULL);
-  }
-  // m (closure epoch) and the caller's mask bytes of every in-frame pixel of the tile
-  {
-    uint8_t* mp = d.m + gt * TPX + l;
-    const int x = tx * TS + l;
-    uint8_t* mk = io.mask + (size_t)d.sfr[s] * d.H * d.W + x;
-#pragma unroll 8
-    for (int iy = 0; iy < 32; ++iy) {
-      const int in = (mc >> iy) & 1;
-      mp[iy * TS] = in ? (uint8_t)ep : (uint8_t)0;
-      const int y = ty * TS + iy;
-      if (y < d.H && x < d.W) mk[(size_t)y * d.W] = (uint8_t)in;
-    }
-  }
-  // reach marks across the border: every open arc leaving a closure pixel of the tile
-  // toward a neighbour pixel that is not an excess node (those are in the closure anyway).
-  // Pass b handles the arcs whose head lies beyond side b (0 N, 1 S, 2 W, 3 E; W/E passes
-  // only rows 0..31): every crossing arc once, from the pixel on that side.
-  int sides = 0;
-  if (any) {
-#pragma unroll 1
-    for (int b = 0; b < 4; ++b) {
-      const int iy = b == 0 ? 0 : (b == 1 ? 31 : l), ix = b == 2 ? 0 : (b == 3 ? 31 : l);
-      const int p = iy * TS + ix;
-      if (!ms[p]) continue;
-      const int ob = os[p];
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        if (!((ob >> k) & 1)) continue;
-        const int y2 = iy + DYk(k), x2 = ix + DXk(k);
-        const bool mine = b == 0 ? y2 < 0 : (b == 1 ? y2 > 31 : ((unsigned)y2 < 32u && (b == 2 ? x2 < 0 : x2 > 31)));
-        if (!mine) continue;
-        const int dy = y2 < 0 ? -1 : (y2 > 31 ? 1 : 0), dx = x2 < 0 ? -1 : (x2 > 31 ? 1 : 0);
-        const int rty = ty + dy, rtx = tx + dx;
-        if (rty < 0 || rty >= d.TY || rtx < 0 || rtx >= d.TX) continue;
-        const size_t rgt = (size_t)s * d.T + rty * d.TX + rtx;
-        if (__ldcg(d.fl + rgt * TPX + (y2 & 31) * TS + (x2 & 31)) & FL_POS) continue;
-        d.reach[(rgt * K + k) * 64 + recv_slot(k, y2 & 31, x2 & 31)] = (uint8_t)ep;
-        sides |= 1 << side_bit(dy, dx);
-      }
-    }
-  }
-  sides = __reduce_or_sync(0xffffffffu, sides);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
-  if (l < 8 && ((sides >> l) & 1) && !(l >= 4 && K == 4)) {
-    const long long n = side_tile(d, gt, l);
-    if (n >= 0) d.flag[n] = 1;
-  }
-  if (l == 0) {
-    if (mat) {  // replace the tile's share of sum max(0,-e) by its current value
-      const long long dl = neg - d.neg0[gt];
-      if (dl) atomicAdd(&d.sumneg[s], (unsigned long long)dl);
-      d.neg0[gt] = neg;
-    }
-    d.tcs[gt] = ep;
-    if (any) d.tmk[gt] = ep;
-    if (fail) atomicAdd(&d.cfail[s], 2);  // cfail: 0 / -1 (after the BFS certificate) + 2 per failure
-  }
-}
-
-template <int K>
-__device__ __noinline__ void task_cseed_group(const Dev& d, const IO& io, size_t gt0, int n, int* smem,
-                                              long long* red, int* bc) {
-  const int t = threadIdx.x, w = t >> 5;
-  const int s = (int)((unsigned)gt0 / (unsigned)d.T);
-  if (t == 0) {
-    // range error (mask stays 0, F = -1) or the attempt already failed
-    bc[2] = __ldcg(d.ferr + s) || __ldcg(d.cfail + s) > 0;
-    bc[0] = 0;
-  }
-  __syncthreads();
-  if (bc[2]) return;
-  if (t < n && __ldcg(d.recv1 + gt0 + t)) atomicOr(&bc[0], 1 << t);
-  __syncthreads();
-  const int rcv = bc[0];
-  const int ep = closure_epoch(d, s);
-  if (w < n && !((rcv >> w) & 1)) {
-    uint8_t* base = reinterpret_cast<uint8_t*>(smem) + w * 2 * TPX;
-    cseed_warp_tile<K>(d, io, gt0 + w, ep, base, base + TPX);
-  }
-  for (int j = 0; j < n; ++j) {  // tiles with inbound flow: block-wide (absorbs it first)
-    if (!((rcv >> j) & 1)) continue;
-    __syncthreads();
-    task_cseed<K>(d, io, gt0 + j, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, red, bc);
-  }
-}
-
 // ---------------------------------------------------------------- a4: closure relax (one tile)
 // Returns the sides to request in bc[1].
 template <int K>
@@ -878,9 +570,7 @@ template <int K>
 constexpr size_t push_smem_bytes() { return sizeof(int) * (2 * HS * HS + TPX + K * TPX + K * 64); }
 // dynamic shared memory of k_solve: the largest task layout
 template <int K>
-constexpr size_t solve_smem_bytes() {
-  return push_smem_bytes<K>() > seed_group_smem_bytes() ? push_smem_bytes<K>() : seed_group_smem_bytes();
-}
+constexpr size_t solve_smem_bytes() { return push_smem_bytes<K>(); }
 static_assert(init_smem_bytes<4>() <= push_smem_bytes<4>() && init_smem_bytes<8>() <= push_smem_bytes<8>(),
               "the init pass's prefetch buffer must fit the push tile's shared memory");
 
@@ -1419,14 +1109,10 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
     switch (md) {
       case M_INIT: task_init<K>(d, io, gt, c.vec != 0, smem); cls = 0; break;
       case M_SEED:
-#ifdef GC_SEED_BLOCK
         for (int j = 0; j < gcnt; ++j) {
           if (j) __syncthreads();
           task_seed<K>(d, io, gt + j, smem, bc);
         }
-#else
-        task_seed_group<K>(d, io, gt, gcnt, smem, bc);
-#endif
         cls = 1;
         break;
       case M_BFS:
@@ -1436,14 +1122,10 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
         break;
       case M_PUSH: task_push<K>(d, io, gt, c, smem, bc, red); cls = 2; break;
       case M_CSEED:
-#ifdef GC_CSEED_BLOCK
         for (int j = 0; j < gcnt; ++j) {
           if (j) __syncthreads();
           task_cseed<K>(d, io, gt + j, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, red, bc);
         }
-#else
-        task_cseed_group<K>(d, io, gt, gcnt, smem, red, bc);
-#endif
         cls = 4;
         break;
       case M_CLOS:
