@@ -49,6 +49,8 @@ struct Ctl {
   long long max_tasks;       // watchdog: tasks per launch before GC_ERR_NOCONV
   int vis_budget;            // push tasks per push phase
   int stall;                 // push tasks without progress before the phase drains
+  int bndsh;                 // relabel distance bound 2 + 2^(1 + bndsh x attempts)
+  int wavesh;                // push height cap: lowest active + 2^(wavesh x attempts)
   int stallx;                // the stall bound doubles with every failed certificate attempt
                              // beyond the first stallx (hard frames: long transport)
   int wave;                  // push phase starts on active tiles with min height <= lowest + wave
@@ -860,7 +862,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     // frame only the excess next to the object boundary has anywhere to go, and the closure
     // certificate proves the rest trapped.  The cap doubles with every failed attempt.
     const int cepn = __ldcg(d.cep + s);
-    const long long capw = cepn == 0 ? (long long)c.wave : (long long)max(c.wave, 1) << min(cepn, 20);
+    const long long capw = cepn == 0 ? (long long)c.wave : (long long)max(c.wave, 1) << min(cepn * c.wavesh, 20);
     const int hcap = md == M_BFS ? (int)min((long long)min(HINF - 1, __ldcg(d.fbnd + s)), (long long)bc[6] + capw)
                                  : HINF - 1;
     if (t == 0) {
@@ -945,7 +947,8 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (nm == M_SEED) {  // a new global relabel, bounded: distances up to 2 + 2^(attempts+1)
         d.fbe[s] += 1;     // (HINF once that exceeds any distance in the frame)
         const int ce = d.cep[s];
-        d.fbnd[s] = (ce >= 24 || (2ll << ce) >= d.hmax) ? HINF : 2 + (2 << ce);
+        const int sh = min(ce * c.bndsh, 30);
+        d.fbnd[s] = (sh >= 24 || (2ll << sh) >= d.hmax) ? HINF : 2 + (2 << sh);
       }
       bc[3] = d.fbe[s];
       d.fmode[s] = nm;
