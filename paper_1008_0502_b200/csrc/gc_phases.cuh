@@ -944,7 +944,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           }
         }
       }
-      if (nm == M_SEED) {  // a new global relabel, bounded: distances up to 2 + 2^(attempts+1)
+      if (nm == M_SEED) {  // a new global relabel, bounded: distances up to 2 + 2^(bndsh x attempts + 1)
         d.fbe[s] += 1;     // (HINF once that exceeds any distance in the frame)
         const int ce = d.cep[s];
         const int sh = min(ce * c.bndsh, 30);
