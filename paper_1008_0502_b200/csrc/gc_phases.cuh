@@ -1201,13 +1201,16 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
 }
 
 // Initial slot assignment: slot s holds frame s in M_INIT, every init tile group of every
-// slot queued.
+// slot queued -- on the chain ring: nothing else is queued yet, and a call whose frames all
+// fit the slots (no refills) then never uses the init ring, whose non-blocking claim lets
+// idle CTAs overshoot it (C3 sequence steps of 8 VGA frames: 4x slower with the initial
+// groups on the init ring).
 __global__ void k_setup(Dev d, int nframes) {
   const int G = (d.T + d.initg - 1) / d.initg;  // init tasks per frame
   const size_t ntask = (size_t)d.nslot * G;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ntask; i += (size_t)gridDim.x * blockDim.x) {
     const size_t s = i / G, g = i - s * G;
-    d.qi[i] = qent(M_INIT, s * d.T + g * d.initg);
+    d.q[i] = qent(M_INIT, s * d.T + g * d.initg);
     if (g == 0) {
       d.sfr[s] = (int)s;
       d.fmode[s] = M_INIT;
@@ -1215,7 +1218,7 @@ __global__ void k_setup(Dev d, int nframes) {
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *d.qitail = ntask;
+    *d.qtail = ntask;
     d.gctr[0] = d.nslot;
   }
 }
