@@ -68,7 +68,7 @@ typedef struct {
   int max_h, max_w;      /* largest frame the context will accept (default 1080 x 1920)  */
   int max_batch;         /* frames solved concurrently per device pass (default: as many
                             as a scratch budget of min(8 GB, 1/16 device memory) holds) */
-  int rounds_per_launch; /* push/relabel rounds inside a tile per push task (default 8)  */
+  int rounds_per_launch; /* push/relabel rounds inside a tile per push task (default 16) */
   int relabel_period;    /* reserved (global relabels follow Goldberg's heuristic)       */
   long long max_launches;/* watchdog: a call may run max_launches x (tiles in flight) tile
                             tasks; exceeded -> GC_ERR_NOCONV (default 1,000,000)          */

@@ -938,9 +938,14 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         } else {
           nm = M_IDLE;
           kind = SET_NONE;
-          if (nf == c.nframes) {  // no init group will be queued any more: release every CTA
-            const unsigned long long p0 = atomicAdd(d.qitail, (unsigned long long)gridDim.x);  // parked on qi
-            for (unsigned i = 0; i < gridDim.x; ++i) qi_put(d, p0 + i, QNOP);
+          if (nf == c.nframes) {  // no init group will be queued any more: release the CTAs
+            // parked on the init ring (tickets beyond its tail), one no-op entry each
+            const unsigned long long ih = atomicAdd(d.qihead, 0ULL), it = atomicAdd(d.qitail, 0ULL);
+            const unsigned parked = ih > it ? (unsigned)min(ih - it, (unsigned long long)gridDim.x) : 0u;
+            if (parked) {
+              const unsigned long long p0 = atomicAdd(d.qitail, (unsigned long long)parked);
+              for (unsigned i = 0; i < parked; ++i) qi_put(d, p0 + i, QNOP);
+            }
           }
         }
       }

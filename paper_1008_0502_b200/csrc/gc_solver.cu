@@ -387,7 +387,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (c->K != 4 && c->K != 8) { delete c; return GC_ERR_ARG; }
   c->max_h = g.max_h > 0 ? g.max_h : 1080;
   c->max_w = g.max_w > 0 ? g.max_w : 1920;
-  c->rounds = g.rounds_per_launch > 0 ? g.rounds_per_launch : 8;
+  c->rounds = g.rounds_per_launch > 0 ? g.rounds_per_launch : 16;  // 8 -> 16: 4K serpentine 3.8 -> 3.4 s, typical frames unchanged
   c->period = g.relabel_period > 0 ? g.relabel_period : 2;
   c->max_launches = g.max_launches > 0 ? g.max_launches : 1000000;
   c->max_batch = g.max_batch > 0 ? g.max_batch : 0;

@@ -18,7 +18,7 @@ for spec in sys.argv[1:]:
     synth.set_serpentine_params(lane=int(lane or 64), big=1 << 20)
     cs, ct, nb = synth.gen_torch("serpentine", synth.BASE_SEED + 4, 0, n, H, W, 4)
     synth.set_serpentine_params()
-    g = gc.GridCut(neighborhood=4, max_h=H, max_w=W)
+    g = gc.GridCut(neighborhood=4, max_h=H, max_w=W, rounds_per_launch=int(os.environ.get("ROUNDS", "0")))
     g.set_profiling(True)
     torch.cuda.synchronize()
     t0 = time.time()
