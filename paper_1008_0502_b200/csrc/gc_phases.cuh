@@ -160,6 +160,31 @@ __device__ __forceinline__ void absorb_pixelwise(const Dev& d, const IO& io, siz
   }
 }
 
+// Halo ring entry t (t < 132: 4 sides x 32, then the corners NW NE SW SE) of tile (ty, tx):
+// the neighbour's border height (HINF off-frame), its hidx position and its side bit.
+__device__ __forceinline__ int halo_candidate(const Dev& d, int s, int ty, int tx, int t, int& pos, int& bit) {
+  int nty = ty, ntx = tx, hi;
+  if (t < 128) {
+    const int side = t >> 5, i = t & 31;
+    int esd;
+    if (side == 0) { nty = ty - 1; esd = 1; pos = hidx(-1, i); bit = 0; }
+    else if (side == 1) { nty = ty + 1; esd = 0; pos = hidx(32, i); bit = 1; }
+    else if (side == 2) { ntx = tx - 1; esd = 3; pos = hidx(i, -1); bit = 2; }
+    else { ntx = tx + 1; esd = 2; pos = hidx(i, 32); bit = 3; }
+    hi = esd * 32 + i;
+  } else {
+    const int c = t - 128;
+    const int dy = (c < 2) ? -1 : 1, dx = (c & 1) ? 1 : -1;
+    bit = dy < 0 ? (dx < 0 ? 4 : 5) : (dx < 0 ? 6 : 7);
+    nty = ty + dy;
+    ntx = tx + dx;
+    pos = hidx(dy < 0 ? -1 : 32, dx < 0 ? -1 : 32);
+    hi = (dy < 0 ? 1 : 0) * 32 + (dx < 0 ? 31 : 0);
+  }
+  if (nty < 0 || nty >= d.TY || ntx < 0 || ntx >= d.TX) return HINF;
+  return d.hedge[((size_t)s * d.T + nty * d.TX + ntx) * 128 + hi];
+}
+
 // ---------------------------------------------------------------- a2: seed (one tile)
 // Absorbs flow still in flight from the push phase (materialising e, r pixel at a time),
 // seeds h = 1 where the node has residual capacity to t, relaxes to the tile-local
@@ -180,14 +205,10 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   __syncthreads();
   const int rcv = bc[0];
   if (bc[2] && !rcv) return;  // untouched uniform sink tile: h = 1, hedge published
-  int fl[4];
-  if (rcv) absorb_pixelwise<K>(d, io, gt, fl, hs + 2048);
-  else {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
-  }
   // halo: the border heights of the neighbours whose seed was skipped in this relabel
-  // (uniform sink tiles: final), INF elsewhere -- the BFS phase brings in the others
+  // (uniform sink tiles: final), INF elsewhere -- the BFS phase brings in the others.  The
+  // candidates of every side are loaded together with the skip stamps and the fl words
+  // (one round trip) and selected after the barrier.
   const int tile_ = (int)(gt - (size_t)s * d.T);
   const int ty_ = tile_ / d.TX, tx_ = tile_ - ty_ * d.TX;
   if (t < 8) {
@@ -195,9 +216,16 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
     const int ok = n >= 0 && !(t >= 4 && K == 4) && __ldcg(d.tsk + n) == bc[6];
     if (ok) atomicOr(&bc[7], 1 << t);
   }
-  for (int i = t; i < HS * HS; i += NTH) hs[i] = HINF;
+  int hpos = 0, hbit = 0, hval = HINF;
+  if (t < 132) hval = halo_candidate(d, s, ty_, tx_, t, hpos, hbit);
+  int fl[4];
+  if (rcv) absorb_pixelwise<K>(d, io, gt, fl, hs + 2048);
+  else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
+  }
   __syncthreads();
-  load_halo_sides(d, s, ty_, tx_, hs, t, bc[7]);
+  if (t < 132) hs[hpos] = ((bc[7] >> hbit) & 1) ? hval : HINF;
   int h[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -388,22 +416,32 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)((unsigned)gt / (unsigned)d.T);
   if (t == 0) {
-    bc[0] = __ldcg(d.recv1 + gt);
+    // every word at once (independent loads, one round trip)
+    const int r1 = __ldcg(d.recv1 + gt), fe = __ldcg(d.ferr + s), cf = __ldcg(d.cfail + s);
+    const int tu = __ldcg(d.tuni + gt), mt = __ldcg(d.mat + gt), tm = __ldcg(d.tmk + gt);
+    const int cp = __ldcg(d.cep + s);
+    bc[0] = r1;
     // range error (mask stays 0, F = -1), the attempt already failed, or (a tile of the
     // group outside the task set) an untouched uniform sink tile that never had closure pixels
-    bc[2] = __ldcg(d.ferr + s) || __ldcg(d.cfail + s) > 0 ||
-            (__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt) && !bc[0] && __ldcg(d.tmk + gt) == 0);
+    bc[2] = (fe != 0) | (cf > 0) | ((tu != 0) & (mt == 0) & (r1 == 0) & (tm == 0));
+    bc[3] = mt | r1;
+    bc[4] = cp % 255 + 1;  // closure epoch (closure_epoch)
   }
   __syncthreads();
   if (bc[2]) return;
+  uint16_t* flh = reinterpret_cast<uint16_t*>(ms + 12288);  // the neighbours' border fl words
+  {
+    const int tile = (int)(gt - (size_t)s * d.T);
+    load_fl_halo(d, s, tile / d.TX, tile % d.TX, flh, t);  // issued with the tile's own loads
+  }
   int fl[4];
   if (bc[0]) absorb_pixelwise<K>(d, io, gt, fl, reinterpret_cast<int*>(ms) + 2048);
   else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
   }
-  const int ep = closure_epoch(d, s);
-  const int mat = bc[0] ? 1 : d.mat[gt];
+  const int ep = bc[4];
+  const int mat = bc[3];
   int mm[4];
   long long neg = 0;
 #pragma unroll
@@ -436,12 +474,6 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
     const int all[4] = {1, 1, 1, 1};
     mask_write(d, io, gt, mm, all);
   }
-  uint16_t* flh = reinterpret_cast<uint16_t*>(ms + 12288);  // the neighbours' border fl words
-  {
-    const int tile = (int)(gt - (size_t)s * d.T);
-    load_fl_halo(d, s, tile / d.TX, tile % d.TX, flh, t);
-  }
-  __syncthreads();
   const int sides = block_or_bits(closure_send<K>(d, gt, mm, os, ep, flh), bc);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
@@ -590,20 +622,24 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   if (t == 0) {
     // phase budget spent or no progress lately: the frame drains to the next global relabel
+    // (every word loaded at once: independent loads, one round trip)
     const int vis = __ldcg(d.fvis + s);
     const int cep = __ldcg(d.cep + s);  // failed certificate attempts: longer phases
-    const bool cond = ((long long)__ldcg(d.frel + s) > (c.relabel_budget << min(cep, 10))) || (vis >= c.vis_budget) ||
-                      (vis - __ldcg(d.fprog + s) > (c.stall << min(max(cep - c.stallx, 0), 24)));
-    bc[0] = cond || __ldcg(d.fdrain + s);
+    const long long rel = (long long)__ldcg(d.frel + s);
+    const int prg = __ldcg(d.fprog + s), drn = __ldcg(d.fdrain + s);
+    const int tu = __ldcg(d.tuni + gt), cap = __ldcg(d.fcap + s);
+    const bool cond = (rel > (c.relabel_budget << min(cep, 10))) | (vis >= c.vis_budget) |
+                      (vis - prg > (c.stall << min(max(cep - c.stallx, 0), 24)));
+    bc[0] = cond | (drn != 0);
     if (cond) d.fdrain[s] = 1;  // no more requests in this phase
     bc[1] = 0;
     // inbound flow: take the flag (acquire: the senders set it after their counters)
     bc[2] = bc[0] ? 0 : atomicExch(&d.recv1[gt], 0);
     fence_gpu();
     bc[3] = 0;
-    bc[4] = __ldcg(d.tuni + gt);
+    bc[4] = tu;
     bc[5] = HINF;
-    bc[7] = __ldcg(d.fcap + s);  // pixels higher than this are frozen in this phase
+    bc[7] = cap;  // pixels higher than this are frozen in this phase
   }
   __syncthreads();
   if (bc[0]) {
