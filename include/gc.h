@@ -91,7 +91,10 @@ typedef struct {
                                 any int32 values are accepted and the result is unchanged */
   int64_t* flow_out;         /* [n] max-flow value of the graph as given                   */
   uint8_t* mask_out;         /* [n][H][W] 1 iff reachable from s in the final residual     */
-  int32_t* flow_state_out;   /* NULL, or [n][K/2][H][W]: this solve's forward-arc flows    */
+  int32_t* flow_state_out;   /* NULL, or [n][K/2][H][W]: this solve's forward-arc flows
+                                (n-link flows of the final maximum preflow; 0 on off-grid
+                                arcs; F = sum c(v,t) - sum max(0, -e) holds; unspecified for a
+                                frame that reports GC_ERR_RANGE)                           */
   int32_t* stats_out;        /* NULL, or [n][4]: push tile tasks, global relabels, BFS relax
                                 tile tasks, status (gc_status of the frame)                */
 } gc_batch;

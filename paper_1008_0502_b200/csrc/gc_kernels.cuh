@@ -671,7 +671,7 @@ struct InitPart {
   int fl[NTH / 32];         // bit 0: capacity out of range, bit 1: not a uniform sink tile
 };
 
-template <int K, bool WARM>
+template <int K, bool WARM, bool EXPORT>
 __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_t gt, const FramePtrs& P,
                                                const int (&a)[4], const int (&b)[4], const int (&c)[K][4],
                                                InitPart* part) {
@@ -708,6 +708,9 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
       acc |= a[i] | b[i];
       int ev = a[i] - b[i];  // a1: pre-cancel min(cs,ct) straight s -> v -> t
       sct += b[i];
+      int fw[K / 2];  // forward-arc flows as initialised (0 cold, the clamped warm flow)
+#pragma unroll
+      for (int k = 0; k < K / 2; ++k) fw[k] = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int on = (vm >> k) & 1;
@@ -722,6 +725,7 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
             const int fv = max(-cq, min(ck, __ldg(wf + (k >> 1) * plane + o0 + i)));
             rk = ck - fv;
             ev -= fv;
+            fw[k >> 1] = fv;
           } else {
             const int fv = max(-ck, min(cq, __ldg(wf + ((k ^ 1) >> 1) * plane + oq)));
             rk = ck + fv;
@@ -733,6 +737,11 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
       f |= (ev > 0 ? FL_POS : 0) | (ev < 0 ? FL_NEG : 0);
       neg += ev < 0 ? -(long long)ev : 0;
       uni &= ev < 0;
+      if (EXPORT) {  // a5: the export of a tile no push ever touches is its initial flow
+        int32_t* fo = io.fstate + fr * plane * (K / 2) + o0 + i;
+#pragma unroll
+        for (int k = 0; k < K / 2; ++k) fo[k * plane] = fw[k];
+      }
     }
     fl4[i] = f;
   }
@@ -874,15 +883,18 @@ __device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, b
         const int tile = tile0 + i + 1;
         init_prefetch<K>(d, P, tile / d.TX, tile % d.TX, pf);
       }
-      tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, part + i);
+      if (io.fstate) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
+      else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i);
     }
   } else {
 #pragma unroll 1
     for (int i = 0; i < n; ++i) {
       const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
       init_load<K>(d, P, ty, tx, vec, a, b, c);
-      if (P.wf) tile_init_regs<K, true>(d, io, gt0 + i, P, a, b, c, part + i);
-      else tile_init_regs<K, false>(d, io, gt0 + i, P, a, b, c, part + i);
+      if (P.wf && io.fstate) tile_init_regs<K, true, true>(d, io, gt0 + i, P, a, b, c, part + i);
+      else if (P.wf) tile_init_regs<K, true, false>(d, io, gt0 + i, P, a, b, c, part + i);
+      else if (io.fstate) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
+      else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i);
     }
   }
   __syncthreads();

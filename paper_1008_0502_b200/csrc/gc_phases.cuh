@@ -20,7 +20,8 @@
 //               mask and the termination certificate), written to the caller's mask   (a4)
 //   M_CLOS   -- closure across tile borders until nothing changes; reaching a node with
 //               e < 0 fails the attempt (-> M_SEED), else the frame is solved          (a4)
-//   M_EXPORT -- all tiles: forward-arc flows for the caller's warm-start state         (a5)
+//   M_EXPORT -- tiles a push touched: forward-arc flows for the caller's warm-start state
+//               (the init pass exports every other tile's initial flow)                (a5)
 //   then the flow value is written and the slot takes the next frame (M_INIT) or idles.
 //
 // Scheduling.  A ring of tile ids with ticket counters (qhead, qtail).  Per frame, fout
@@ -852,7 +853,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
 // first task set of a phase: NONE = the slot idles; EMPTY = no task (the next transition
 // follows at once)
 enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_CSEED = 5, SET_EMPTY = 6,
-       SET_INITG = 8 };
+       SET_INITG = 8, SET_MAT = 9 };
 
 __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
   const int f = d.sfr[s];
@@ -953,7 +954,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           kind = SET_FLAG;
         } else {  // certified: the mask is written
           d.cfail[s] = 0;
-          if (io.fstate && !d.ferr[s]) nm = M_EXPORT;
+          if (io.fstate && !d.ferr[s]) { nm = M_EXPORT; kind = SET_MAT; }
           else finished = true;
         }
       } else if (md == M_EXPORT) {
@@ -1007,6 +1008,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (i < d.T) {
         const size_t gt = base_gt + i;
         if (kind == SET_ALL) want = 1;
+        else if (kind == SET_MAT) want = __ldcg(d.mat + gt);  // others: exported by the init pass
         else if (kind == SET_INITG) want = (i % d.initg) == 0;  // one init task per tile group
         else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1
           want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));
