@@ -79,7 +79,7 @@ struct Dev {
   int32_t* tsk;     // [NS]   global relabel (fbe) in which the tile's seed was skipped (its
                     //        border heights, all 1 in frame, are final for that relabel)
   // per frame slot (state machine): zero-initialised by one memset
-  int32_t* fmode;   // [nslot] M_INIT, M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_EXPORT, M_IDLE
+  int32_t* fmode;   // [nslot] M_INIT, M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_IDLE
   int32_t* sfr;     // [nslot] batch frame index held by the slot
   int32_t* fout;    // [nslot] tasks of the running phase queued or running
   int32_t* gctr;    // [4] next frame to start, frames finished, range-error frames, -
@@ -117,7 +117,7 @@ struct Dev {
   unsigned long long* pdbg;    // [16] development counters (profiling only)
 };
 
-enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_EXPORT = 7, M_IDLE = 8 };
+enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_IDLE = 8 };
 
 struct IO {
   const int32_t* cs;

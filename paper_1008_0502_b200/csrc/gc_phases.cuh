@@ -20,8 +20,8 @@
 //               mask and the termination certificate), written to the caller's mask   (a4)
 //   M_CLOS   -- closure across tile borders until nothing changes; reaching a node with
 //               e < 0 fails the attempt (-> M_SEED), else the frame is solved          (a4)
-//   M_EXPORT -- tiles a push touched: forward-arc flows for the caller's warm-start state
-//               (the init pass exports every other tile's initial flow)                (a5)
+//   (a5, the caller's warm-start state: the init pass writes every tile's initial flow to
+//    flow_state_out, the closure seed of a tile a push touched its current one)
 //   then the flow value is written and the slot takes the next frame (M_INIT) or idles.
 //
 // Scheduling.  A ring of tile ids with ticket counters (qhead, qtail).  Per frame, fout
@@ -407,6 +407,9 @@ __device__ __forceinline__ void mask_write(const Dev& d, const IO& io, size_t gt
   }
 }
 
+template <int K>
+__device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t gt);
+
 // ---------------------------------------------------------------- a4: closure seed (one tile)
 // Absorbs flow still in flight, closes {e > 0} inside the tile, writes the tile's m,
 // marks reach across the border (flagging the receivers for the closure phase), checks the
@@ -493,6 +496,10 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
     if (fail) atomicAdd(&d.cfail[s], 2);  // cfail: 0 / -1 (after the BFS certificate) + 2 per failure
   }
   flag_sides(d, gt, sides, K);
+  // a5: a tile a push touched exports its forward-arc flows here (the init pass wrote every
+  // other tile's); a failed attempt's export is rewritten by the next attempt, which
+  // closure-seeds every materialised tile again
+  if (io.fstate && mat) task_export<K>(d, io, gt);
 }
 
 // ---------------------------------------------------------------- a4: closure relax (one tile)
@@ -853,7 +860,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
 // first task set of a phase: NONE = the slot idles; EMPTY = no task (the next transition
 // follows at once)
 enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_CSEED = 5, SET_EMPTY = 6,
-       SET_INITG = 8, SET_MAT = 9 };
+       SET_INITG = 8 };
 
 __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
   const int f = d.sfr[s];
@@ -954,11 +961,8 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           kind = SET_FLAG;
         } else {  // certified: the mask is written
           d.cfail[s] = 0;
-          if (io.fstate && !d.ferr[s]) { nm = M_EXPORT; kind = SET_MAT; }
-          else finished = true;
+          finished = true;  // (flow_state_out is written by the init pass and the closure seeds)
         }
-      } else if (md == M_EXPORT) {
-        finished = true;
       }
       if (finished) {
         finish_frame(d, io, s, c);
@@ -1008,7 +1012,6 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (i < d.T) {
         const size_t gt = base_gt + i;
         if (kind == SET_ALL) want = 1;
-        else if (kind == SET_MAT) want = __ldcg(d.mat + gt);  // others: exported by the init pass
         else if (kind == SET_INITG) want = (i % d.initg) == 0;  // one init task per tile group
         else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1
           want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));
@@ -1178,7 +1181,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
         task_crelax<K>(d, io, gt, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, bc);
         cls = 4;
         break;
-      default: task_export<K>(d, io, gt); cls = 5; break;
+      default: break;  // (no other task kinds)
     }
     // release this task's writes, then request the neighbour tiles it changed.  One
     // continuation stays in this CTA (next_s): the tile itself if it must run again, else
