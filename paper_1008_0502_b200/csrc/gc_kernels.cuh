@@ -852,7 +852,7 @@ constexpr size_t init_smem_bytes() {
 }
 
 template <int K>
-__device__ __noinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, int* smem) {
+__device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, int* smem) {
   const int s = (int)((unsigned)gt0 / (unsigned)d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
   const int n = min(d.initg, d.T - tile0);
   const FramePtrs P = frame_ptrs(d, io, s, K);

@@ -1074,7 +1074,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
 
 // ---------------------------------------------------------------- the persistent kernel
 template <int K>
-__global__ void __launch_bounds__(NTH, GC_MINB) k_solve(Dev d, IO io, Ctl c) {
+__global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ Dev d, const __grid_constant__ IO io, const __grid_constant__ Ctl c) {
   extern __shared__ __align__(16) int smem[];
   __shared__ int bc[8];
   __shared__ long long red[NTH / 32];
