@@ -52,6 +52,9 @@ struct gc_ctx {
   // host-API staging (device)
   char* stage = nullptr;
   size_t stage_bytes = 0;
+  cudaStream_t copy_st = nullptr;                  // H2D of the next chunk, overlapped with the solve
+  cudaEvent_t ev_in[2] = {nullptr, nullptr};       // staging buffer b filled
+  cudaEvent_t ev_free[2] = {nullptr, nullptr};     // staging buffer b solved and read back
   size_t words_bytes = 0;
 };
 
@@ -439,6 +442,11 @@ void gc_destroy(gc_ctx* c) {
   for (auto ev : c->evpool) cudaEventDestroy(ev);
   if (c->pool) cudaFree(c->pool);
   if (c->stage) cudaFree(c->stage);
+  for (int b = 0; b < 2; ++b) {
+    if (c->ev_in[b]) cudaEventDestroy(c->ev_in[b]);
+    if (c->ev_free[b]) cudaEventDestroy(c->ev_free[b]);
+  }
+  if (c->copy_st) cudaStreamDestroy(c->copy_st);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->habort) cudaFreeHost(c->habort);
   if (c->dtiles) cudaFree(c->dtiles);
@@ -514,7 +522,13 @@ gc_status gc_solve_batch_host(gc_ctx* c, const gc_batch* b, void* stream) {
   // staging: caps (2+K planes), warm (K/2), flow state (K/2), mask (1 B), flow (8 B), stats
   const size_t per = plane * 4 * (2 + K) + (b->warm_flow ? plane * 4 * (K / 2) : 0) +
                      (b->flow_state_out ? plane * 4 * (K / 2) : 0) + plane + 8 + 16 + 4 * 256;
-  const size_t need = per * chunk;
+  // Two staging buffers when the batch spans several chunks: the H2D copy of chunk i+1 runs on
+  // copy_st while chunk i is solved on `st` (solve_chunk blocks the host, so the copy is
+  // enqueued before it); the D2H read-back of chunk i follows its solve on `st`.
+  const int nchunks = (b->n + chunk - 1) / chunk;
+  const int nbuf = nchunks > 1 ? 2 : 1;
+  const size_t half = align_up(per * chunk, 256);
+  const size_t need = half * nbuf;
   if (need > c->stage_bytes) {
     if (c->stage) cudaFree(c->stage);
     c->stage = nullptr;
@@ -522,36 +536,70 @@ gc_status gc_solve_batch_host(gc_ctx* c, const gc_batch* b, void* stream) {
     if (cudaMalloc(&c->stage, need) != cudaSuccess) { cudaGetLastError(); c->err = "staging alloc"; return GC_ERR_OOM; }
     c->stage_bytes = need;
   }
+  if (!c->copy_st) {
+    if (!ck(c, cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking), "copy stream")) return GC_ERR_CUDA;
+    for (int k = 0; k < 2; ++k) {
+      if (!ck(c, cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming), "event") ||
+          !ck(c, cudaEventCreateWithFlags(&c->ev_free[k], cudaEventDisableTiming), "event"))
+        return GC_ERR_CUDA;
+    }
+  }
+  struct Stage {
+    int32_t *cs, *ct, *nb, *wf, *fs, *st;
+    uint8_t* mask;
+    int64_t* flow;
+  };
+  auto stage_of = [&](int i) {
+    const int f0 = i * chunk, m = b->n - f0 < chunk ? b->n - f0 : chunk;
+    char* p = c->stage + (size_t)(i % nbuf) * half;
+    auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
+    Stage s;
+    s.cs = (int32_t*)take(m * plane * 4);
+    s.ct = (int32_t*)take(m * plane * 4);
+    s.nb = (int32_t*)take(m * plane * 4 * K);
+    s.wf = b->warm_flow ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
+    s.fs = b->flow_state_out ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
+    s.mask = (uint8_t*)take(m * plane);
+    s.flow = (int64_t*)take(m * 8);
+    s.st = (int32_t*)take(m * 16);
+    return s;
+  };
+  auto upload = [&](int i) {  // H2D of chunk i on copy_st, once its buffer's previous chunk is read back
+    const int f0 = i * chunk, m = b->n - f0 < chunk ? b->n - f0 : chunk, k = i % nbuf;
+    const Stage s = stage_of(i);
+    cudaStream_t cs = c->copy_st;
+    if (i >= nbuf) cudaStreamWaitEvent(cs, c->ev_free[k], 0);
+    cudaMemcpyAsync(s.cs, b->cap_s + f0 * plane, m * plane * 4, cudaMemcpyHostToDevice, cs);
+    cudaMemcpyAsync(s.ct, b->cap_t + f0 * plane, m * plane * 4, cudaMemcpyHostToDevice, cs);
+    cudaMemcpyAsync(s.nb, b->cap_nb + f0 * plane * K, m * plane * 4 * K, cudaMemcpyHostToDevice, cs);
+    if (s.wf)
+      cudaMemcpyAsync(s.wf, b->warm_flow + f0 * plane * (K / 2), m * plane * 4 * (K / 2), cudaMemcpyHostToDevice, cs);
+    cudaEventRecord(c->ev_in[k], cs);
+  };
   gc_status res = GC_OK;
   Launcher L{c, st};
-  for (int f0 = 0; f0 < b->n; f0 += chunk) {
-    const int m = b->n - f0 < chunk ? b->n - f0 : chunk;
-    char* p = c->stage;
-    auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
-    int32_t* dcs = (int32_t*)take(m * plane * 4);
-    int32_t* dct = (int32_t*)take(m * plane * 4);
-    int32_t* dnb = (int32_t*)take(m * plane * 4 * K);
-    int32_t* dwf = b->warm_flow ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
-    int32_t* dfs = b->flow_state_out ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
-    uint8_t* dmask = (uint8_t*)take(m * plane);
-    int64_t* dflow = (int64_t*)take(m * 8);
-    int32_t* dstats = (int32_t*)take(m * 16);
-    cudaMemcpyAsync(dcs, b->cap_s + f0 * plane, m * plane * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dct, b->cap_t + f0 * plane, m * plane * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dnb, b->cap_nb + f0 * plane * K, m * plane * 4 * K, cudaMemcpyHostToDevice, st);
-    if (dwf)
-      cudaMemcpyAsync(dwf, b->warm_flow + f0 * plane * (K / 2), m * plane * 4 * (K / 2), cudaMemcpyHostToDevice, st);
-    IO io{dcs, dct, dnb, dwf, dflow, dmask, dfs, dstats};
+  // copy_st starts after the work already on the caller's stream (a previous call's staging use)
+  cudaEventRecord(c->ev_free[0], st);
+  cudaStreamWaitEvent(c->copy_st, c->ev_free[0], 0);
+  if (nchunks > 0) upload(0);
+  for (int i = 0; i < nchunks; ++i) {
+    const int f0 = i * chunk, m = b->n - f0 < chunk ? b->n - f0 : chunk, k = i % nbuf;
+    if (i + 1 < nchunks) upload(i + 1);
+    const Stage s = stage_of(i);
+    cudaStreamWaitEvent(st, c->ev_in[k], 0);
+    IO io{s.cs, s.ct, s.nb, s.wf, s.flow, s.mask, s.fs, s.st};
     gc_status r = (K == 8) ? solve_chunk<8>(c, io, m, H, W, st, L) : solve_chunk<4>(c, io, m, H, W, st, L);
     res = worst(res, r);
     if (r == GC_ERR_CUDA) break;
-    cudaMemcpyAsync(b->mask_out + f0 * plane, dmask, m * plane, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(b->flow_out + f0, dflow, m * 8, cudaMemcpyDeviceToHost, st);
-    if (b->stats_out) cudaMemcpyAsync(b->stats_out + f0 * 4, dstats, m * 16, cudaMemcpyDeviceToHost, st);
-    if (dfs)
-      cudaMemcpyAsync(b->flow_state_out + f0 * plane * (K / 2), dfs, m * plane * 4 * (K / 2), cudaMemcpyDeviceToHost,
+    cudaMemcpyAsync(b->mask_out + f0 * plane, s.mask, m * plane, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(b->flow_out + f0, s.flow, m * 8, cudaMemcpyDeviceToHost, st);
+    if (b->stats_out) cudaMemcpyAsync(b->stats_out + f0 * 4, s.st, m * 16, cudaMemcpyDeviceToHost, st);
+    if (s.fs)
+      cudaMemcpyAsync(b->flow_state_out + f0 * plane * (K / 2), s.fs, m * plane * 4 * (K / 2), cudaMemcpyDeviceToHost,
                       st);
+    cudaEventRecord(c->ev_free[k], st);
   }
+  if (!ck(c, cudaStreamSynchronize(c->copy_st), "host solve copies")) res = GC_ERR_CUDA;
   if (!ck(c, cudaStreamSynchronize(st), "host solve")) res = GC_ERR_CUDA;
   c->last_launches = L.n;
   if (c->prof) resolve_profile(c);

@@ -213,6 +213,25 @@ def test_host_entry_point_matches_device(torch, gc):
     assert g.launches() > 0
 
 
+def test_host_entry_point_pipelined_chunks(torch, gc, monkeypatch):
+    """Host pointers over several chunks (GC_CHUNK=2, 7 frames: 4 chunks, ragged last): the H2D
+    copy of chunk i+1 overlaps the solve of chunk i in two staging buffers. Cold and warm-started
+    (next frames, warm_flow = the previous frames' exported flow) both equal the oracle."""
+    monkeypatch.setenv("GC_CHUNK", "2")
+    n = 7
+    cs, ct, nb = synth.gen_host("blob", 11, 0, n + 1, 96, 128, 4)
+    g = solver(gc, 4)
+    F, m, fs, st = g.solve_host(cs[:n], ct[:n], nb[:n], flow_state=True, stats=True)
+    check_against_oracle(cs[:n], ct[:n], nb[:n], F, m, "bk")
+    assert (st[:, 3] == 0).all()
+    c1, t1, n1 = (np.ascontiguousarray(a[1:]) for a in (cs, ct, nb))
+    Fw, mw = g.solve_host(c1, t1, n1, warm_flow=fs)
+    Fd, md = g.solve(*to_dev(torch, c1, t1, n1))
+    np.testing.assert_array_equal(Fw, Fd.cpu().numpy())
+    np.testing.assert_array_equal(mw, md.cpu().numpy())
+    check_against_oracle(c1, t1, n1, Fw, mw, "bk", frames=[0, n - 1])
+
+
 def test_range_error(torch, gc):
     cs, ct, nb = synth.gen_host("blob", 9, 0, 3, 40, 40, 4, garbage=True)
     cs[1, 5, 5] = -1
