@@ -2,6 +2,10 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
+# make DEV=1: development build that reads the GC_* tuning knobs from the environment
+ifeq ($(DEV),1)
+NVFLAGS += -DGC_DEV_KNOBS
+endif
 PKG := paper_1008_0502_b200
 
 all: $(PKG)/libgc.so synth/libsynth.so oracle/liboracle.so

@@ -294,6 +294,31 @@ def run_warm(args, cfg):
         dist.destroy_process_group()
 
 
+def verify_shard(cfg, seed, t_first, cs, ct, nb, flow, mask, nverify, world):
+    """--verify: every frame of this rank's shard (or the first `nverify`) against the CPU oracle
+    (Boykov-Kolmogorov), bit-exact in F and mask, outside the timed region.  The caps are the
+    ones the GPU solved (the CUDA twin of synth/, bit-identical to the host twin), copied to
+    the host in chunks; the oracle runs on this rank's share of the host cores."""
+    import numpy as np
+
+    import oracle  # test infrastructure: only the verify / cpu_baseline / reference legs use it
+    n = cs.shape[0] if nverify <= 0 else min(nverify, cs.shape[0])
+    threads = max(1, host_cores() // max(world, 1))
+    chunk = max(threads, 8)
+    bad, t0 = [], time.perf_counter()
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        Fo, mo = oracle.solve_batch(cs[a:b].cpu().numpy(), ct[a:b].cpu().numpy(), nb[a:b].cpu().numpy(), "bk",
+                                    threads=threads)
+        Fg, mg = flow[a:b].cpu().numpy(), mask[a:b].cpu().numpy()
+        for i in range(b - a):
+            if int(Fg[i]) != int(Fo[i]) or not np.array_equal(mg[i], mo[i]):
+                bad.append(t_first + a + i)
+    return {"frames": n, "first_frame": t_first, "mismatches": len(bad), "bad_frames": bad[:16],
+            "oracle": "Boykov-Kolmogorov (oracle/oracle.cpp)", "threads": threads,
+            "seconds": round(time.perf_counter() - t0, 1), "compared": "F (int64) and mask bytes, every frame"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -306,11 +331,20 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-frames", type=int, default=32)
     ap.add_argument("--profile-steps", type=int, default=1)
+    ap.add_argument("--verify", type=int, default=-1, metavar="N",
+                    help="after timing, compare the first N frames of each rank's shard with the CPU oracle "
+                         "(0: all frames; default: off)")
+    ap.add_argument("--cross-check", type=int, default=8, metavar="M",
+                    help="N > 1: each rank re-solves the first M frames of the next rank's shard")
     ap.add_argument("--warm", action="store_true",
                     help="sequence mode (C3): S sequences x L frames, frame t warm-started from t-1")
     ap.add_argument("--seqs", type=int, default=8)
     ap.add_argument("--seq-len", type=int, default=120)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # no launcher: start one rank per GPU ourselves (the same env torchrun would set)
+        from paper_1008_0502_b200 import shard
+        sys.exit(shard.launch_local_ranks(args.gpus, [os.path.abspath(__file__)] + sys.argv[1:]))
     cfg = dict(CONFIGS[args.config])
     if args.frames:
         cfg["frames"] = args.frames
@@ -376,6 +410,8 @@ def main():
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev) if l2_flush else None
     launches = 0
     ms_sum = 0.0
+    g.kernel_ms(reset=True)
+    g.profile(reset=True)
     if not l2_flush:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -395,6 +431,10 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             ms_sum += e0.elapsed_time(e1)
+    # the persistent kernel's own device time in the timed steps (CUDA events the library
+    # records around every k_solve launch on the launching stream; no profiling counters on)
+    kms_timed = g.kernel_ms(reset=True)
+    nl_timed = max(g.profile(reset=True)["init"][0], 1)
     barrier()
     clocks = clk.stop()
     ms_max = shard.max_over_ranks(ms_sum, dev, world)
@@ -402,12 +442,24 @@ def main():
     value = px_total / (ms_max * 1e-3) / 1e6
     fps = world * n * args.steps / (ms_max * 1e-3)
 
-    # ---- final statistics over NCCL (the only collective: SURVEY.md §8(a) a6)
-    stats, per_frame = shard.reduce_stats(*shard.frame_stats(flow, mask), world)
+    # ---- final statistics over NCCL (the only collectives: SURVEY.md §8(a) a6, §8(e)):
+    # per-frame digests (F, popcount, 64-bit mask hash) computed on the device
+    digest = g.digest(flow, mask)
+    stats, per_frame = shard.reduce_stats(*shard.frame_stats(digest), world)
     bad_frames = int(stats[2].item())
+    cross = None
+    if world > 1 and args.cross_check > 0:
+        m = min(args.cross_check, n)
+        nxt, _ = shard.frame_range((rank + 1) % world, world, cfg["frames"])
+        pc, pt, pn = synth.gen_torch(cfg["kind"], seed, nxt, m, H, W, K, device=dev)
+        pf, pm = g.solve(pc, pt, pn)
+        pdg = g.digest(pf, pm)
+        cross = {"frames_per_rank": m, "mismatches": shard.cross_rank_mismatches(
+            digest[:m][:, [0, 2]], pdg[:, [0, 2]], world, rank),
+            "what": "rank r re-solves the first frames of rank r+1's shard; (F, mask hash) must match"}
+        del pc, pt, pn
 
-    # ---- profiled replica steps: the persistent kernel's device time (CUDA events on the
-    # launching stream) and the tile tasks of each class it ran
+    # ---- profiled replica step: tile tasks and CTA time per class (diagnostic only)
     g.set_profiling(True)
     g.profile(reset=True)
     g.kernel_ms(reset=True)
@@ -415,32 +467,45 @@ def main():
         g.solve(cs, ct, nb, out=(flow, mask))
     torch.cuda.synchronize()
     prof = g.profile(reset=True)
-    kms = g.kernel_ms(reset=True)
+    kms_prof = g.kernel_ms(reset=True)
     g.set_profiling(False)
     peak, peak_src = load_peak()
-    nl = max(prof["init"][0], 1)
-    avg_ms = kms / nl
-    bytes_launch = sum(tile_bytes(c, K) * prof[c][2] for c in prof) / nl
+    nlp = max(prof["init"][0], 1)
+
+    # ---- roofline of the dominant (only) kernel, k_solve:
+    # algorithmic bytes = compulsory bytes per pixel (read cs, ct, K n-link planes, write the
+    # mask) x pixels per launch, over the launch's unprofiled device time
+    avg_ms = kms_timed / nl_timed
+    px_launch = n * H * W * args.steps / nl_timed
+    bytes_launch = compulsory_bytes_per_px(K) * px_launch
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
-    # measured DRAM traffic (ncu dram__bytes_read + write of the same kernel, per frame,
-    # scaled to this launch's frames); null when no capture of this config is committed
-    traffic = None
+    # the kernel's own time cannot exceed the step it is part of (same stream, same steps)
+    assert kms_timed <= ms_sum * 1.001 + 0.01, (kms_timed, ms_sum)
+    # measured DRAM traffic of the benched launch (ncu dram__bytes_read + write, committed
+    # capture of this config and launch size); null when none is committed
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
             rec = json.load(open(tp)).get(args.config, {}).get("k_solve")
-            if rec:
-                traffic = int(rec["dram_bytes_per_frame"] * n / nl * args.profile_steps)
+            if rec and int(rec.get("frames_per_launch", -1)) == int(round(px_launch / (H * W))):
+                traffic = int(rec["dram_bytes_per_launch"])
+                traffic_src = rec.get("source")
         except Exception:
             traffic = None
+    task_bytes = sum(tile_bytes(c, K) * prof[c][2] for c in prof) / nlp
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": f"k_solve<{K}>",
-                "bytes_per_launch": int(bytes_launch), "avg_launch_ms": round(avg_ms, 4),
-                "launches_per_step": round(nl / args.profile_steps, 2),
-                "share_of_step": 1.0,  # the step is this one persistent kernel (+ a setup kernel)
-                "peak_source": peak_src,
-                "classes": {c: {"tiles": v[2], "cta_ms": round(v[1], 3), "bytes": tile_bytes(c, K) * v[2]}
-                            for c, v in prof.items()}}
+                "bytes_per_launch": int(bytes_launch),
+                "bytes_rule": f"{compulsory_bytes_per_px(K)} B/px compulsory (read cs, ct, {K} n-link planes as int32, "
+                              f"write the uint8 mask) x {int(px_launch)} px per launch",
+                "avg_launch_ms": round(avg_ms, 4), "launches_per_step": round(nl_timed / args.steps, 2),
+                "share_of_step": round(min(1.0, kms_timed / ms_sum), 4) if ms_sum > 0 else None,
+                "peak_source": peak_src, "traffic_source": traffic_src,
+                "task_bytes_diag": {"bytes_per_launch": int(task_bytes),
+                                    "profiled_launch_ms": round(kms_prof / nlp, 4),
+                                    "classes": {c: {"tiles": v[2], "cta_ms": round(v[1], 3),
+                                                    "bytes": tile_bytes(c, K) * v[2]} for c, v in prof.items()}}}
     comp = compulsory_bytes_per_px(K) * n * H * W * world * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with HOST buffers (pinned), copies inside timing
@@ -473,6 +538,15 @@ def main():
                "note": "gc_solve_batch_host on pinned host buffers; H2D caps + D2H mask/flow inside the timed region"}
         # results through the host path must equal the device path
         assert np.array_equal(hflow.numpy(), flow[:ne].cpu().numpy())
+        assert np.array_equal(hmask.numpy(), mask[:ne].cpu().numpy())
+
+    verify = None
+    if args.verify >= 0:
+        verify = verify_shard(cfg, seed, t_first, cs, ct, nb, flow, mask, args.verify, world)
+        if world > 1:
+            vt = torch.tensor([verify["frames"], verify["mismatches"]], dtype=torch.int64, device=dev)
+            dist.all_reduce(vt)
+            verify["frames_all_ranks"], verify["mismatches_all_ranks"] = int(vt[0]), int(vt[1])
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -496,7 +570,10 @@ def main():
                "gpu_launches": int(launches),
                "clocks": clocks,
                "frames_failed": bad_frames,
-               "checksum": {"sum_F": int(stats[0].item()), "sum_mask": int(stats[1].item())},
+               "checksum": {"sum_F": int(stats[0].item()), "sum_mask": int(stats[1].item()),
+                            "hash_xor": int(np.bitwise_xor.reduce(per_frame[:, 2].cpu().numpy()))},
+               "cross_rank": cross,
+               "verify": verify,
                "paper_context": "graph-cut stage 1.47 / 6.65 / 1.41 Mpx/s on a GeForce 9800GT (P:757-762)"}
         print(json.dumps(out), flush=True)
     if world > 1:

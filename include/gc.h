@@ -61,9 +61,11 @@ typedef enum {
 
 #define GC_CAP_MAX ((1 << 26) - 1)
 
-/* 0 in any field selects the default. */
+/* 0 in any field selects the default -- except `device`, where 0 is device 0.  A NULL
+ * config selects every default (the current device). */
 typedef struct {
-  int device;            /* CUDA device ordinal (default: current device)                */
+  int device;            /* CUDA device ordinal (0 = device 0); < 0: the calling thread's
+                            current device                                                */
   int neighborhood;      /* 4 or 8 (default 4)                                            */
   int max_h, max_w;      /* largest frame the context will accept (default 1080 x 1920)  */
   int max_batch;         /* frames solved concurrently per device pass (default: as many
@@ -106,6 +108,17 @@ gc_status gc_solve_batch(gc_ctx* ctx, const gc_batch* batch, void* stream);
  * results back, in chunks, on `stream`.  All pointers in *batch are host pointers. */
 gc_status gc_solve_batch_host(gc_ctx* ctx, const gc_batch* batch, void* stream);
 
+/* Per-frame digest of solved frames -- the statistics the frame-sharded multi-GPU path
+ * gathers: out[i] = { flow[i], popcount(mask_i), H(mask_i), 0 }
+ * with H(m) = sum over pixels p = y*W + x with m[p] != 0 of splitmix64(p + 1), mod 2^64
+ * (splitmix64: z += 0x9e3779b97f4a7c15; z = (z ^ z>>30) * 0xbf58476d1ce4e5b9;
+ * z = (z ^ z>>27) * 0x94d049bb133111eb; z ^ z>>31), stored as int64 bits.  flow [n] int64,
+ * mask [n][H][W] uint8 and out [n][4] int64 are DEVICE pointers on the context's device.
+ * GC_ERR_ARG for n < 0, H or W <= 0, or a NULL pointer with n > 0; returns after the work on
+ * `stream` completed. */
+gc_status gc_frame_digest(gc_ctx* ctx, int n, int H, int W, const int64_t* flow, const uint8_t* mask,
+                          int64_t* out, void* stream);
+
 /* Message for the last failing call on this context ("" if none).  Never NULL. */
 const char* gc_last_error(const gc_ctx* ctx);
 
@@ -125,7 +138,8 @@ void gc_set_profiling(gc_ctx* ctx, int enable);
  * group of tiles), accumulated since the last
  * reset; any pointer may be NULL; resets the counters if reset != 0. */
 void gc_get_profile(gc_ctx* ctx, long long* launches, double* ms, long long* tiles, int reset);
-/* Device time (ms, CUDA events) of the k_solve launches since the last reset (profiling on). */
+/* Device time (ms, CUDA events on the launching stream) of the k_solve launches since the
+ * last reset; always measured (launches[] of gc_get_profile counts them). */
 double gc_get_kernel_ms(gc_ctx* ctx, int reset);
 
 #ifdef __cplusplus

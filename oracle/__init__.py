@@ -94,3 +94,20 @@ def solve_batch(cs, ct, nb, algo: str = "bk", threads: int | None = None):
     lib().oracle_solve_batch(ALGOS[algo], n, H, W, K, cs.ctypes.data, ct.ctypes.data, nb.ctypes.data,
                              mask.ctypes.data, F.ctypes.data, int(threads))
     return F, mask
+
+
+def _splitmix64(z):
+    z = z + np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def mask_digest(mask):
+    """(popcount, H) of one [H,W] mask, H = sum over set pixels p = y*W + x of splitmix64(p + 1)
+    mod 2^64, returned as a signed int64 -- the digest include/gc.h documents for
+    gc_frame_digest, written out here independently (numpy) for comparing oracle masks."""
+    idx = np.flatnonzero(np.asarray(mask).reshape(-1)).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        h = _splitmix64(idx + np.uint64(1)).sum(dtype=np.uint64)
+    return int(idx.size), int(np.array(h, dtype=np.uint64).view(np.int64))

@@ -16,12 +16,11 @@ import os
 import numpy as np
 
 __all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host",
-           "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "CAP_MAX",
+           "gc_frame_digest", "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "CAP_MAX",
            "STATUS", "lib_path"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# GC_LIB_PATH: development A/B of two builds of the same library (tools/ab.sh)
-lib_path = os.environ.get("GC_LIB_PATH") or os.path.join(_HERE, "libgc.so")
+lib_path = os.path.join(_HERE, "libgc.so")
 CAP_MAX = (1 << 26) - 1
 STATUS = {0: "GC_OK", 1: "GC_ERR_ARG", 2: "GC_ERR_RANGE", 3: "GC_ERR_OOM", 4: "GC_ERR_CUDA", 5: "GC_ERR_NOCONV"}
 PROFILE_CLASSES = ("init", "bfs", "push", "sched", "closure", "export")
@@ -66,9 +65,12 @@ _lib.gc_debug_counters.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_ulon
 _lib.gc_debug_counters.restype = None
 _lib.gc_get_kernel_ms.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.gc_get_kernel_ms.restype = ctypes.c_double
+_lib.gc_frame_digest.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+_lib.gc_frame_digest.restype = ctypes.c_int
 
 EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
-            "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms")
+            "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "gc_frame_digest")
 
 
 class GcError(RuntimeError):
@@ -128,6 +130,11 @@ def gc_get_kernel_ms(ctx, reset: bool = False) -> float:
     return float(_lib.gc_get_kernel_ms(ctx, int(bool(reset))))
 
 
+def gc_frame_digest(ctx, n: int, H: int, W: int, flow: int, mask: int, out: int, stream: int) -> int:
+    return _lib.gc_frame_digest(ctx, n, H, W, ctypes.c_void_p(flow), ctypes.c_void_p(mask), ctypes.c_void_p(out),
+                                ctypes.c_void_p(stream))
+
+
 def _ptr(x):
     if x is None:
         return None
@@ -145,8 +152,10 @@ class GridCut:
     """
 
     def __init__(self, neighborhood: int = 4, max_h: int = 1080, max_w: int = 1920, max_batch: int = 0,
-                 rounds_per_launch: int = 0, relabel_period: int = 0, max_launches: int = 0, device: int = 0):
+                 rounds_per_launch: int = 0, relabel_period: int = 0, max_launches: int = 0, device: int | None = None):
         self.K = neighborhood
+        if device is None:  # the current CUDA device (gc.h: device < 0)
+            device = -1
         cfg = gc_config(device, neighborhood, max_h, max_w, max_batch, rounds_per_launch, relabel_period,
                         max_launches)
         self.ctx = gc_create(cfg)
@@ -217,6 +226,16 @@ class GridCut:
         if stats:
             res.append(stt)
         return tuple(res)
+
+    def digest(self, flow, mask, stream=None):
+        """Per-frame (F, popcount, mask hash, 0) int64 [n, 4] on the device (gc_frame_digest)."""
+        import torch
+        n, H, W = mask.shape
+        assert flow.dtype == torch.int64 and mask.dtype == torch.uint8 and mask.is_contiguous()
+        out = torch.empty((n, 4), dtype=torch.int64, device=mask.device)
+        s = torch.cuda.current_stream(mask.device).cuda_stream if stream is None else stream
+        self._check(gc_frame_digest(self.ctx, n, H, W, _ptr(flow), _ptr(mask), _ptr(out), s))
+        return out
 
     def launches(self) -> int:
         return gc_last_launches(self.ctx)

@@ -1128,13 +1128,18 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
       }
       task_s = v;
     }
-    if (t == 0 && (++ntask_local & 15) == 0) {  // watchdogs: task budget, host stop request
-      if (atomicAdd(d.ntask, 16ULL) + 16 >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
-      if ((ntask_local & 255) == 0 && *d.hostabort) *(volatile int*)&d.done[1] = 1;
+    if (t == 0) {
+      if ((++ntask_local & 15) == 0) {  // watchdogs: task budget, host stop request
+        if (atomicAdd(d.ntask, 16ULL) + 16 >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
+        if ((ntask_local & 255) == 0 && *d.hostabort) *(volatile int*)&d.done[1] = 1;
+      }
+      // the abort flag is read by thread 0 alone: every thread of the CTA then takes the
+      // same decision from task_s (a per-thread read could split the CTA at a barrier)
+      if (*(volatile int*)&d.done[1]) task_s = QEXIT;
     }
     __syncthreads();
     const uint32_t v = task_s;
-    if (v == QEXIT || *(volatile int*)&d.done[1]) break;
+    if (v == QEXIT) break;
     if (v == QNOP) {
       __syncthreads();  // every thread has read task_s before thread 0 takes the next one
       continue;
@@ -1146,6 +1151,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     const bool reqd = md == M_BFS || md == M_PUSH || md == M_CLOS;  // request-driven phase
     int c0 = 0;
     uint64_t w0 = 0;
+    __shared__ int drain_s;
     if (t == 0) {
       if (reqd) c0 = atomicAdd(&d.treq[gt], 0);
       fence_gpu();  // acquire: the writes of the task's producers
@@ -1188,13 +1194,14 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     // the first newly queued neighbour -- dependency chains (a BFS wave, flow moving
     // across tiles) then advance without a trip through the queue.
     fence_gpu();
+    if (t == 0) drain_s = md == M_PUSH && __ldcg(d.fdrain + s);  // one read: one decision per CTA
     __syncthreads();
     int rem = 0;
     if (reqd) {
       // concurrently: thread 0 settles the tile's own requests, threads 1..8 request the
       // neighbours; no requests while a push phase drains (inflow stays flagged in recv1
       // and is absorbed by the next closure seed / seed)
-      const bool drain = md == M_PUSH && __ldcg(d.fdrain + s);
+      const bool drain = drain_s != 0;
       if (t == 0) {
         if (drain) {
           atomicExch(&d.treq[gt], 0);

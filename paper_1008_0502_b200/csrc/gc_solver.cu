@@ -37,6 +37,7 @@ struct gc_ctx {
                                   // (doubled from 1 per failed certificate attempt)
   int selfrun = 0;                // 1: a push tile re-runs itself only after progress
   int grid = 0;                   // k_solve CTAs of the last launch
+  int grid_max = 0;               // persistent grid of k_solve<K> on this context's device
   std::string err;
   long long last_launches = 0;
   bool prof = false;
@@ -61,6 +62,17 @@ struct gc_ctx {
 namespace {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Development tuning knobs (environment variables), compiled in only with -DGC_DEV_KNOBS
+// (`make DEV=1`).  The product library reads no environment variable but GC_TIMEOUT_S.
+const char* knob(const char* name) {
+#ifdef GC_DEV_KNOBS
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 // Bytes of scratch per frame with T tiles.
 size_t frame_bytes(int K, size_t T) {
@@ -95,7 +107,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.nslot = nslot;
   d.hmax = d.T * TPX + 2;
   d.initg = d.T / 32 < 1 ? 1 : (d.T / 32 > 32 ? 32 : d.T / 32);
-  if (const char* ev = getenv("GC_INITG")) d.initg = atoi(ev) > 0 && atoi(ev) <= INIT_GMAX ? atoi(ev) : d.initg;
+  if (const char* ev = knob("GC_INITG")) d.initg = atoi(ev) > 0 && atoi(ev) <= INIT_GMAX ? atoi(ev) : d.initg;
   const size_t T = d.T, ns = (size_t)nslot * T, K = c->K;
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
@@ -183,8 +195,20 @@ struct Launcher {
   long long n = 0;  // kernel launches issued
 };
 
-// Profiling counters of the last solve: tasks and summed CTA time per class, plus the
-// device time of each k_solve launch (CUDA events on the launching stream).
+// Device time of every k_solve launch (CUDA events on the launching stream; always on).
+void resolve_timing(gc_ctx* c) {
+  for (auto& p : c->pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+    for (int i = 0; i < 6; ++i) c->prof_n[i] += 1;
+    c->kernel_ms += ms;
+  }
+  c->pending.clear();
+  c->evnext = 0;
+}
+
+// Profiling counters of the last solve (profiling builds of the run only): tasks and summed
+// CTA time per class.
 void resolve_profile(gc_ctx* c) {
   unsigned long long t[28];
   if (cudaMemcpy(t, c->dtiles, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
@@ -197,14 +221,6 @@ void resolve_profile(gc_ctx* c) {
     }
     cudaMemset(c->dtiles, 0, sizeof(t));
   }
-  for (auto& p : c->pending) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
-    for (int i = 0; i < 6; ++i) c->prof_n[i] += 1;
-    c->kernel_ms += ms;
-  }
-  c->pending.clear();
-  c->evnext = 0;
 }
 
 // Persistent grid size: resident CTAs per SM x SMs.
@@ -227,12 +243,12 @@ int chunk_frames(gc_ctx* c, int H, int W) {
   const size_t fb = frame_bytes(c->K, T);
   size_t n = c->pool_bytes / fb;
   size_t want = T >= 40000 / 24 ? 24 : (40000 + T - 1) / T;
-  if (const char* ev = getenv("GC_SLOTS")) want = atoi(ev) > 0 ? atoi(ev) : want;  // tuning knob
+  if (const char* ev = knob("GC_SLOTS")) want = atoi(ev) > 0 ? atoi(ev) : want;  // tuning knob
   if (n > want) n = want;
   if (n < 1) n = 1;
   if (c->max_batch > 0 && n > (size_t)c->max_batch) n = c->max_batch;
   if (n * T >= (1u << 24)) n = ((1u << 24) - 1) / T;  // queue entries hold 24-bit tile ids
-  const char* env = getenv("GC_CHUNK");
+  const char* env = knob("GC_CHUNK");
   if (env && atoi(env) > 0 && (size_t)atoi(env) < n) n = atoi(env);
   return (int)n;
 }
@@ -250,15 +266,10 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   const int nslot = chunk_frames(c, H, W) < nframes ? chunk_frames(c, H, W) : nframes;
   size_t sg_bytes = 0, q_bytes = 0;
   Dev d = carve(c, nslot, H, W, &sg_bytes, &q_bytes);
-  static int g_solve[9] = {0};
   const size_t smem = solve_smem_bytes<K>();
-  if (!g_solve[K]) {
-    cudaFuncSetAttribute(k_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    g_solve[K] = persistent_grid(c, k_solve<K>, smem);
-  }
   const size_t ns = (size_t)nslot * d.T;
-  int grid = g_solve[K];
-  if (const char* ev = getenv("GC_GRID")) grid = atoi(ev) > 0 && atoi(ev) < grid ? atoi(ev) : grid;
+  int grid = c->grid_max;  // computed per context (its device) in gc_create
+  if (const char* ev = knob("GC_GRID")) grid = atoi(ev) > 0 && atoi(ev) < grid ? atoi(ev) : grid;
   c->grid = grid;
   if (!ck(c, cudaMemsetAsync(d.fmode, 0, c->words_bytes, st), "memset")) return GC_ERR_CUDA;
   if (!ck(c, cudaMemsetAsync(d.treq, 0, sg_bytes, st), "memset")) return GC_ERR_CUDA;
@@ -274,8 +285,8 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   // (x2 per attempt: 28 -> 20 ms for C4's cold-start frame alone, same results)
   ctl.bndsh = 2;
   ctl.wavesh = 2;
-  if (const char* ev = getenv("GC_BNDSH")) ctl.bndsh = atoi(ev) > 0 ? atoi(ev) : ctl.bndsh;
-  if (const char* ev = getenv("GC_WAVESH")) ctl.wavesh = atoi(ev) > 0 ? atoi(ev) : ctl.wavesh;
+  if (const char* ev = knob("GC_BNDSH")) ctl.bndsh = atoi(ev) > 0 ? atoi(ev) : ctl.bndsh;
+  if (const char* ev = knob("GC_WAVESH")) ctl.wavesh = atoi(ev) > 0 ? atoi(ev) : ctl.wavesh;
   ctl.wave = c->wave;
   ctl.selfrun = c->selfrun;
   ctl.rounds = c->rounds;
@@ -287,25 +298,21 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   const double mt = (double)c->max_launches * (double)ns;
   ctl.max_tasks = mt > 9e18 ? (long long)9e18 : (long long)mt;
   *c->habort = 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (c->prof) {
-    if (c->evnext + 2 > c->evpool.size()) {
-      for (int i = 0; i < 16; ++i) {
-        cudaEvent_t ev;
-        cudaEventCreate(&ev);
-        c->evpool.push_back(ev);
-      }
+  // the launch's device time, always measured (gc_get_kernel_ms): two events per launch
+  if (c->evnext + 2 > c->evpool.size()) {
+    for (int i = 0; i < 16; ++i) {
+      cudaEvent_t ev;
+      if (!ck(c, cudaEventCreate(&ev), "event")) return GC_ERR_CUDA;
+      c->evpool.push_back(ev);
     }
-    e0 = c->evpool[c->evnext++];
-    e1 = c->evpool[c->evnext++];
-    cudaEventRecord(e0, st);
   }
+  cudaEvent_t e0 = c->evpool[c->evnext++];
+  cudaEvent_t e1 = c->evpool[c->evnext++];
+  cudaEventRecord(e0, st);
   k_solve<K><<<grid, NTH, smem, st>>>(d, io, ctl);
   ++L.n;
-  if (c->prof) {
-    cudaEventRecord(e1, st);
-    c->pending.push_back({0, {e0, e1}});
-  }
+  cudaEventRecord(e1, st);
+  c->pending.push_back({0, {e0, e1}});
   if (!ck(c, cudaGetLastError(), "k_solve launch")) return GC_ERR_CUDA;
   cudaMemcpyAsync(c->hpin, d.gctr, 32, cudaMemcpyDeviceToHost, st);  // gctr[4], done[4]
   // wait (spinning for the first 2 ms: small calls are latency-bound, a sleep costs ~60 us);
@@ -323,7 +330,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
     }
   }
   const bool aborted = c->hpin[5] != 0 || c->hpin[1] < nframes;
-  if (aborted && getenv("GC_DEBUG")) {  // development aid: where did each slot stop?
+  if (aborted && knob("GC_DEBUG")) {  // development aid: where did each slot stop?
     std::vector<int32_t> w(c->words_bytes / 4);
     cudaMemcpy(w.data(), d.fmode, w.size() * 4, cudaMemcpyDeviceToHost);
     const int32_t* base = w.data();
@@ -373,6 +380,46 @@ gc_status worst(gc_status a, gc_status b) {
   return a != GC_OK ? a : b;
 }
 
+// a6: per-frame digest of solved frames (gc_frame_digest): F, popcount and a 64-bit hash of
+// the mask, H(m) = sum over set pixels p of splitmix64(p + 1) mod 2^64 (order-independent, so
+// blocks reduce in any order).  grid (blocks per frame, n); out zeroed before the launch.
+__device__ __forceinline__ unsigned long long dg_mix(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_digest(size_t plane, const int64_t* flow, const uint8_t* mask, unsigned long long* out) {
+  const int f = blockIdx.y;
+  const uint8_t* m = mask + (size_t)f * plane;
+  unsigned long long pop = 0, h = 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x * 4;
+  for (size_t p = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; p < plane; p += stride) {
+    if (p + 3 < plane && (((uintptr_t)(m + p)) & 3) == 0) {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(m + p);
+      if (w) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if ((w >> (8 * i)) & 0xffu) { ++pop; h += dg_mix(p + i + 1); }
+      }
+    } else {
+      for (size_t i = p; i < p + 4 && i < plane; ++i)
+        if (m[i]) { ++pop; h += dg_mix(i + 1); }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pop += __shfl_xor_sync(0xffffffffu, pop, o);
+    h += __shfl_xor_sync(0xffffffffu, h, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (pop) atomicAdd(out + (size_t)f * 4 + 1, pop);
+    if (h) atomicAdd(out + (size_t)f * 4 + 2, h);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[(size_t)f * 4] = (unsigned long long)flow[f];
+}
+
 }  // namespace
 
 extern "C" {
@@ -384,8 +431,12 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   memset(&z, 0, sizeof(z));
   const gc_config& g = cfg ? *cfg : z;
   gc_ctx* c = new gc_ctx();
-  if (cudaGetDevice(&c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
-  if (g.device > 0) c->dev = g.device;
+  if (cfg && g.device >= 0) {
+    c->dev = g.device;  // an explicit ordinal (0 = device 0)
+  } else if (cudaGetDevice(&c->dev) != cudaSuccess) {  // device < 0 (or no config): current device
+    delete c;
+    return GC_ERR_CUDA;
+  }
   c->K = g.neighborhood ? g.neighborhood : 4;
   if (c->K != 4 && c->K != 8) { delete c; return GC_ERR_ARG; }
   c->max_h = g.max_h > 0 ? g.max_h : 1080;
@@ -394,12 +445,12 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   c->period = g.relabel_period > 0 ? g.relabel_period : 2;
   c->max_launches = g.max_launches > 0 ? g.max_launches : 1000000;
   c->max_batch = g.max_batch > 0 ? g.max_batch : 0;
-  if (const char* ev = getenv("GC_ALPHA")) c->alpha = atof(ev);          // tuning knobs
-  if (const char* ev = getenv("GC_VIS")) c->vis_mult = atoi(ev);
-  if (const char* ev = getenv("GC_STALL")) c->stall = atoi(ev);
-  if (const char* ev = getenv("GC_STALLX")) c->stallx = atoi(ev);
-  if (const char* ev = getenv("GC_WAVE")) c->wave = atoi(ev);
-  if (const char* ev = getenv("GC_SELFRUN")) c->selfrun = atoi(ev);
+  if (const char* ev = knob("GC_ALPHA")) c->alpha = atof(ev);          // tuning knobs
+  if (const char* ev = knob("GC_VIS")) c->vis_mult = atoi(ev);
+  if (const char* ev = knob("GC_STALL")) c->stall = atoi(ev);
+  if (const char* ev = knob("GC_STALLX")) c->stallx = atoi(ev);
+  if (const char* ev = knob("GC_WAVE")) c->wave = atoi(ev);
+  if (const char* ev = knob("GC_SELFRUN")) c->selfrun = atoi(ev);
   if (const char* ev = getenv("GC_TIMEOUT_S")) c->timeout_s = atof(ev);
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
   if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
@@ -415,7 +466,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
     cudaMemGetInfo(&fr, &tot);
     size_t budget = (size_t)8 << 30;
     if (tot > 0 && tot / 16 < budget) budget = tot / 16;
-    if (const char* ev = getenv("GC_SCRATCH_MB")) budget = (size_t)atoll(ev) << 20;  // tuning knob
+    if (const char* ev = knob("GC_SCRATCH_MB")) budget = (size_t)atoll(ev) << 20;  // tuning knob
     nf = budget / fb;
     if (nf < 1) nf = 1;
   }
@@ -433,6 +484,18 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
     return GC_ERR_OOM;
   }
   *c->habort = 0;
+  // persistent grid (resident CTAs per SM x SMs of this device), per context
+  {
+    const size_t smem = c->K == 8 ? solve_smem_bytes<8>() : solve_smem_bytes<4>();
+    cudaError_t e = c->K == 8 ? cudaFuncSetAttribute(k_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                              : cudaFuncSetAttribute(k_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    c->grid_max = c->K == 8 ? persistent_grid(c, k_solve<8>, smem) : persistent_grid(c, k_solve<4>, smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      gc_destroy(c);
+      return GC_ERR_CUDA;
+    }
+  }
   *out = c;
   return GC_OK;
 }
@@ -488,6 +551,26 @@ double gc_get_kernel_ms(gc_ctx* c, int reset) {
   return v;
 }
 
+gc_status gc_frame_digest(gc_ctx* c, int n, int H, int W, const int64_t* flow, const uint8_t* mask, int64_t* out,
+                          void* stream) {
+  if (!c) return GC_ERR_ARG;
+  if (n < 0 || H <= 0 || W <= 0 || (n > 0 && (!flow || !mask || !out))) {
+    c->err = "gc_frame_digest: bad arguments";
+    return GC_ERR_ARG;
+  }
+  if (n == 0) return GC_OK;
+  cudaSetDevice(c->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t plane = (size_t)H * W;
+  if (!ck(c, cudaMemsetAsync(out, 0, (size_t)n * 32, st), "digest memset")) return GC_ERR_CUDA;
+  const unsigned bx = (unsigned)((plane / 4 + 255) / 256 < 64 ? (plane / 4 + 255) / 256 + 1 : 64);
+  k_digest<<<dim3(bx, (unsigned)n), 256, 0, st>>>(plane, flow, mask, reinterpret_cast<unsigned long long*>(out));
+  if (!ck(c, cudaGetLastError(), "k_digest launch")) return GC_ERR_CUDA;
+  if (!ck(c, cudaStreamSynchronize(st), "k_digest")) return GC_ERR_CUDA;
+  c->last_launches = 1;
+  return GC_OK;
+}
+
 gc_status gc_solve_batch(gc_ctx* c, const gc_batch* b, void* stream) {
   gc_status s0 = check_batch(c, b);
   if (s0 != GC_OK) return s0;
@@ -504,6 +587,7 @@ gc_status gc_solve_batch(gc_ctx* c, const gc_batch* b, void* stream) {
   }
   (void)plane;
   c->last_launches = L.n;
+  resolve_timing(c);
   if (c->prof) resolve_profile(c);
   if (res == GC_ERR_RANGE && c->err.empty()) c->err = "capacity out of range [0, GC_CAP_MAX] in some frame";
   if (res == GC_ERR_NOCONV && c->err.empty()) c->err = "max_launches exceeded before convergence";
@@ -519,15 +603,37 @@ gc_status gc_solve_batch_host(gc_ctx* c, const gc_batch* b, void* stream) {
   const int H = b->H, W = b->W, K = c->K;
   const size_t plane = (size_t)H * W;
   int chunk = chunk_frames(c, H, W);
-  // staging: caps (2+K planes), warm (K/2), flow state (K/2), mask (1 B), flow (8 B), stats
-  const size_t per = plane * 4 * (2 + K) + (b->warm_flow ? plane * 4 * (K / 2) : 0) +
-                     (b->flow_state_out ? plane * 4 * (K / 2) : 0) + plane + 8 + 16 + 4 * 256;
+  if (chunk > b->n) chunk = b->n > 0 ? b->n : 1;
   // Two staging buffers when the batch spans several chunks: the H2D copy of chunk i+1 runs on
   // copy_st while chunk i is solved on `st` (solve_chunk blocks the host, so the copy is
   // enqueued before it); the D2H read-back of chunk i follows its solve on `st`.
   const int nchunks = (b->n + chunk - 1) / chunk;
   const int nbuf = nchunks > 1 ? 2 : 1;
-  const size_t half = align_up(per * chunk, 256);
+  struct Stage {
+    int32_t *cs, *ct, *nb, *wf, *fs, *st;
+    uint8_t* mask;
+    int64_t* flow;
+    size_t bytes;  // extent of the layout from the buffer's start
+  };
+  // one staging buffer's layout for m frames: caps (2+K planes), warm (K/2), flow state (K/2),
+  // mask (1 B), flow (8 B), stats (16 B); every sub-buffer 256-byte aligned.  The buffer size
+  // (`half`) comes from this same layout, so no sub-buffer can reach into the next buffer.
+  auto layout = [&](char* base, int m) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { char* q = base + off; off += align_up(bytes, 256); return q; };
+    Stage s;
+    s.cs = (int32_t*)take(m * plane * 4);
+    s.ct = (int32_t*)take(m * plane * 4);
+    s.nb = (int32_t*)take(m * plane * 4 * K);
+    s.wf = b->warm_flow ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
+    s.fs = b->flow_state_out ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
+    s.mask = (uint8_t*)take(m * plane);
+    s.flow = (int64_t*)take(m * 8);
+    s.st = (int32_t*)take(m * 16);
+    s.bytes = off;
+    return s;
+  };
+  const size_t half = layout(nullptr, chunk).bytes;
   const size_t need = half * nbuf;
   if (need > c->stage_bytes) {
     if (c->stage) cudaFree(c->stage);
@@ -544,25 +650,9 @@ gc_status gc_solve_batch_host(gc_ctx* c, const gc_batch* b, void* stream) {
         return GC_ERR_CUDA;
     }
   }
-  struct Stage {
-    int32_t *cs, *ct, *nb, *wf, *fs, *st;
-    uint8_t* mask;
-    int64_t* flow;
-  };
   auto stage_of = [&](int i) {
     const int f0 = i * chunk, m = b->n - f0 < chunk ? b->n - f0 : chunk;
-    char* p = c->stage + (size_t)(i % nbuf) * half;
-    auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
-    Stage s;
-    s.cs = (int32_t*)take(m * plane * 4);
-    s.ct = (int32_t*)take(m * plane * 4);
-    s.nb = (int32_t*)take(m * plane * 4 * K);
-    s.wf = b->warm_flow ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
-    s.fs = b->flow_state_out ? (int32_t*)take(m * plane * 4 * (K / 2)) : nullptr;
-    s.mask = (uint8_t*)take(m * plane);
-    s.flow = (int64_t*)take(m * 8);
-    s.st = (int32_t*)take(m * 16);
-    return s;
+    return layout(c->stage + (size_t)(i % nbuf) * half, m);
   };
   auto upload = [&](int i) {  // H2D of chunk i on copy_st, once its buffer's previous chunk is read back
     const int f0 = i * chunk, m = b->n - f0 < chunk ? b->n - f0 : chunk, k = i % nbuf;
@@ -602,6 +692,7 @@ gc_status gc_solve_batch_host(gc_ctx* c, const gc_batch* b, void* stream) {
   if (!ck(c, cudaStreamSynchronize(c->copy_st), "host solve copies")) res = GC_ERR_CUDA;
   if (!ck(c, cudaStreamSynchronize(st), "host solve")) res = GC_ERR_CUDA;
   c->last_launches = L.n;
+  resolve_timing(c);
   if (c->prof) resolve_profile(c);
   if (res == GC_ERR_RANGE && c->err.empty()) c->err = "capacity out of range [0, GC_CAP_MAX] in some frame";
   if (res == GC_ERR_NOCONV && c->err.empty()) c->err = "max_launches exceeded before convergence";

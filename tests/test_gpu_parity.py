@@ -5,12 +5,9 @@ import pytest
 
 import oracle
 import synth
+from certify import check_against_oracle, cut_cert, cut_torch, residual_closure_host
 
 pytestmark = pytest.mark.gpu
-
-DY = [0, 0, 1, -1, 1, -1, 1, -1]
-DX = [1, -1, 0, 0, 1, -1, -1, 1]
-
 
 @pytest.fixture(scope="module")
 def torch():
@@ -37,41 +34,6 @@ def solver(gc, K, max_h=1080, max_w=1920, **kw):
 
 def to_dev(torch, *arrs):
     return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrs]
-
-
-def check_against_oracle(cs, ct, nb, F, mask, algo="dinic", frames=None):
-    n = cs.shape[0]
-    idx = range(n) if frames is None else frames
-    for i in idx:
-        Fo, mo = oracle.solve(cs[i], ct[i], nb[i], algo)
-        assert int(F[i]) == Fo, f"frame {i}: F gpu {int(F[i])} oracle {Fo}"
-        if not np.array_equal(mask[i], mo):
-            bad = np.argwhere(mask[i] != mo)
-            raise AssertionError(f"frame {i}: {len(bad)} mask mismatches, first {bad[:5].tolist()}")
-
-
-def cut_cert(cs, ct, nb, f):
-    """Oracle-free certificate (SURVEY.md §8(c)): e from caps and the exported forward flow;
-    F(f) = sum ct - sum max(0,-e); returns (feasible, F(f))."""
-    K, H, W = nb.shape
-    e = cs.astype(np.int64) - ct.astype(np.int64)
-    ok = True
-    for j in range(K // 2):
-        k = 2 * j
-        fj = f[j].astype(np.int64)
-        y0, y1 = max(0, -DY[k]), H - max(0, DY[k])
-        x0, x1 = max(0, -DX[k]), W - max(0, DX[k])
-        src = fj[y0:y1, x0:x1]
-        cfw = nb[k, y0:y1, x0:x1].astype(np.int64)
-        crv = nb[k ^ 1, y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]].astype(np.int64)
-        ok &= bool(np.all(src <= cfw) and np.all(-src <= crv))
-        e[y0:y1, x0:x1] -= src
-        e[y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]] += src
-        # off-grid flows must be zero
-        full = np.zeros_like(fj, bool)
-        full[y0:y1, x0:x1] = True
-        ok &= bool(np.all(fj[~full] == 0))
-    return ok, int(ct.astype(np.int64).sum() - np.maximum(0, -e).sum())
 
 
 # ----------------------------------------------------------------------------- generator twin
@@ -213,14 +175,13 @@ def test_host_entry_point_matches_device(torch, gc):
     assert g.launches() > 0
 
 
-def test_host_entry_point_pipelined_chunks(torch, gc, monkeypatch):
-    """Host pointers over several chunks (GC_CHUNK=2, 7 frames: 4 chunks, ragged last): the H2D
+def test_host_entry_point_pipelined_chunks(torch, gc):
+    """Host pointers over several chunks (max_batch=2, 7 frames: 4 chunks, ragged last): the H2D
     copy of chunk i+1 overlaps the solve of chunk i in two staging buffers. Cold and warm-started
     (next frames, warm_flow = the previous frames' exported flow) both equal the oracle."""
-    monkeypatch.setenv("GC_CHUNK", "2")
     n = 7
     cs, ct, nb = synth.gen_host("blob", 11, 0, n + 1, 96, 128, 4)
-    g = solver(gc, 4)
+    g = solver(gc, 4, max_batch=2)
     F, m, fs, st = g.solve_host(cs[:n], ct[:n], nb[:n], flow_state=True, stats=True)
     check_against_oracle(cs[:n], ct[:n], nb[:n], F, m, "bk")
     assert (st[:, 3] == 0).all()
@@ -230,6 +191,50 @@ def test_host_entry_point_pipelined_chunks(torch, gc, monkeypatch):
     np.testing.assert_array_equal(Fw, Fd.cpu().numpy())
     np.testing.assert_array_equal(mw, md.cpu().numpy())
     check_against_oracle(c1, t1, n1, Fw, mw, "bk", frames=[0, n - 1])
+
+
+@pytest.mark.parametrize("H,W,K", [(37, 53, 4), (61, 45, 8), (100, 100, 4)])
+def test_host_entry_point_one_frame_chunks_odd_geometry(torch, gc, H, W, K):
+    """max_batch=1 (one frame per chunk, two staging buffers in turn) on geometries whose
+    sub-buffers need alignment padding, warm start in and flow state out: every sub-buffer of
+    a staging buffer lies inside it (the buffer size now comes from the same
+    layout), so results equal the device path and the oracle on every frame."""
+    n = 5
+    cs, ct, nb = synth.gen_host("blob", 21 + K, 0, n + 1, H, W, K)
+    g = solver(gc, K, 128, 128, max_batch=1)
+    F, m, fs = g.solve_host(cs[:n], ct[:n], nb[:n], flow_state=True)
+    check_against_oracle(cs[:n], ct[:n], nb[:n], F, m, "bk")
+    for i in range(n):
+        ok, Ff = cut_cert(cs[i], ct[i], nb[i], fs[i])
+        assert ok and Ff == int(F[i]), i
+    c1, t1, n1 = (np.ascontiguousarray(a[1:]) for a in (cs, ct, nb))
+    Fw, mw, fw = g.solve_host(c1, t1, n1, warm_flow=fs, flow_state=True)
+    check_against_oracle(c1, t1, n1, Fw, mw, "bk")
+    for i in range(n):
+        ok, Ff = cut_cert(c1[i], t1[i], n1[i], fw[i])
+        assert ok and Ff == int(Fw[i]), i
+
+
+def test_explicit_device_zero(torch, gc):
+    """gc_config.device = 0 selects device 0 explicitly (it is not the "default" value)."""
+    cs, ct, nb = synth.gen_host("blob", 4, 0, 2, 48, 64, 4)
+    g = gc.GridCut(neighborhood=4, max_h=64, max_w=64, device=0)
+    F, m = g.solve(*to_dev(torch, cs, ct, nb))
+    check_against_oracle(cs, ct, nb, F.cpu().numpy(), m.cpu().numpy())
+    g.close()
+
+
+def test_frame_digest_matches_oracle_masks(torch, gc):
+    """gc_frame_digest (the a6 statistics) on solved frames equals the digest of the oracle's
+    masks recomputed in numpy from include/gc.h's definition."""
+    cs, ct, nb = synth.gen_host("blob", 13, 0, 6, 70, 90, 8)
+    g = solver(gc, 8, 128, 128)
+    F, m = g.solve(*to_dev(torch, cs, ct, nb))
+    dg = g.digest(F, m).cpu().numpy()
+    Fo, mo = oracle.solve_batch(cs, ct, nb, "bk")
+    for i in range(6):
+        pop, h = oracle.mask_digest(mo[i])
+        assert (int(dg[i, 0]), int(dg[i, 1]), int(dg[i, 2]), int(dg[i, 3])) == (int(Fo[i]), pop, h, 0), i
 
 
 def test_range_error(torch, gc):
@@ -277,22 +282,6 @@ def test_two_contexts_interleaved(torch, gc):
     check_against_oracle(*c4, Fa.cpu().numpy(), ma.cpu().numpy())
     check_against_oracle(*c8, Fb.cpu().numpy(), mb.cpu().numpy())
     a.close(); b.close()
-
-
-def cut_torch(torch, cs, ct, nb, mask):
-    """cut(S) of SURVEY.md §8(c), S = mask, written out in plain PyTorch on the device:
-    sum_{v not in S} cs + sum_{v in S} ct + sum over in-grid arcs p -> q, p in S, q not in S."""
-    S = mask.bool()
-    n, K, H, W = nb.shape
-    val = torch.where(S, ct, cs).to(torch.int64).sum(dim=(1, 2))
-    for k in range(K):
-        dy, dx = DY[k], DX[k]
-        y0, y1 = max(0, -dy), H - max(0, dy)
-        x0, x1 = max(0, -dx), W - max(0, dx)
-        p = S[:, y0:y1, x0:x1]
-        q = S[:, y0 + dy:y1 + dy, x0 + dx:x1 + dx]
-        val += (nb[:, k, y0:y1, x0:x1].to(torch.int64) * (p & ~q)).sum(dim=(1, 2))
-    return val
 
 
 def test_c4_batch_flow_is_cut_of_mask(torch, gc):
@@ -365,49 +354,6 @@ def test_host_watchdog_stops_the_kernel(torch, gc, monkeypatch):
     F2, m2 = g2.solve(*to_dev(torch, cs, ct, nb))
     check_against_oracle(cs, ct, nb, F2.cpu().numpy(), m2.cpu().numpy(), "bk", frames=[0, 7])
     g2.close()
-
-
-def residual_closure_host(cs, ct, nb, f):
-    """Pixels reachable from s in the residual graph of the exported flow f:
-    the closure of {e > 0} (s -> v keeps residual capacity e(v)) under n-link arcs with
-    r_k(p) = c_k(p) - f(p -> p + d_k) > 0.  Plain scipy BFS (library routine), no solver code."""
-    import scipy.sparse as sp
-    from scipy.sparse.csgraph import breadth_first_order
-    K, H, W = nb.shape
-    N = H * W
-    idx = np.arange(N, dtype=np.int64).reshape(H, W)
-    e = cs.astype(np.int64) - ct.astype(np.int64)
-    flow = {}  # flow on arc p -> p + d_k for every k, from the forward-arc flows
-    for j in range(K // 2):
-        k = 2 * j
-        fk = np.zeros((H, W), np.int64)
-        y0, y1 = max(0, -DY[k]), H - max(0, DY[k])
-        x0, x1 = max(0, -DX[k]), W - max(0, DX[k])
-        fk[y0:y1, x0:x1] = f[j, y0:y1, x0:x1]
-        flow[k] = fk
-        rv = np.zeros((H, W), np.int64)  # reverse arc q -> p carries -f(p -> q), stored at q
-        rv[y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]] = -fk[y0:y1, x0:x1]
-        flow[k ^ 1] = rv
-        e[y0:y1, x0:x1] -= fk[y0:y1, x0:x1]
-        e[y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]] += fk[y0:y1, x0:x1]
-    rows, cols = [], []
-    for k in range(K):
-        y0, y1 = max(0, -DY[k]), H - max(0, DY[k])
-        x0, x1 = max(0, -DX[k]), W - max(0, DX[k])
-        r = nb[k, y0:y1, x0:x1].astype(np.int64) - flow[k][y0:y1, x0:x1]
-        open_ = r > 0
-        rows.append(idx[y0:y1, x0:x1][open_])
-        cols.append(idx[y0 + DY[k]:y1 + DY[k], x0 + DX[k]:x1 + DX[k]][open_])
-    src = np.flatnonzero(e.ravel() > 0)  # super-source N -> every excess node
-    rows.append(np.full(src.size, N, np.int64))
-    cols.append(src)
-    r_ = np.concatenate(rows)
-    c_ = np.concatenate(cols)
-    G = sp.csr_matrix((np.ones(r_.size, np.int8), (r_, c_)), shape=(N + 1, N + 1))
-    order = breadth_first_order(G, N, directed=True, return_predecessors=False)
-    m = np.zeros(N + 1, np.uint8)
-    m[order] = 1
-    return m[:N].reshape(H, W)
 
 
 def test_c5_4k_serpentine_certified(torch, gc):
