@@ -126,6 +126,18 @@ def debug_counters(ctx, reset: bool = False):
     return list(out)
 
 
+_lib.gc_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
+_lib.gc_debug_trace.restype = ctypes.c_longlong
+
+
+def debug_trace(ctx, cap: int = 4 << 20, reset: bool = True):
+    """Development per-task trace (profiling level 2; not part of gc.h): [m, 4] uint64 records
+    (globaltimer start, duration ns, md << 56 | gcnt << 48 | cta << 32 | frame, tile)."""
+    out = np.zeros((cap, 4), np.uint64)
+    n = int(_lib.gc_debug_trace(ctx, out.ctypes.data, cap, int(bool(reset))))
+    return out[:min(n, cap)]
+
+
 def gc_get_kernel_ms(ctx, reset: bool = False) -> float:
     return float(_lib.gc_get_kernel_ms(ctx, int(bool(reset))))
 
@@ -240,8 +252,9 @@ class GridCut:
     def launches(self) -> int:
         return gc_last_launches(self.ctx)
 
-    def set_profiling(self, on: bool):
-        gc_set_profiling(self.ctx, on)
+    def set_profiling(self, on):
+        """False/True, or 2 for the development per-task trace as well."""
+        _lib.gc_set_profiling(self.ctx, int(on))
 
     def profile(self, reset=False):
         return gc_get_profile(self.ctx, reset)

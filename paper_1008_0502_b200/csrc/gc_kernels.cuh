@@ -115,6 +115,11 @@ struct Dev {
   unsigned long long* ptiles;  // [6] tasks per class (profiling only, else NULL)
   unsigned long long* pns;     // [6] ns per class summed over CTAs (profiling only)
   unsigned long long* pdbg;    // [16] development counters (profiling only)
+  // development trace (profiling level 2 only, else NULL): one record of 4 u64 per task --
+  // globaltimer start, duration ns, (md << 56 | gcnt << 48 | cta << 32 | frame), tile
+  unsigned long long* trace;
+  unsigned long long* trace_n;
+  unsigned long long trace_cap;
 };
 
 enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_IDLE = 8 };

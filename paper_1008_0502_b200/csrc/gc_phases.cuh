@@ -1233,6 +1233,17 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
         uint64_t w1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
         atomicAdd(&d.pns[cls], (unsigned long long)(w1 - w0));
+        if (d.trace) {
+          const unsigned long long i = atomicAdd(d.trace_n, 1ULL);
+          if (i < d.trace_cap) {
+            unsigned long long* r = d.trace + 4 * i;
+            r[0] = w0;
+            r[1] = w1 - w0;
+            r[2] = ((unsigned long long)md << 56) | ((unsigned long long)gcnt << 48) |
+                   ((unsigned long long)blockIdx.x << 32) | (unsigned)d.sfr[s];
+            r[3] = gt - (size_t)s * d.T;
+          }
+        }
         // tiles processed (an init task covers a group of tiles)
         const int tl = (int)(gt - (size_t)s * d.T);
         atomicAdd(&d.ptiles[cls], md == M_INIT ? (unsigned long long)min(d.initg, d.T - tl) : (unsigned long long)gcnt);
@@ -1242,11 +1253,22 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     if (bc[3]) {
       uint64_t w0t = 0;
       if (prof && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0t));
+      const int sfr0 = d.sfr[s];
       transition(d, io, s, c, bc);
       if (prof && t == 0) {
         uint64_t w1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
         t_idle += w1 - w0t;
+        if (d.trace) {  // transition record: md 15, tile = the new mode
+          const unsigned long long i = atomicAdd(d.trace_n, 1ULL);
+          if (i < d.trace_cap) {
+            unsigned long long* r = d.trace + 4 * i;
+            r[0] = w0t;
+            r[1] = w1 - w0t;
+            r[2] = (15ULL << 56) | ((unsigned long long)blockIdx.x << 32) | (unsigned)sfr0;
+            r[3] = (unsigned long long)(unsigned)__ldcg(d.fmode + s);
+          }
+        }
       }
     }
   }

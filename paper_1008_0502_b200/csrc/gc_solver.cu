@@ -41,6 +41,9 @@ struct gc_ctx {
   std::string err;
   long long last_launches = 0;
   bool prof = false;
+  int prof_level = 0;                    // 2: also the per-task trace (development)
+  unsigned long long* trace = nullptr;   // device trace buffer [trace_cap][4] + counter
+  unsigned long long trace_cap = 0;
   long long prof_n[6] = {0, 0, 0, 0, 0, 0};
   long long prof_tiles[6] = {0, 0, 0, 0, 0, 0};
   unsigned long long* dtiles = nullptr;  // device counters [12]: tasks [6], ns [6]
@@ -177,6 +180,9 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.ptiles = c->prof ? c->dtiles : nullptr;
   d.pns = c->prof ? c->dtiles + 6 : nullptr;
   d.pdbg = c->prof ? c->dtiles + 12 : nullptr;
+  d.trace = c->prof_level >= 2 ? c->trace + 1 : nullptr;
+  d.trace_n = c->prof_level >= 2 ? c->trace : nullptr;
+  d.trace_cap = c->trace_cap;
   return d;
 }
 
@@ -513,6 +519,7 @@ void gc_destroy(gc_ctx* c) {
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->habort) cudaFreeHost(c->habort);
   if (c->dtiles) cudaFree(c->dtiles);
+  if (c->trace) cudaFree(c->trace);
   delete c;
 }
 
@@ -521,7 +528,34 @@ const char* gc_last_error(const gc_ctx* c) { return c ? c->err.c_str() : "NULL c
 long long gc_last_launches(const gc_ctx* c) { return c ? c->last_launches : 0; }
 
 void gc_set_profiling(gc_ctx* c, int enable) {
-  if (c) c->prof = enable != 0;
+  if (!c) return;
+  c->prof = enable != 0;
+  c->prof_level = enable;
+  if (enable >= 2 && !c->trace) {  // development trace: 4M task records
+    c->trace_cap = 4u << 20;
+    if (cudaMalloc(&c->trace, (c->trace_cap * 4 + 1) * 8) != cudaSuccess) {
+      cudaGetLastError();
+      c->trace = nullptr;
+      c->trace_cap = 0;
+      c->prof_level = 1;
+    } else {
+      cudaMemset(c->trace, 0, 8);
+    }
+  }
+}
+
+// Development trace of the last solves (profiling level 2; not part of gc.h): copies up to
+// `cap` records of 4 u64 (see Dev::trace) to host `out`, returns the number recorded (may
+// exceed cap) and resets the trace if reset != 0.
+long long gc_debug_trace(gc_ctx* c, unsigned long long* out, long long cap, int reset) {
+  if (!c || !c->trace) return 0;
+  unsigned long long n = 0;
+  cudaMemcpy(&n, c->trace, 8, cudaMemcpyDeviceToHost);
+  const unsigned long long m = n < (unsigned long long)cap ? n : (unsigned long long)cap;
+  const unsigned long long mm = m < c->trace_cap ? m : c->trace_cap;
+  if (out && mm) cudaMemcpy(out, c->trace + 1, mm * 32, cudaMemcpyDeviceToHost);
+  if (reset) cudaMemset(c->trace, 0, 8);
+  return (long long)n;
 }
 
 void gc_get_profile(gc_ctx* c, long long* launches, double* ms, long long* tiles, int reset) {
