@@ -21,7 +21,6 @@
 //                              arc direction and receiver edge slot: `sent` written only by
 //                              the sending tile, `got` only by the receiver (no atomics)
 //   reach [slot][tile][k][64]  min-cut reach marks arriving across the border (closure epoch)
-//   m  [slot][tile][1024] u8   closure membership, as the epoch of the closure attempt
 // A tile is processed by at most one CTA at a time (gc_phases.cuh); all mutable state is
 // read through L2 (the library is compiled with -dlcm=cg), the caps through the read-only
 // path.
@@ -62,9 +61,13 @@ struct Dev {
   uint8_t* reach;
   long long* neg0;  // [NS] the tile's share of sumneg: sum max(0,-e) as initialised, updated
                     //      by each closure seed of a materialised tile
-  uint8_t* m;       // [NS][1024] closure attempt epoch of the pixels in the closure
-  int32_t* tcs;     // [NS]   epoch of the closure attempt that last wrote the tile's m
-  int32_t* tmk;     // [NS]   epoch of the closure attempt in which the tile got closure pixels
+  int32_t* tsrc;    // [NS]   uniform source tile: every in-frame pixel has e > 0 (all in the
+                    //        closure; the init pass wrote its mask bytes = 1)
+  int32_t* tss;     // [NS]   global relabel (fbe) in which the seed of this uniform source tile
+                    //        was skipped: its stored h / hedge are stale, read as HINF, until a
+                    //        relax or push task of that relabel writes them (and clears it)
+  int32_t* tmk;     // [NS]   epoch of the closure attempt in which the tile's mask bytes got a
+                    //        1 beyond its excess pixels (rewritten by the next attempt)
   int32_t* mat;     // [NS]   e, r of the tile are materialised
   int32_t* tact;    // [NS]   tile has an active node (e > 0, h < HINF)
   int32_t* flag;    // [NS]   tile is in the first task set of the next phase (seed -> BFS, cseed -> closure)
@@ -196,8 +199,10 @@ __device__ __forceinline__ void recv_pixel(int k, int sl, int& uy, int& ux) {
 __device__ __forceinline__ int hidx(int iy, int ix) { return (iy + 1) * HS + (ix + 1); }
 __device__ __forceinline__ bool on_border(int iy, int ix) { return iy == 0 || iy == 31 || ix == 0 || ix == 31; }
 
-// Load the 34x34 halo ring of heights from the neighbours' border copies (HINF off-frame).
-__device__ __forceinline__ void load_halo(const Dev& d, int s, int ty, int tx, int* hs, int t) {
+// Load the 34x34 halo ring of heights from the neighbours' border copies (HINF off-frame, and
+// HINF for a neighbour whose seed was skipped in relabel `ep` as a uniform source tile and
+// that no task has relabelled since: its stored copy is stale).
+__device__ __forceinline__ void load_halo(const Dev& d, int s, int ty, int tx, int* hs, int t, int ep) {
   if (t < 128) {
     const int side = t >> 5, i = t & 31;
     int nty = ty, ntx = tx, esd, pos;
@@ -206,16 +211,22 @@ __device__ __forceinline__ void load_halo(const Dev& d, int s, int ty, int tx, i
     else if (side == 2) { ntx = tx - 1; esd = 3; pos = hidx(i, -1); }
     else { ntx = tx + 1; esd = 2; pos = hidx(i, 32); }
     int v = HINF;
-    if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
-      v = d.hedge[(((size_t)s * d.T + nty * d.TX + ntx) * 4 + esd) * 32 + i];
+    if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX) {
+      const size_t n = (size_t)s * d.T + nty * d.TX + ntx;
+      const int hv = d.hedge[(n * 4 + esd) * 32 + i];
+      v = __ldcg(d.tss + n) == ep ? HINF : hv;
+    }
     hs[pos] = v;
   } else if (t < 132) {
     const int c = t - 128;
     const int dy = (c < 2) ? -1 : 1, dx = (c & 1) ? 1 : -1;
     const int nty = ty + dy, ntx = tx + dx;
     int v = HINF;
-    if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX)
-      v = d.hedge[(((size_t)s * d.T + nty * d.TX + ntx) * 4 + (dy < 0 ? 1 : 0)) * 32 + (dx < 0 ? 31 : 0)];
+    if (nty >= 0 && nty < d.TY && ntx >= 0 && ntx < d.TX) {
+      const size_t n = (size_t)s * d.T + nty * d.TX + ntx;
+      const int hv = d.hedge[(n * 4 + (dy < 0 ? 1 : 0)) * 32 + (dx < 0 ? 31 : 0)];
+      v = __ldcg(d.tss + n) == ep ? HINF : hv;
+    }
     hs[hidx(dy < 0 ? -1 : 32, dx < 0 ? -1 : 32)] = v;
   }
 }
@@ -673,7 +684,8 @@ constexpr int INIT_GMAX = 32;  // tiles per init task, at most
 struct InitPart {
   long long sct[NTH / 32];  // sum c(v,t)
   long long neg[NTH / 32];  // sum max(0,-e)
-  int fl[NTH / 32];         // bit 0: capacity out of range, bit 1: not a uniform sink tile
+  int fl[NTH / 32];         // bit 0: capacity out of range, bit 1: not a uniform sink tile,
+                            // bit 2: not a uniform source tile
 };
 
 template <int K, bool WARM, bool EXPORT>
@@ -693,7 +705,7 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
   // arcs whose far end is in the frame: all of them for tiles away from the frame border
   const bool inner = ty > 0 && tx > 0 && (ty + 1) * TS < H && (tx + 1) * TS < W;
   int acc = 0;  // OR of every in-grid capacity: one is outside [0, GC_CAP_MAX] iff acc & ~CAPMAX
-  int uni = 1;
+  int uni = 1, src = 1;
   long long sct = 0, neg = 0;
   int fl4[4];
 #pragma unroll
@@ -742,6 +754,7 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
       f |= (ev > 0 ? FL_POS : 0) | (ev < 0 ? FL_NEG : 0);
       neg += ev < 0 ? -(long long)ev : 0;
       uni &= ev < 0;
+      src &= ev > 0;
       if (EXPORT) {  // a5: the export of a tile no push ever touches is its initial flow
         int32_t* fo = io.fstate + fr * plane * (K / 2) + o0 + i;
 #pragma unroll
@@ -755,14 +768,17 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
   w.x = (unsigned short)fl4[0]; w.y = (unsigned short)fl4[1];
   w.z = (unsigned short)fl4[2]; w.w = (unsigned short)fl4[3];
   *reinterpret_cast<ushort4*>(d.fl + gt * TPX + iy * TS + ix0) = w;
-  if (y < H) {  // the caller's mask starts all 0; the closure phases write the ones
+  if (y < H) {  // the caller's mask starts as the excess pixels (e > 0: always in the closure);
+                 // the closure phases write the other closure pixels (and rewrite touched tiles)
     uint8_t* mk = io.mask + fr * plane + (size_t)y * W + x0;
+    const uint32_t mw = ((fl4[0] >> 8) & 1u) | (((fl4[1] >> 8) & 1u) << 8) | (((fl4[2] >> 8) & 1u) << 16) |
+                        (((unsigned)(fl4[3] >> 8) & 1u) << 24);
     if (x0 + 3 < W && ((uintptr_t)mk & 3) == 0) {
-      *reinterpret_cast<uint32_t*>(mk) = 0u;
+      *reinterpret_cast<uint32_t*>(mk) = mw;
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (x0 + i < W) mk[i] = 0;
+        if (x0 + i < W) mk[i] = (uint8_t)((mw >> (8 * i)) & 1u);
     }
   }
   if (t < K * 16) reinterpret_cast<uint32_t*>(d.reach + gt * K * 64)[t] = 0u;
@@ -773,7 +789,7 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
   const unsigned s_hi = __reduce_add_sync(0xffffffffu, (unsigned)(us >> 16));
   const unsigned n_lo = __reduce_add_sync(0xffffffffu, (unsigned)(un & 0xffffu));
   const unsigned n_hi = __reduce_add_sync(0xffffffffu, (unsigned)(un >> 16));
-  const int wfl = __reduce_or_sync(0xffffffffu, bad | ((!uni) << 1));
+  const int wfl = __reduce_or_sync(0xffffffffu, bad | ((!uni) << 1) | ((!src) << 2));
   if ((t & 31) == 0) {
     part->sct[t >> 5] = (long long)s_lo + ((long long)s_hi << 16);
     part->neg[t >> 5] = (long long)n_lo + ((long long)n_hi << 16);
@@ -792,7 +808,7 @@ __device__ __forceinline__ void init_finalize(const Dev& d, size_t gt0, int n, c
     int f = 0;
 #pragma unroll
     for (int w = 0; w < NTH / 32; ++w) { sa += part[t].sct[w]; sb += part[t].neg[w]; f |= part[t].fl[w]; }
-    const int uni = !(f & 2);
+    const int uni = !(f & 2), src = !(f & 4);
     if (sa) atomicAdd(&d.sumct[s], (unsigned long long)sa);
     if (sb) atomicAdd(&d.sumneg[s], (unsigned long long)sb);  // corrected by the closure seed if e changes
     d.neg0[gt] = sb;
@@ -801,11 +817,12 @@ __device__ __forceinline__ void init_finalize(const Dev& d, size_t gt0, int n, c
     d.recv1[gt] = 0;
     d.tact[gt] = 0;
     d.tuni[gt] = uni;
+    d.tsrc[gt] = src;
     d.tfix[gt] = uni;
     d.tph[gt] = -1;
-    d.tcs[gt] = 0;
     d.tmk[gt] = 0;
     d.tsk[gt] = 0;  // relabel epochs restart at 1 per frame: a stale stamp would alias
+    d.tss[gt] = 0;
     if (f & 1) d.ferr[s] = 1;
     uni_s[t] = uni;
   }

@@ -59,12 +59,23 @@ struct Ctl {
   int rounds;                // push/relabel rounds per push task
   int nframes;
   int vec;                   // caller rows 16-byte aligned: int4 loads in the init pass
+  int K4;                    // 4-neighbour frames (no diagonal arcs)
 };
 
 // ------------------------------------------------------------------ queue primitives
 // Release/acquire fence at GPU scope (cheaper than __threadfence's sequentially consistent
 // fence); every mutable load goes to L2 (-dlcm=cg), so it is all the ordering needed.
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const volatile uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void q_put(const Dev& d, unsigned long long p, uint32_t v) {
   volatile uint32_t* slot = d.q + (p & d.qmask);
@@ -156,7 +167,8 @@ __device__ __forceinline__ void absorb_pixelwise(const Dev& d, const IO& io, siz
   if (t == 0) {
     d.mat[gt] = 1;
     d.recv1[gt] = 0;
-    d.tuni[gt] = 0;  // the tile changed: no longer a known uniform sink tile (a seed recomputes)
+    d.tuni[gt] = 0;  // the tile changed: no longer a known uniform sink / source tile (a seed
+    d.tsrc[gt] = 0;  // recomputes)
     d.tfix[gt] = 0;
   }
 }
@@ -198,14 +210,16 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   const int s = (int)((unsigned)gt / (unsigned)d.T);
   if (t == 0) {
     bc[0] = __ldcg(d.recv1 + gt);
-    bc[2] = __ldcg(d.tuni + gt);
+    bc[2] = __ldcg(d.tuni + gt) | __ldcg(d.tsrc + gt);
     bc[6] = __ldcg(d.fbe + s);
     bc[7] = 0;
     bc[4] = __ldcg(d.fbnd + s);
   }
   __syncthreads();
   const int rcv = bc[0];
-  if (bc[2] && !rcv) return;  // untouched uniform sink tile: h = 1, hedge published
+  // a uniform sink tile (h = 1, hedge published) or a uniform source tile (no sink: h = HINF,
+  // its tss stamp says so) without inflow is not seeded (the transition stamped it)
+  if (bc[2] && !rcv) return;
   // halo: the border heights of the neighbours whose seed was skipped in this relabel
   // (uniform sink tiles: final), INF elsewhere -- the BFS phase brings in the others.  The
   // candidates of every side are loaded together with the skip stamps and the fl words
@@ -235,7 +249,7 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   }
   __syncthreads();
   bfs_fixpoint<K>(hs, fl, h, bc[4]);
-  int act = 0, fix = 1, uni = 1, bits = 0, mnh = HINF;
+  int act = 0, fix = 1, uni = 1, src = 1, bits = 0, mnh = HINF;
   const int tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
 #pragma unroll
@@ -247,6 +261,7 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
     fix &= (h[j] == 1) || !(fl[j] & 0xff);
     const bool in = ty * TS + iy < d.H && tx * TS + ix < d.W;
     uni &= !in || (fl[j] & FL_NEG);
+    src &= !in || (fl[j] & FL_POS);
     if (on_border(iy, ix) && h[j] < HINF) bits |= border_bits(iy, ix);
   }
   store_hedge(d, gt, h, t);
@@ -257,12 +272,15 @@ __device__ __forceinline__ void task_seed(const Dev& d, const IO& io, size_t gt,
   if ((t & 31) == 0) atomicMin(&bc[5], mnh);
   fix = __syncthreads_and(fix);
   uni = __syncthreads_and(uni);
+  src = __syncthreads_and(src);
   if ((t & 31) == 0 && bits) atomicOr(&bc[1], bits);
   if (t == 0) {
     d.tact[gt] = act;
     d.tminh[gt] = bc[5];
     d.tfix[gt] = fix;
     d.tuni[gt] = uni;
+    d.tsrc[gt] = src;
+    d.tss[gt] = 0;  // h and hedge written in this relabel
   }
   flag_sides(d, gt, bc[1], K);
 }
@@ -275,16 +293,24 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
   const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
-  if (t == 0) { bc[1] = 0; bc[4] = __ldcg(d.fbnd + s); }
+  if (t == 0) {
+    bc[1] = 0;
+    bc[4] = __ldcg(d.fbnd + s);
+    const int ep = __ldcg(d.fbe + s);
+    bc[6] = ep;
+    bc[7] = __ldcg(d.tss + gt) == ep;  // seed skipped (uniform source): stored h stale, HINF
+  }
+  __syncthreads();
+  const int ep = bc[6], stale = bc[7];
   int fl[4], h[4], h0[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int lp = (iy0 + 8 * j) * TS + ix;
     fl[j] = d.fl[gt * TPX + lp];
-    h[j] = h0[j] = d.h[gt * TPX + lp];
+    h[j] = h0[j] = stale ? HINF : d.h[gt * TPX + lp];
     hs[hidx(iy0 + 8 * j, ix)] = h[j];
   }
-  load_halo(d, s, ty, tx, hs, t);
+  load_halo(d, s, ty, tx, hs, t, ep);
   __syncthreads();
   bfs_fixpoint<K>(hs, fl, h, bc[4]);
   int any = 0, bits = 0, act = 0, fix = 1, mnh = HINF;
@@ -311,6 +337,13 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
     for (int j = 0; j < 4; ++j) d.h[gt * TPX + (iy0 + 8 * j) * TS + ix] = h[j];
     store_hedge(d, gt, h, t);
     if (t == 0) { d.tact[gt] = act; d.tfix[gt] = fix; d.tminh[gt] = bc[5]; }
+    if (stale) {  // h and hedge now hold this relabel's values: readers may use them
+      __syncthreads();
+      if (t == 0) {
+        fence_gpu();
+        d.tss[gt] = 0;
+      }
+    }
   }
 }
 
@@ -319,8 +352,11 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
 // with e < 0 (residual capacity to t), no excess can reach t: the preflow is maximum and
 // the closure is the source side of the inclusion-minimal minimum cut --
 // the certificate that ends a solve.  Otherwise the attempt fails (cfail) and the frame
-// returns to a global relabel.  Closure membership and border reach marks carry the
-// attempt's epoch, so a failed attempt leaves nothing behind.
+// returns to a global relabel.  Border reach marks carry the attempt's epoch, so a failed
+// attempt leaves nothing behind.  The caller's mask starts as the excess pixels (the init
+// pass writes it; they are in every closure): a tile a push touched (mat) rewrites all its
+// bytes in its closure seed, an untouched tile only writes the closure pixels beyond its
+// excess pixels ("extras", flagged in tmk so that the next attempt rewrites the tile).
 __device__ __forceinline__ int closure_epoch(const Dev& d, int s) { return __ldcg(d.cep + s) % 255 + 1; }
 
 template <int K>
@@ -351,8 +387,12 @@ __device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uin
   }
 }
 
-// Marks the border arcs leaving newly reached pixels with the epoch; returns the sides
-// (side_bit) of the neighbour tiles that were marked.
+// Marks the border arcs leaving the pixels with send[j] set with the epoch (a mark is only
+// set if the receiving pixel is not an excess node -- those are in the closure anyway -- and
+// was not set before in this attempt); returns the sides (side_bit) of the neighbour tiles
+// that got a NEW mark.  Each mark slot has one writer (the tile of the sending pixel), so the
+// check-and-set needs no atomic; since only new marks request the receiver, the closure
+// phase ends once no tile adds a pixel.
 template <int K>
 __device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (&send)[4], const uint8_t* os,
                                             int ep, const uint16_t* flh) {
@@ -374,8 +414,11 @@ __device__ __forceinline__ int closure_send(const Dev& d, size_t gt, const int (
       const int rty = ty + dy, rtx = tx + dx;
       if (rty < 0 || rty >= d.TY || rtx < 0 || rtx >= d.TX) continue;
       const size_t rgt = (size_t)s * d.T + rty * d.TX + rtx;
-      d.reach[(rgt * K + k) * 64 + recv_slot(k, y2 & 31, x2 & 31)] = (uint8_t)ep;
-      sides |= 1 << side_bit(dy, dx);
+      uint8_t* mk = d.reach + (rgt * K + k) * 64 + recv_slot(k, y2 & 31, x2 & 31);
+      if (*mk != (uint8_t)ep) {
+        *mk = (uint8_t)ep;
+        sides |= 1 << side_bit(dy, dx);
+      }
     }
   }
   return sides;
@@ -391,9 +434,7 @@ __device__ __forceinline__ int block_or_bits(int bits, int* bc) {
   return bc[1];
 }
 
-// The caller's mask bytes of the tile's in-frame pixels with wr[j] set: 1 iff in the closure.
-// Written during the attempt itself: if it fails, every tile that got closure pixels (tmk)
-// is closure-seeded again in the next attempt, which rewrites all its bytes.
+// The caller's mask bytes of the tile's in-frame pixels with wr[j] set: mm[j].
 __device__ __forceinline__ void mask_write(const Dev& d, const IO& io, size_t gt, const int (&mm)[4],
                                            const int (&wr)[4]) {
   const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
@@ -411,9 +452,12 @@ template <int K>
 __device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t gt);
 
 // ---------------------------------------------------------------- a4: closure seed (one tile)
-// Absorbs flow still in flight, closes {e > 0} inside the tile, writes the tile's m,
-// marks reach across the border (flagging the receivers for the closure phase), checks the
-// certificate, and brings the tile's share of sum max(0,-e) up to date.
+// Absorbs flow still in flight, closes {e > 0} inside the tile, writes the mask bytes that
+// differ from the init pass's (all of a touched tile), marks reach across the border
+// (flagging the receivers for the closure phase), checks the certificate, and brings the
+// tile's share of sum max(0,-e) up to date.  An untouched uniform source tile (every pixel
+// e > 0: closure = the whole tile, mask already written) only marks its border arcs.  A
+// frame with out-of-range caps gets an all-0 mask here (gc.h).
 template <int K>
 __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
                                            long long* red, int* bc) {
@@ -423,16 +467,26 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
     // every word at once (independent loads, one round trip)
     const int r1 = __ldcg(d.recv1 + gt), fe = __ldcg(d.ferr + s), cf = __ldcg(d.cfail + s);
     const int tu = __ldcg(d.tuni + gt), mt = __ldcg(d.mat + gt), tm = __ldcg(d.tmk + gt);
+    const int tsr = __ldcg(d.tsrc + gt);
     const int cp = __ldcg(d.cep + s);
     bc[0] = r1;
-    // range error (mask stays 0, F = -1), the attempt already failed, or (a tile of the
-    // group outside the task set) an untouched uniform sink tile that never had closure pixels
-    bc[2] = (fe != 0) | (cf > 0) | ((tu != 0) & (mt == 0) & (r1 == 0) & (tm == 0));
-    bc[3] = mt | r1;
-    bc[4] = cp % 255 + 1;  // closure epoch (closure_epoch)
+    // 2: range error (mask all 0, F = -1); 1: skip -- the attempt already failed, or (a tile of
+    // the group outside the task set) an untouched uniform sink tile without extra mask bytes;
+    // 3: untouched uniform source tile (border marks only); 0: full closure seed
+    bc[2] = fe ? 2 : ((cf > 0) | ((tu != 0) & (mt == 0) & (r1 == 0) & (tm == 0))) ? 1
+                                                                                  : ((tsr != 0) & (mt == 0) & (r1 == 0)) ? 3 : 0;
+    bc[3] = mt | r1;        // e, r materialised: rewrite every mask byte, recompute the deficit
+    bc[5] = (mt | r1) | tm; // every mask byte of the tile is (re)written
+    bc[4] = cp % 255 + 1;   // closure epoch (closure_epoch)
   }
   __syncthreads();
-  if (bc[2]) return;
+  const int mode = bc[2];
+  if (mode == 1) return;
+  if (mode == 2) {  // range error: the frame's mask is all 0
+    const int none[4] = {0, 0, 0, 0}, all[4] = {1, 1, 1, 1};
+    mask_write(d, io, gt, none, all);
+    return;
+  }
   uint16_t* flh = reinterpret_cast<uint16_t*>(ms + 12288);  // the neighbours' border fl words
   {
     const int tile = (int)(gt - (size_t)s * d.T);
@@ -445,13 +499,14 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
     for (int j = 0; j < 4; ++j) fl[j] = d.fl[gt * TPX + (iy0 + 8 * j) * TS + ix];
   }
   const int ep = bc[4];
-  const int mat = bc[3];
-  int mm[4];
+  const int mat = bc[3], wall = bc[5];
+  int mm[4], pos[4];
   long long neg = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int lp = (iy0 + 8 * j) * TS + ix;
-    mm[j] = (fl[j] & FL_POS) ? 1 : 0;
+    pos[j] = (fl[j] & FL_POS) ? 1 : 0;
+    mm[j] = pos[j];
     ms[lp] = (uint8_t)mm[j];
     os[lp] = (uint8_t)(fl[j] & 0xff);
     if (mat) {
@@ -460,29 +515,36 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
     }
   }
   __syncthreads();
-  closure_fixpoint<K>(ms, os, mm);
-  int fail = 0, any = 0;
+  int fail = 0, extra = 0;
+  if (mode == 0) {
+    closure_fixpoint<K>(ms, os, mm);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = mm[j] ? (uint8_t)ep : (uint8_t)0;
-    fail |= mm[j] && (fl[j] & FL_NEG);
-    any |= mm[j];
+    for (int j = 0; j < 4; ++j) {
+      fail |= mm[j] && (fl[j] & FL_NEG);
+      extra |= mm[j] & !pos[j];
+    }
+    fail = __syncthreads_or(fail);
+    extra = __syncthreads_or(extra);
+    if (wall) {
+      const int all[4] = {1, 1, 1, 1};
+      mask_write(d, io, gt, mm, all);
+    } else if (extra) {
+      int wr[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) wr[j] = mm[j] & !pos[j];
+      mask_write(d, io, gt, mm, wr);
+    }
   }
-  fail = __syncthreads_or(fail);
-  any = __syncthreads_or(any);
-  if (d.pdbg) {  // development: closure-seed tiles, tiles entirely in the closure
-    const int full = __syncthreads_and(mm[0] & mm[1] & mm[2] & mm[3]);
-    if (t == 0) { atomicAdd(&d.pdbg[9], 1ULL); if (full) atomicAdd(&d.pdbg[10], 1ULL); }
-  }
-  {
-    const int all[4] = {1, 1, 1, 1};
-    mask_write(d, io, gt, mm, all);
+  if (d.pdbg) {  // development: closure-seed tiles, border-only ones
+    if (t == 0) { atomicAdd(&d.pdbg[9], 1ULL); if (mode == 3) atomicAdd(&d.pdbg[10], 1ULL); }
   }
   const int sides = block_or_bits(closure_send<K>(d, gt, mm, os, ep, flh), bc);
+  if (mat) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
-  if ((t & 31) == 0) red[t >> 5] = neg;
-  __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) neg += __shfl_xor_sync(0xffffffffu, neg, o);
+    if ((t & 31) == 0) red[t >> 5] = neg;
+    __syncthreads();
+  }
   if (t == 0) {
     if (mat) {  // replace the tile's share of sum max(0,-e) by its current value
       long long tot = 0;
@@ -491,8 +553,8 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
       if (dl) atomicAdd(&d.sumneg[s], (unsigned long long)dl);
       d.neg0[gt] = tot;
     }
-    d.tcs[gt] = ep;
-    if (any) d.tmk[gt] = ep;
+    if (mode == 0 && wall) d.tmk[gt] = extra ? ep : 0;  // every byte rewritten just now
+    else if (extra) d.tmk[gt] = ep;
     if (fail) atomicAdd(&d.cfail[s], 2);  // cfail: 0 / -1 (after the BFS certificate) + 2 per failure
   }
   flag_sides(d, gt, sides, K);
@@ -503,7 +565,9 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
 }
 
 // ---------------------------------------------------------------- a4: closure relax (one tile)
-// Returns the sides to request in bc[1].
+// Recomputes the tile's closure from its excess pixels and the reach marks of this attempt,
+// writes mask bytes of its pixels beyond the excess ones, checks the certificate and marks
+// the border arcs of those pixels.  Returns the sides to request (new marks) in bc[1].
 template <int K>
 __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
                                             int* bc) {
@@ -512,19 +576,19 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
   if (t == 0) {
     bc[1] = 0;
     bc[2] = __ldcg(d.cfail + s) > 0;
+    bc[4] = closure_epoch(d, s);
   }
   __syncthreads();
   if (bc[2]) return;  // the attempt already failed
-  const int ep = closure_epoch(d, s);
-  const bool valid = __ldcg(d.tcs + gt) == ep;  // else m is stale: the tile was not closure-seeded
-  int mm[4], m0[4], fl[4];
+  const int ep = bc[4];
+  int mm[4], pos[4], fl[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j, lp = iy * TS + ix;
     fl[j] = d.fl[gt * TPX + lp];
-    m0[j] = valid && d.m[gt * TPX + lp] == ep;
+    pos[j] = (fl[j] & FL_POS) ? 1 : 0;
     os[lp] = (uint8_t)(fl[j] & 0xff);
-    int got = m0[j];
+    int got = pos[j];
     if (!got && on_border(iy, ix)) {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -541,24 +605,15 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
   int nw[4], any = 0, fail = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    nw[j] = mm[j] & !m0[j];
+    nw[j] = mm[j] & !pos[j];  // closure pixels beyond the excess ones (their bytes may be new)
     any |= nw[j];
     fail |= nw[j] && (fl[j] & FL_NEG);
   }
   any = __syncthreads_or(any);
   fail = __syncthreads_or(fail);
   if (d.pdbg && t == 0) { atomicAdd(&d.pdbg[11], 1ULL); if (any) atomicAdd(&d.pdbg[12], 1ULL); }
-  if (any || !valid) {
-    int wr[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      wr[j] = nw[j] || !valid;
-      if (wr[j]) d.m[gt * TPX + (iy0 + 8 * j) * TS + ix] = mm[j] ? (uint8_t)ep : (uint8_t)0;
-    }
-    mask_write(d, io, gt, mm, wr);
-  }
+  if (any) mask_write(d, io, gt, mm, nw);
   if (t == 0) {
-    if (!valid) d.tcs[gt] = ep;
     if (any) d.tmk[gt] = ep;
     if (fail) atomicAdd(&d.cfail[s], 2);
   }
@@ -636,6 +691,7 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     const long long rel = (long long)__ldcg(d.frel + s);
     const int prg = __ldcg(d.fprog + s), drn = __ldcg(d.fdrain + s);
     const int tu = __ldcg(d.tuni + gt), cap = __ldcg(d.fcap + s);
+    const int ep = __ldcg(d.fbe + s), ts = __ldcg(d.tss + gt);
     const bool cond = (rel > (c.relabel_budget << min(cep, 10))) | (vis >= c.vis_budget) |
                       (vis - prg > (c.stall << min(max(cep - c.stallx, 0), 24)));
     bc[0] = cond | (drn != 0);
@@ -648,13 +704,15 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     bc[4] = tu;
     bc[5] = HINF;
     bc[7] = cap;  // pixels higher than this are frozen in this phase
+    bc[6] = ep;
+    red[0] = ts == ep;  // seed skipped (uniform source), no relax since: stored h stale, HINF
   }
   __syncthreads();
   if (bc[0]) {
     if (d.pdbg && t == 0) atomicAdd(&d.pdbg[4], 1ULL);
     return;
   }
-  const int rcv = bc[2], uni = bc[4], hcap = bc[7];
+  const int rcv = bc[2], uni = bc[4], hcap = bc[7], hep = bc[6], stale = (int)red[0];
   tile_load_smem<K>(d, io, gt, es, rs, c.vec != 0);
   long long neg0 = 0;  // deficit of the tile before the task (flow absorbed = progress)
 #pragma unroll
@@ -671,12 +729,13 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
   for (int j = 0; j < 4; ++j) {
     const int iy = iy0 + 8 * j;
     // a uniform sink tile's heights are not stored: h = 1 in frame
-    const int hv = uni ? ((ty * TS + iy < d.H && tx * TS + ix < d.W) ? 1 : HINF) : d.h[gt * TPX + iy * TS + ix];
+    const int hv = uni ? ((ty * TS + iy < d.H && tx * TS + ix < d.W) ? 1 : HINF)
+                       : (stale ? HINF : d.h[gt * TPX + iy * TS + ix]);
     hb[0][hidx(iy, ix)] = hv;
     hb[1][hidx(iy, ix)] = hv;
   }
-  load_halo(d, s, ty, tx, hb[0], t);
-  load_halo(d, s, ty, tx, hb[1], t);
+  load_halo(d, s, ty, tx, hb[0], t, hep);
+  load_halo(d, s, ty, tx, hb[1], t, hep);
   for (int i = t; i < K * 64; i += NTH) (&oacc[0][0])[i] = 0;
   __syncthreads();
   int nrel = 0;  // relabel operations (global-relabel heuristic)
@@ -831,7 +890,9 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
     d.tact[gt] = act;
     d.mat[gt] = 1;
     d.tuni[gt] = 0;
+    d.tsrc[gt] = 0;
     d.tfix[gt] = 0;
+    d.tss[gt] = 0;  // h and hedge were written (after the fence above)
     const int v = atomicAdd(&d.fvis[s], 1) + 1;
     // progress: flow absorbed by deficit nodes, or excess at a height lower than any seen
     // so far in the phase (flow moving toward the sink; excess that only sloshes and
@@ -882,7 +943,8 @@ __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, 
 
 // Run by one CTA when the phase of slot s has no task left (fout[s] == 0): decide the next
 // phase and enqueue its tasks.  Loops while a phase turns out to have no task at all.
-__device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const Ctl& c, int* bc) {
+__device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const Ctl& c, int* bc, uint32_t* sbits,
+                                        int sbits_words) {
   const int t = threadIdx.x;
   if (t == 0) atomicAdd(&d.fout[s], 1);  // guard: no other CTA can see fout == 0 while we enqueue
   for (;;) {
@@ -915,7 +977,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       bool finished = false;
       if (md == M_INIT) {
         nm = d.ferr[s] ? M_CSEED : M_SEED;
-        kind = d.ferr[s] ? SET_EMPTY : SET_SEED;
+        kind = d.ferr[s] ? SET_ALL : SET_SEED;  // range error: the closure seeds zero the mask
       } else if (md == M_SEED) {
         nm = M_BFS;
         kind = SET_FLAG;
@@ -1006,6 +1068,18 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     if (kind == SET_NONE) break;
     // enqueue the phase's first task set, NTH tiles at a time
     const size_t base_gt = (size_t)s * d.T;
+    // closure seeds: an untouched uniform source tile whose neighbours are all uniform source
+    // tiles has nothing to do (its closure is the whole tile, its mask bytes are written, and
+    // no border arc reaches a pixel that is not an excess node) -- a bit per tile of tsrc
+    const bool srcskip = kind == SET_CSEED && (d.T + 31) / 32 <= sbits_words;
+    if (srcskip) {
+      for (int b0 = 0; b0 < d.T; b0 += NTH) {
+        const int i = b0 + t;
+        const unsigned bal = __ballot_sync(0xffffffffu, i < d.T && __ldcg(d.tsrc + base_gt + i) != 0);
+        if ((t & 31) == 0 && i < d.T + 31) sbits[i >> 5] = bal;
+      }
+      __syncthreads();
+    }
     for (int b0 = 0; kind != SET_EMPTY && b0 < d.T; b0 += NTH) {
       const int i = b0 + t;
       int want = 0;
@@ -1013,13 +1087,32 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         const size_t gt = base_gt + i;
         if (kind == SET_ALL) want = 1;
         else if (kind == SET_INITG) want = (i % d.initg) == 0;  // one init task per tile group
-        else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1
-          want = !(__ldcg(d.tuni + gt) && !__ldcg(d.recv1 + gt));
-          if (!want) d.tsk[gt] = bc[3];
+        else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1, uniform source
+          const int tu = __ldcg(d.tuni + gt), tsr = __ldcg(d.tsrc + gt), r1 = __ldcg(d.recv1 + gt);
+          want = !((tu | tsr) && !r1);  // tiles have no sink pixel: h = HINF until relaxed
+          if (!want && tu) d.tsk[gt] = bc[3];
+          if (!want && !tu) {
+            d.tss[gt] = bc[3];
+            d.tact[gt] = 0;
+          }
           d.flag[gt] = 0;
         } else if (kind == SET_CSEED) {  // untouched uniform sink tiles are never in the closure
-          want = !(__ldcg(d.tuni + gt) && !__ldcg(d.mat + gt) && !__ldcg(d.recv1 + gt)) ||
-                 __ldcg(d.tmk + gt) != 0;  // mask bytes of a failed attempt are rewritten
+          const int tu = __ldcg(d.tuni + gt), mt = __ldcg(d.mat + gt), r1 = __ldcg(d.recv1 + gt);
+          const int tm = __ldcg(d.tmk + gt);
+          want = !(tu && !mt && !r1) || tm != 0;  // mask bytes of a failed attempt are rewritten
+          if (want && srcskip && !mt && !r1 && !tm && ((sbits[i >> 5] >> (i & 31)) & 1)) {
+            const int ty = i / d.TX, tx = i - ty * d.TX;
+            bool inner = true;
+            for (int dy = -1; dy <= 1; ++dy)
+              for (int dx = -1; dx <= 1; ++dx) {
+                const int ny = ty + dy, nx = tx + dx;
+                if ((dy == 0 && dx == 0) || ny < 0 || ny >= d.TY || nx < 0 || nx >= d.TX) continue;
+                if (dy != 0 && dx != 0 && c.K4) continue;  // no diagonal arcs
+                const int n = ny * d.TX + nx;
+                inner &= ((sbits[n >> 5] >> (n & 31)) & 1) != 0;
+              }
+            if (inner) want = 0;
+          }
           d.flag[gt] = 0;
         } else if (kind == SET_FLAG) {
           want = __ldcg(d.flag + gt);
@@ -1084,7 +1177,6 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
   const int t = threadIdx.x;
   const bool prof = d.pns != nullptr;
   unsigned long long t_idle = 0;
-  unsigned long long tick = 0;  // thread 0: queue ticket
   unsigned ntask_local = 0;
   for (;;) {
     if (t == 0 && next_s != QEMPTY) {  // local continuation
@@ -1105,22 +1197,19 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
         asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qh), "=l"(qt) : "l"(d.qhead));
         asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qih), "=l"(qit) : "l"(d.qihead));
         if (qt <= qh && qit > qih) {
-          tick = atomicAdd(d.qihead, 1ULL);
-          slot = d.qi + (tick & d.qimask);
+          slot = d.qi + (atomicAdd(d.qihead, 1ULL) & d.qimask);
         } else {
-          tick = atomicAdd(d.qhead, 1ULL);
-          slot = d.q + (tick & d.qmask);
+          slot = d.q + (atomicAdd(d.qhead, 1ULL) & d.qmask);
         }
       }
-      {
-        while ((v = *slot) == QEMPTY) {
-          if (*(volatile int*)&d.done[0] || *(volatile int*)&d.done[1]) { v = QEXIT; break; }
-          if ((++spins & 255) == 0 && *d.hostabort) { *(volatile int*)&d.done[1] = 1; v = QEXIT; break; }
-          __nanosleep(ns);
-          ns = ns < 1024 ? 2 * ns : 1024;
-        }
-        if (v != QEXIT) *slot = QEMPTY;
+      // acquire: the task's producers wrote its state before they queued it
+      while ((v = ld_acquire_u32(slot)) == QEMPTY) {
+        if (*(volatile int*)&d.done[0] || *(volatile int*)&d.done[1]) { v = QEXIT; break; }
+        if ((++spins & 255) == 0 && *d.hostabort) { *(volatile int*)&d.done[1] = 1; v = QEXIT; break; }
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : 1024;
       }
+      if (v != QEXIT) *slot = QEMPTY;
       if (prof) {
         uint64_t w1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));
@@ -1128,11 +1217,9 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
       }
       task_s = v;
     }
-    if (t == 0) {
-      if ((++ntask_local & 15) == 0) {  // watchdogs: task budget, host stop request
-        if (atomicAdd(d.ntask, 16ULL) + 16 >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
-        if ((ntask_local & 255) == 0 && *d.hostabort) *(volatile int*)&d.done[1] = 1;
-      }
+    if (t == 0 && (++ntask_local & 15) == 0) {  // watchdogs: task budget, host stop request, abort
+      if (atomicAdd(d.ntask, 16ULL) + 16 >= (unsigned long long)c.max_tasks) *(volatile int*)&d.done[1] = 1;
+      if ((ntask_local & 255) == 0 && *d.hostabort) *(volatile int*)&d.done[1] = 1;
       // the abort flag is read by thread 0 alone: every thread of the CTA then takes the
       // same decision from task_s (a per-thread read could split the CTA at a barrier)
       if (*(volatile int*)&d.done[1]) task_s = QEXIT;
@@ -1153,8 +1240,9 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     uint64_t w0 = 0;
     __shared__ int drain_s;
     if (t == 0) {
-      if (reqd) c0 = atomicAdd(&d.treq[gt], 0);
-      fence_gpu();  // acquire: the writes of the task's producers
+      // the tile's pending requests at the start (acquire: read before any of its state; the
+      // queue slot was read with acquire, and a continuation was queued by this CTA itself)
+      if (reqd) c0 = ld_acquire_s32(d.treq + gt);
       if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0));
       bc[1] = 0;
       bc[3] = 0;
@@ -1254,7 +1342,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
       uint64_t w0t = 0;
       if (prof && t == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0t));
       const int sfr0 = d.sfr[s];
-      transition(d, io, s, c, bc);
+      transition(d, io, s, c, bc, reinterpret_cast<uint32_t*>(smem), (int)(sizeof(int) * (2 * HS * HS + TPX + K * TPX + K * 64) / 4));
       if (prof && t == 0) {
         uint64_t w1;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1));

@@ -86,9 +86,8 @@ size_t frame_bytes(int K, size_t T) {
   b += T * 128 * 4;               // hedge
   b += 2 * T * K * 64 * 4;        // sent, got
   b += T * K * 64;                // reach
-  b += T * 8 + 12 * T * 4;        // neg0 + tile flags
-  b += T * TPX;                   // m
-  b += 2 * T * 4 * 2;             // queue (capacity >= 2 x tiles in flight)
+  b += T * 8 + 13 * T * 4;        // neg0 + tile flags
+  b += 2 * T * 4 * 2;             // queues (capacity >= 2 x tiles in flight)
   b += 4 * 24 + 8 * 4;            // frame words
   return b + 16 * 256;            // alignment slack
 }
@@ -173,9 +172,9 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.tph = (int32_t*)take(ns * 4);
   d.tminh = (int32_t*)take(ns * 4);
   d.tsk = (int32_t*)take(ns * 4);
-  d.tcs = (int32_t*)take(ns * 4);
+  d.tsrc = (int32_t*)take(ns * 4);
+  d.tss = (int32_t*)take(ns * 4);
   d.tmk = (int32_t*)take(ns * 4);
-  d.m = (uint8_t*)take(ns * TPX);
   d.hostabort = c->habort_dev;
   d.ptiles = c->prof ? c->dtiles : nullptr;
   d.pns = c->prof ? c->dtiles + 6 : nullptr;
@@ -297,6 +296,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   ctl.selfrun = c->selfrun;
   ctl.rounds = c->rounds;
   ctl.nframes = nframes;
+  ctl.K4 = K == 4;
   // int4 loads in the init pass when every caller row is 16-byte aligned
   ctl.vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
             ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
