@@ -207,10 +207,11 @@ def run_reference(args, cfg):
 
 
 def run_warm(args, cfg):
-    """Sequence mode for C3 (BASELINE.json configs[2]): S sequences of L frames; the frames
-    at time t of all sequences are one batch, warm-started from the flows the batch at t-1
-    exported (Kohli-Torr-style reuse).  The same schedule is also run cold.  One
-    step = the L batches of a sequence set; value = warm throughput."""
+    """Sequence mode for C3 (BASELINE.json configs[2]): S sequences of L frames solved in ONE
+    device pass per step through gc_solve_sequences -- a frame slot holds a sequence and frame
+    t is warm-started from the flows frame t-1 exported (Kohli-Torr-style reuse).
+    The same pass is also timed cold (warm=0, same schedule); results must agree.  One step =
+    the S x L frames; value = warm throughput."""
     import torch
 
     import paper_1008_0502_b200 as gc
@@ -230,60 +231,57 @@ def run_warm(args, cfg):
     seed = synth.BASE_SEED + cfg["seed_off"]
     t0, _ = shard.frame_range(rank, world, S * L)  # each rank takes its own S sequences
     cs, ct, nb = synth.gen_torch(cfg["kind"], seed, t0, S * L, H, W, K, device=dev, seq_len=L)
-    # [sequence][time] -> [time][sequence]: the batch of time t is contiguous
-    order = torch.arange(S * L, device=dev).view(S, L).t().reshape(-1)
-    cs, ct, nb = cs[order].contiguous(), ct[order].contiguous(), nb[order].contiguous()
+    cs, ct, nb = (a.view((S, L) + tuple(a.shape[1:])) for a in (cs, ct, nb))
     g = gc.GridCut(neighborhood=K, max_h=H, max_w=W)
-    flow = torch.empty(S, dtype=torch.int64, device=dev)
-    mask = torch.empty((S, H, W), dtype=torch.uint8, device=dev)
+    flow = torch.empty((S, L), dtype=torch.int64, device=dev)
+    mask = torch.empty((S, L, H, W), dtype=torch.uint8, device=dev)
+    flow_c = torch.empty_like(flow)
+    mask_c = torch.empty_like(mask)
     stream = torch.cuda.current_stream(dev)
 
-    def sweep(warm):
-        prev, launches = None, 0
-        Fs = []
-        for t in range(L):
-            sl = slice(t * S, (t + 1) * S)
-            res = g.solve(cs[sl], ct[sl], nb[sl], warm_flow=prev if warm else None, flow_state=warm, out=(flow, mask))
-            if warm:
-                prev = res[2]
-            Fs.append(flow.clone())
-            launches += g.launches()
-        return torch.stack(Fs), launches
-
     for _ in range(args.warmup):
-        sweep(True)
-        sweep(False)
+        g.solve_sequences(cs, ct, nb, warm=True, out=(flow, mask))
+        g.solve_sequences(cs, ct, nb, warm=False, out=(flow_c, mask_c))
     torch.cuda.synchronize()
 
-    def timed(warm):
+    def timed(warm, out):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches = 0
+        g.kernel_ms(reset=True)
         e0.record(stream)
         for _ in range(args.steps):
-            F, nl = sweep(warm)
-            launches += nl
+            g.solve_sequences(cs, ct, nb, warm=warm, out=out)
+            launches += g.launches()
         e1.record(stream)
         torch.cuda.synchronize()
-        return shard.max_over_ranks(e0.elapsed_time(e1), dev, world), F, launches
+        return shard.max_over_ranks(e0.elapsed_time(e1), dev, world), launches, g.kernel_ms(reset=True)
 
     clk = ClockSampler(None)
     clk.start()
     time.sleep(0.3)
-    ms_w, Fw, lw = timed(True)
-    ms_c, Fc, _ = timed(False)
+    ms_w, lw, kw = timed(True, (flow, mask))
+    ms_c, _, kc = timed(False, (flow_c, mask_c))
     clocks = clk.stop()
-    assert torch.equal(Fw, Fc), "warm-started flow values differ from cold ones"
+    assert torch.equal(flow, flow_c) and torch.equal(mask, mask_c), "warm-started results differ from cold ones"
     px = world * S * L * H * W * args.steps
+    peak, peak_src = load_peak()
+    wb = compulsory_bytes_per_px(K, warm=True)  # + the warm flows read and written per frame
     if rank == 0:
         out = {"metric": METRIC, "value": round(px / (ms_w * 1e-3) / 1e6, 1), "unit": "Mpixel/s", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_w / args.steps, 3),
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
                "data": "synthetic (seeded saliency-blob sequences, synth/; generated on device before timing)",
-               "config": {"workload": f"{cfg['workload']}: {S} sequences x {L} frames, frame t warm-started from "
-                                      f"t-1 (batch = the {S} frames of one time step)",
+               "config": {"workload": f"{cfg['workload']}: {S} sequences x {L} frames in one gc_solve_sequences "
+                                      f"pass, frame t warm-started from t-1",
                           "H": H, "W": W, "K": K, "sequences_per_rank": S, "seq_len": L,
-                          "parallelism": f"sequence-sharded dp{world}"},
+                          "parallelism": f"sequence-sharded dp{world}",
+                          "l2": f"inputs {S * L * H * W * 4 * (2 + K) / 1e9:.1f} GB per rank >> 126 MB L2"},
                "fps": round(world * S * L * args.steps / (ms_w * 1e-3), 1),
+               "roofline": {"bound": "hbm", "kernel": f"k_solve<{K}>", "unit": "GB/s", "peak": peak,
+                            "achieved": round(wb * S * L * H * W * args.steps / (kw * 1e-3) / 1e9, 1),
+                            "frac": round(wb * S * L * H * W * args.steps / (kw * 1e-3) / 1e9 / peak, 4),
+                            "bytes_rule": f"{wb} B/px (caps + 2 warm-flow planes read, mask + 2 flow planes written)",
+                            "avg_launch_ms": round(kw / args.steps, 4), "traffic": None, "peak_source": peak_src},
                "cold_same_schedule": {"value": round(px / (ms_c * 1e-3) / 1e6, 1), "unit": "Mpixel/s",
                                       "ms_per_step": round(ms_c / args.steps, 3)},
                "warm_speedup": round(ms_c / ms_w, 3), "warm_equals_cold": True,

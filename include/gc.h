@@ -104,6 +104,30 @@ typedef struct {
 /* Device-pointer entry point.  `stream` is a cudaStream_t (NULL = legacy default). */
 gc_status gc_solve_batch(gc_ctx* ctx, const gc_batch* batch, void* stream);
 
+/* Video sequences (BASELINE config C3; Kohli-Torr-style dynamic cuts): S sequences of
+ * L frames each, frame index f = j * L + t (sequence j, time t), every array laid out like
+ * gc_batch's with n = S * L.  The whole set is ONE device pass: a frame slot holds a sequence
+ * and, when frame t is solved, takes frame t+1 of the same sequence -- warm-started (warm != 0)
+ * from the forward-arc flows frame t just exported, which the context keeps on the device
+ * (clamped to the new capacities exactly as gc_batch.warm_flow is, so F and mask equal a cold
+ * solve of every frame); warm == 0 runs the same schedule cold.  Results are F and the
+ * canonical mask of every frame, as gc_solve_batch defines them.  Device pointers; errors as
+ * gc_solve_batch (GC_ERR_ARG: S < 0, L <= 0, bad H/W, NULL required pointer). */
+typedef struct {
+  int S, L, H, W;
+  const int32_t* cap_s;      /* [S][L][H][W]                                                 */
+  const int32_t* cap_t;      /* [S][L][H][W]                                                 */
+  const int32_t* cap_nb;     /* [S][L][K][H][W]                                              */
+  const int32_t* warm_flow;  /* NULL, or [S][K/2][H][W]: warm start of each sequence's frame 0 */
+  int64_t* flow_out;         /* [S][L]                                                       */
+  uint8_t* mask_out;         /* [S][L][H][W]                                                 */
+  int32_t* flow_state_out;   /* NULL, or [S][K/2][H][W]: the flows of each sequence's last
+                                frame (to continue the sequences in a later call)           */
+  int32_t* stats_out;        /* NULL, or [S][L][4] as gc_batch.stats_out                     */
+  int warm;                  /* 1: frame t >= 1 warm-started from frame t-1; 0: all cold     */
+} gc_seq_batch;
+gc_status gc_solve_sequences(gc_ctx* ctx, const gc_seq_batch* batch, void* stream);
+
 /* Host-pointer entry point: same semantics; the library copies inputs to the device and
  * results back, in chunks, on `stream`.  All pointers in *batch are host pointers. */
 gc_status gc_solve_batch_host(gc_ctx* ctx, const gc_batch* batch, void* stream);

@@ -15,7 +15,7 @@ import os
 
 import numpy as np
 
-__all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host",
+__all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_solve_sequences",
            "gc_frame_digest", "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "CAP_MAX",
            "STATUS", "lib_path"]
 
@@ -44,12 +44,21 @@ class gc_batch(ctypes.Structure):
                 ("flow_state_out", ctypes.c_void_p), ("stats_out", ctypes.c_void_p)]
 
 
+class gc_seq_batch(ctypes.Structure):
+    _fields_ = [("S", ctypes.c_int), ("L", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int),
+                ("cap_s", ctypes.c_void_p), ("cap_t", ctypes.c_void_p), ("cap_nb", ctypes.c_void_p),
+                ("warm_flow", ctypes.c_void_p), ("flow_out", ctypes.c_void_p), ("mask_out", ctypes.c_void_p),
+                ("flow_state_out", ctypes.c_void_p), ("stats_out", ctypes.c_void_p), ("warm", ctypes.c_int)]
+
+
 _lib.gc_create.argtypes = [ctypes.POINTER(gc_config), ctypes.POINTER(ctypes.c_void_p)]
 _lib.gc_create.restype = ctypes.c_int
 _lib.gc_destroy.argtypes = [ctypes.c_void_p]
 _lib.gc_destroy.restype = None
 _lib.gc_solve_batch.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_batch), ctypes.c_void_p]
 _lib.gc_solve_batch.restype = ctypes.c_int
+_lib.gc_solve_sequences.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_seq_batch), ctypes.c_void_p]
+_lib.gc_solve_sequences.restype = ctypes.c_int
 _lib.gc_solve_batch_host.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_batch), ctypes.c_void_p]
 _lib.gc_solve_batch_host.restype = ctypes.c_int
 _lib.gc_last_error.argtypes = [ctypes.c_void_p]
@@ -70,7 +79,8 @@ _lib.gc_frame_digest.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ct
 _lib.gc_frame_digest.restype = ctypes.c_int
 
 EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
-            "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "gc_frame_digest")
+            "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "gc_frame_digest",
+            "gc_solve_sequences")
 
 
 class GcError(RuntimeError):
@@ -93,6 +103,10 @@ def gc_destroy(ctx) -> None:
 
 def gc_solve_batch(ctx, batch: gc_batch, stream: int) -> int:
     return _lib.gc_solve_batch(ctx, ctypes.byref(batch), ctypes.c_void_p(stream))
+
+
+def gc_solve_sequences(ctx, batch: gc_seq_batch, stream: int) -> int:
+    return _lib.gc_solve_sequences(ctx, ctypes.byref(batch), ctypes.c_void_p(stream))
 
 
 def gc_solve_batch_host(ctx, batch: gc_batch, stream: int) -> int:
@@ -208,6 +222,37 @@ class GridCut:
                      _ptr(fs), _ptr(stt))
         s = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
         self.last_status = self._check(gc_solve_batch(self.ctx, b, s), allow)
+        res = [flow, mask]
+        if flow_state:
+            res.append(fs)
+        if stats:
+            res.append(stt)
+        return tuple(res)
+
+    def solve_sequences(self, cap_s, cap_t, cap_nb, warm=True, warm_flow=None, flow_state=False, stats=False,
+                        stream=None, allow=(), out=None):
+        """S sequences of L frames in one device pass (gc_solve_sequences): cap_s, cap_t
+        [S, L, H, W], cap_nb [S, L, K, H, W] int32 CUDA tensors; frame t >= 1 of a sequence is
+        warm-started from frame t-1's flows when `warm`.  Returns flow [S, L] int64 and mask
+        [S, L, H, W] uint8 (+ the last frames' flow state [S, K/2, H, W], + stats [S, L, 4])."""
+        import torch
+        S, L, H, W = cap_s.shape
+        K = self.K
+        assert cap_nb.shape == (S, L, K, H, W), cap_nb.shape
+        for t in (cap_s, cap_t, cap_nb) + ((warm_flow,) if warm_flow is not None else ()):
+            assert t.dtype == torch.int32 and t.is_cuda and t.is_contiguous()
+        dev = cap_s.device
+        if out is None:
+            flow = torch.empty((S, L), dtype=torch.int64, device=dev)
+            mask = torch.empty((S, L, H, W), dtype=torch.uint8, device=dev)
+        else:
+            flow, mask = out
+        fs = torch.empty((S, K // 2, H, W), dtype=torch.int32, device=dev) if flow_state else None
+        stt = torch.empty((S, L, 4), dtype=torch.int32, device=dev) if stats else None
+        b = gc_seq_batch(S, L, H, W, _ptr(cap_s), _ptr(cap_t), _ptr(cap_nb), _ptr(warm_flow), _ptr(flow), _ptr(mask),
+                         _ptr(fs), _ptr(stt), int(bool(warm)))
+        s = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
+        self.last_status = self._check(gc_solve_sequences(self.ctx, b, s), allow)
         res = [flow, mask]
         if flow_state:
             res.append(fs)

@@ -49,6 +49,7 @@ __host__ __device__ constexpr int DXk(int k) {
 struct Dev {
   int H, W, TY, TX, T, nslot;
   int initg;  // tiles per init task
+  int bulkg;  // tiles per seed / closure-seed task (1, 2, 4 or 8)
   int hmax;  // relabel cap: heights >= hmax are unreachable (HINF)
   int32_t* e;
   int32_t* h;
@@ -82,6 +83,10 @@ struct Dev {
   int32_t* tsk;     // [NS]   global relabel (fbe) in which the tile's seed was skipped (its
                     //        border heights, all 1 in frame, are final for that relabel)
   // per frame slot (state machine): zero-initialised by one memset
+  const int32_t** swf;  // [nslot] warm-start flows of the slot's frame ([K/2][H][W]) or NULL
+  int32_t** sfs;        // [nslot] where the slot's frame exports its flows ([K/2][H][W]) or NULL
+  int32_t* fbuf;        // sequence mode, warm: [nslot][2][K/2][H][W] ping-pong flow buffers (frame
+                        // t exports into buffer t & 1, frame t+1 starts from it)
   int32_t* fmode;   // [nslot] M_INIT, M_SEED, M_BFS, M_PUSH, M_CSEED, M_CLOS, M_IDLE
   int32_t* sfr;     // [nslot] batch frame index held by the slot
   int32_t* fout;    // [nslot] tasks of the running phase queued or running
@@ -314,7 +319,7 @@ __device__ __forceinline__ void tile_from_caps(const Dev& d, const IO& io, int s
   const int32_t* cs = io.cs + f * plane;
   const int32_t* ct = io.ct + f * plane;
   const int32_t* nb = io.nb + f * plane * K;
-  const int32_t* wf = io.wf ? io.wf + f * plane * (K / 2) : nullptr;
+  const int32_t* wf = d.swf[s];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
@@ -437,7 +442,7 @@ __device__ __forceinline__ void px_er(const Dev& d, const IO& io, size_t gt, int
   const size_t plane = (size_t)H * W;
   const size_t f = (size_t)d.sfr[s];
   const int32_t* nb = io.nb + f * plane * K;
-  const int32_t* wf = io.wf ? io.wf + f * plane * (K / 2) : nullptr;
+  const int32_t* wf = d.swf[s];
   const bool in = y < H && x < W;
   const size_t o = (size_t)y * W + x;
   e = in ? __ldg(io.cs + f * plane + o) - __ldg(io.ct + f * plane + o) : 0;
@@ -475,6 +480,7 @@ struct FramePtrs {
   const int32_t* ct;
   const int32_t* nb;
   const int32_t* wf;
+  int32_t* fs;
 };
 __device__ __forceinline__ FramePtrs frame_ptrs(const Dev& d, const IO& io, int s, int K) {
   const size_t plane = (size_t)d.H * d.W;
@@ -484,7 +490,8 @@ __device__ __forceinline__ FramePtrs frame_ptrs(const Dev& d, const IO& io, int 
   p.cs = io.cs + fr * plane;
   p.ct = io.ct + fr * plane;
   p.nb = io.nb + fr * plane * K;
-  p.wf = io.wf ? io.wf + fr * plane * (K / 2) : nullptr;
+  p.wf = d.swf[s];
+  p.fs = d.sfs[s];
   return p;
 }
 
@@ -537,7 +544,7 @@ __device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int H = d.H, W = d.W;
   const int ix = t & 31, iy0 = t >> 5;
-  if (vec && !io.wf) {  // cold, aligned rows: the init pass's loads (row t/8, columns 4(t%8)..+3)
+  if (vec && !d.swf[s]) {  // cold, aligned rows: the init pass's loads (row t/8, columns 4(t%8)..+3)
     const FramePtrs P = frame_ptrs(d, io, s, K);
     int a[4], b[4], c[K][4];
     init_load<K>(d, P, ty, tx, true, a, b, c);
@@ -571,7 +578,7 @@ __device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_
   const int32_t* cs = io.cs + f * plane;
   const int32_t* ct = io.ct + f * plane;
   const int32_t* nb = io.nb + f * plane * K;
-  const int32_t* wf = io.wf ? io.wf + f * plane * (K / 2) : nullptr;
+  const int32_t* wf = d.swf[s];
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
     const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix, lp = (iy0 + 8 * j) * TS + ix;
@@ -756,7 +763,7 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
       uni &= ev < 0;
       src &= ev > 0;
       if (EXPORT) {  // a5: the export of a tile no push ever touches is its initial flow
-        int32_t* fo = io.fstate + fr * plane * (K / 2) + o0 + i;
+        int32_t* fo = P.fs + o0 + i;
 #pragma unroll
         for (int k = 0; k < K / 2; ++k) fo[k * plane] = fw[k];
       }
@@ -798,7 +805,8 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
 }
 
 // Per-tile results of an init group, after a barrier: tile words, frame sums, range flag,
-// and the border heights of uniform sink tiles (h = 1 in frame).
+// and the border heights of uniform sink tiles (h = 1 in frame).  uni_s[i]: bit 0 uniform
+// sink, bit 1 uniform source (the fused seed of the first relabel skips both).
 __device__ __forceinline__ void init_finalize(const Dev& d, size_t gt0, int n, const InitPart* part, int* uni_s) {
   const int t = threadIdx.x;
   const int s = (int)((unsigned)gt0 / (unsigned)d.T);
@@ -813,7 +821,6 @@ __device__ __forceinline__ void init_finalize(const Dev& d, size_t gt0, int n, c
     if (sb) atomicAdd(&d.sumneg[s], (unsigned long long)sb);  // corrected by the closure seed if e changes
     d.neg0[gt] = sb;
     d.mat[gt] = 0;
-    d.flag[gt] = 0;
     d.recv1[gt] = 0;
     d.tact[gt] = 0;
     d.tuni[gt] = uni;
@@ -822,13 +829,13 @@ __device__ __forceinline__ void init_finalize(const Dev& d, size_t gt0, int n, c
     d.tph[gt] = -1;
     d.tmk[gt] = 0;
     d.tsk[gt] = 0;  // relabel epochs restart at 1 per frame: a stale stamp would alias
-    d.tss[gt] = 0;
+    d.tss[gt] = src ? 1 : 0;  // the first relabel (epoch 1) does not seed a uniform source tile
     if (f & 1) d.ferr[s] = 1;
-    uni_s[t] = uni;
+    uni_s[t] = uni | (src << 1);
   }
   __syncthreads();
   for (int j = 0; j < n; ++j) {
-    if (!uni_s[j] || t >= 128) continue;
+    if (!(uni_s[j] & 1) || t >= 128) continue;
     const int tile = (int)(gt0 + j - (size_t)s * d.T);
     const int ty = tile / d.TX, tx = tile - ty * d.TX;
     const int side = t >> 5, i = t & 31;
@@ -905,7 +912,7 @@ __device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0
         const int tile = tile0 + i + 1;
         init_prefetch<K>(d, P, tile / d.TX, tile % d.TX, pf);
       }
-      if (io.fstate) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
+      if (P.fs) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
       else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i);
     }
   } else {
@@ -913,9 +920,9 @@ __device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0
     for (int i = 0; i < n; ++i) {
       const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
       init_load<K>(d, P, ty, tx, vec, a, b, c);
-      if (P.wf && io.fstate) tile_init_regs<K, true, true>(d, io, gt0 + i, P, a, b, c, part + i);
+      if (P.wf && P.fs) tile_init_regs<K, true, true>(d, io, gt0 + i, P, a, b, c, part + i);
       else if (P.wf) tile_init_regs<K, true, false>(d, io, gt0 + i, P, a, b, c, part + i);
-      else if (io.fstate) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
+      else if (P.fs) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
       else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i);
     }
   }

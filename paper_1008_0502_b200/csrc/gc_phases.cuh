@@ -60,7 +60,39 @@ struct Ctl {
   int nframes;
   int vec;                   // caller rows 16-byte aligned: int4 loads in the init pass
   int K4;                    // 4-neighbour frames (no diagonal arcs)
+  int seqL;                  // sequence mode (gc_solve_sequences): frames per sequence; 0: batch
+  int seqS;                  // sequence mode: number of sequences
+  int seqWarm;               // sequence mode: frame t >= 1 warm-started from frame t-1's flows
 };
+
+// Slot s takes batch frame f: its frame index and where its warm-start flows come from and
+// its exported flows go.  Batch mode: the caller's warm_flow / flow_state_out planes of frame
+// f.  Sequence mode (f = j * L + t): frame 0 of sequence j starts from the caller's
+// warm_flow[j] (or cold); frame t >= 1 from the ping-pong buffer frame t-1 exported into
+// (warm) or cold; frame t exports into buffer t & 1, the last frame into flow_state_out[j].
+// Distance bound of a global relabel after `ce` failed certificate attempts: 2 + 2^(1 +
+// bndsh x ce) (HINF -- exact -- once that exceeds any distance in the frame).
+__device__ __forceinline__ int relabel_bound(const Dev& d, const Ctl& c, int ce) {
+  const int sh = min(ce * c.bndsh, 30);
+  return (sh >= 24 || (2ll << sh) >= d.hmax) ? HINF : 2 + (2 << sh);
+}
+
+__device__ __forceinline__ void slot_assign(const Dev& d, const IO& io, const Ctl& c, int s, int f) {
+  const size_t pl = (size_t)d.H * d.W * (c.K4 ? 2 : 4);
+  d.sfr[s] = f;
+  d.fbe[s] = 1;  // the frame's first global relabel is seeded by its init tasks
+  d.fbnd[s] = relabel_bound(d, c, 0);
+  if (!c.seqL) {
+    d.swf[s] = io.wf ? io.wf + (size_t)f * pl : nullptr;
+    d.sfs[s] = io.fstate ? io.fstate + (size_t)f * pl : nullptr;
+    return;
+  }
+  const int j = f / c.seqL, tt = f - j * c.seqL;
+  int32_t* buf = d.fbuf + (size_t)s * 2 * pl;
+  d.swf[s] = tt == 0 ? (io.wf ? io.wf + (size_t)j * pl : nullptr) : (c.seqWarm ? buf + ((tt - 1) & 1) * pl : nullptr);
+  d.sfs[s] = tt == c.seqL - 1 ? (io.fstate ? io.fstate + (size_t)j * pl : nullptr)
+                              : (c.seqWarm ? buf + (tt & 1) * pl : nullptr);
+}
 
 // ------------------------------------------------------------------ queue primitives
 // Release/acquire fence at GPU scope (cheaper than __threadfence's sequentially consistent
@@ -95,7 +127,6 @@ __device__ __forceinline__ void qi_put(const Dev& d, unsigned long long p, uint3
 __device__ __forceinline__ uint32_t qent(int md, size_t gt, int cnt = 1) {
   return ((uint32_t)md << 28) | ((uint32_t)(cnt - 1) << 24) | (uint32_t)gt;
 }
-constexpr int BULK_G = 8;  // tiles per seed / closure-seed task
 
 // Neighbour tile of gt on side b (0 N, 1 S, 2 W, 3 E, 4 NW, 5 NE, 6 SW, 7 SE); -1 if off-frame.
 __device__ __forceinline__ long long side_tile(const Dev& d, size_t gt, int b) {
@@ -561,7 +592,7 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
   // a5: a tile a push touched exports its forward-arc flows here (the init pass wrote every
   // other tile's); a failed attempt's export is rewritten by the next attempt, which
   // closure-seeds every materialised tile again
-  if (io.fstate && mat) task_export<K>(d, io, gt);
+  if (mat && d.sfs[s]) task_export<K>(d, io, gt);
 }
 
 // ---------------------------------------------------------------- a4: closure relax (one tile)
@@ -635,6 +666,7 @@ __device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t g
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const size_t fr = (size_t)d.sfr[s];
+  int32_t* fsp = d.sfs[s];
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
     const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
@@ -647,7 +679,7 @@ __device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t g
       const int y2 = y + DYk(k), x2 = x + DXk(k);
       int f = 0;
       if (y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = io.nb[fr * plane * K + k * plane + o] - r[k];
-      io.fstate[fr * plane * (K / 2) + (k >> 1) * plane + o] = f;
+      fsp[(k >> 1) * plane + o] = f;
     }
   }
 }
@@ -917,6 +949,67 @@ __device__ __forceinline__ void task_push(const Dev& d, const IO& io, size_t gt,
   }
 }
 
+// ---------------------------------------------------------------- a2 fused into a1
+// The seed of the frame's first global relabel (epoch 1, bound fbnd), run by the init task
+// for the tiles of its group that are neither uniform sink nor uniform source (those are
+// never seeded: h = 1 published at init / h = HINF by their tss stamp): h = 1 on nodes with
+// e < 0, tile-local BFS fixpoint with an INF halo (the relax phase brings the neighbours'
+// heights in: the neighbours that see a finite border height are flagged here, the tiles
+// next to a uniform sink tile by the INIT -> BFS transition).  fl was written by this CTA.
+template <int K>
+__device__ void init_seed_group(const Dev& d, size_t gt0, int* smem) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  const int s = (int)((unsigned)gt0 / (unsigned)d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
+  const int n = min(d.initg, d.T - tile0);
+  const int* uni_s = reinterpret_cast<const int*>(reinterpret_cast<const InitPart*>(smem) + INIT_GMAX);
+  int* hs = const_cast<int*>(uni_s) + INIT_GMAX;  // [HS * HS]
+  int* sc = hs + HS * HS;                         // scratch [4]
+  const int bnd = __ldcg(d.fbnd + s);
+  for (int j = 0; j < n; ++j) {
+    if (uni_s[j]) continue;
+    const size_t gt = gt0 + j;
+    __syncthreads();  // hs / sc of the previous tile consumed
+    int fl[4], h[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) fl[q] = __ldcg(d.fl + gt * TPX + (iy0 + 8 * q) * TS + ix);
+    for (int i = t; i < HS * HS; i += NTH) hs[i] = HINF;
+    if (t == 0) { sc[0] = 0; sc[1] = HINF; }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      h[q] = (fl[q] & FL_NEG) ? 1 : HINF;
+      hs[hidx(iy0 + 8 * q, ix)] = h[q];
+    }
+    __syncthreads();
+    bfs_fixpoint<K>(hs, fl, h, bnd);
+    int act = 0, fix = 1, bits = 0, mnh = HINF;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int iy = iy0 + 8 * q;
+      d.h[gt * TPX + iy * TS + ix] = h[q];
+      act |= (fl[q] & FL_POS) && h[q] < HINF;
+      if (fl[q] & FL_POS) mnh = min(mnh, h[q]);
+      fix &= (h[q] == 1) || !(fl[q] & 0xff);
+      if (on_border(iy, ix) && h[q] < HINF) bits |= border_bits(iy, ix);
+    }
+    store_hedge(d, gt, h, t);
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    mnh = __reduce_min_sync(0xffffffffu, mnh);
+    if ((t & 31) == 0) {
+      if (bits) atomicOr(&sc[0], bits);
+      atomicMin(&sc[1], mnh);
+    }
+    act = __syncthreads_or(act);
+    fix = __syncthreads_and(fix);
+    if (t == 0) {
+      d.tact[gt] = act;
+      d.tminh[gt] = sc[1];
+      d.tfix[gt] = fix;
+    }
+    flag_sides(d, gt, sc[0], K);
+  }
+}
+
 // ---------------------------------------------------------------- transitions
 // first task set of a phase: NONE = the slot idles; EMPTY = no task (the next transition
 // follows at once)
@@ -976,8 +1069,11 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       int* st = d.fstat + s * 4;
       bool finished = false;
       if (md == M_INIT) {
-        nm = d.ferr[s] ? M_CSEED : M_SEED;
-        kind = d.ferr[s] ? SET_ALL : SET_SEED;  // range error: the closure seeds zero the mask
+        // the init tasks seeded the first global relabel (init_seed_group): straight to its
+        // relax phase; range error: the closure seeds zero the mask
+        nm = d.ferr[s] ? M_CSEED : M_BFS;
+        kind = d.ferr[s] ? SET_ALL : SET_FLAG;
+        if (!d.ferr[s]) st[1] += 1;
       } else if (md == M_SEED) {
         nm = M_BFS;
         kind = SET_FLAG;
@@ -1028,21 +1124,34 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       }
       if (finished) {
         finish_frame(d, io, s, c);
-        const int nf = atomicAdd(&d.gctr[0], 1);
-        if (nf < c.nframes) {  // refill the slot with the next frame of the batch
-          d.sfr[s] = nf;
+        // refill the slot: the next frame of the batch, or in sequence mode the next frame of
+        // the slot's sequence, then the first frame of the next sequence not started
+        int nf;
+        if (c.seqL) {
+          const int f = d.sfr[s];
+          if ((f + 1) % c.seqL != 0) {
+            nf = f + 1;
+          } else {
+            const int j = atomicAdd(&d.gctr[0], 1);
+            nf = j < c.seqS ? j * c.seqL : c.nframes;
+          }
+        } else {
+          nf = atomicAdd(&d.gctr[0], 1);
+        }
+        if (nf < c.nframes) {
+          slot_assign(d, io, c, s, nf);
           d.ferr[s] = 0;
           d.fph[s] = 0; d.fvis[s] = 0; d.fprog[s] = 0;
           st[0] = st[1] = st[2] = st[3] = 0;
           d.frel[s] = 0; d.sumct[s] = 0; d.sumneg[s] = 0;
-          d.cep[s] = 0; d.cfail[s] = 0; d.fdrain[s] = 0; d.fbe[s] = 0;
+          d.cep[s] = 0; d.cfail[s] = 0; d.fdrain[s] = 0;  // (fbe, fbnd: slot_assign)
           nm = M_INIT;
           kind = SET_INITG;
         } else {
           nm = M_IDLE;
           kind = SET_NONE;
-          if (nf == c.nframes) {  // no init group will be queued any more: release the CTAs
-            // parked on the init ring (tickets beyond its tail), one no-op entry each
+          {  // a slot goes idle: release the CTAs parked on the init ring (tickets beyond its
+             // tail; in batch mode no init group will be queued any more), one no-op entry each
             const unsigned long long ih = atomicAdd(d.qihead, 0ULL), it = atomicAdd(d.qitail, 0ULL);
             const unsigned parked = ih > it ? (unsigned)min(ih - it, (unsigned long long)gridDim.x) : 0u;
             if (parked) {
@@ -1052,11 +1161,9 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           }
         }
       }
-      if (nm == M_SEED) {  // a new global relabel, bounded: distances up to 2 + 2^(bndsh x attempts + 1)
-        d.fbe[s] += 1;     // (HINF once that exceeds any distance in the frame)
-        const int ce = d.cep[s];
-        const int sh = min(ce * c.bndsh, 30);
-        d.fbnd[s] = (sh >= 24 || (2ll << sh) >= d.hmax) ? HINF : 2 + (2 << sh);
+      if (nm == M_SEED) {  // a new global relabel, bounded (relabel_bound)
+        d.fbe[s] += 1;
+        d.fbnd[s] = relabel_bound(d, c, d.cep[s]);
       }
       bc[3] = d.fbe[s];
       d.fmode[s] = nm;
@@ -1072,10 +1179,14 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     // tiles has nothing to do (its closure is the whole tile, its mask bytes are written, and
     // no border arc reaches a pixel that is not an excess node) -- a bit per tile of tsrc
     const bool srcskip = kind == SET_CSEED && (d.T + 31) / 32 <= sbits_words;
-    if (srcskip) {
+    // the first relabel's relax phase: a tile next to a uniform sink tile is relaxed (its fused
+    // seed had an INF halo) -- a bit per tile of tuni
+    const bool unibits = kind == SET_FLAG && md == M_INIT;
+    if (srcskip || unibits) {
       for (int b0 = 0; b0 < d.T; b0 += NTH) {
         const int i = b0 + t;
-        const unsigned bal = __ballot_sync(0xffffffffu, i < d.T && __ldcg(d.tsrc + base_gt + i) != 0);
+        const int32_t* w = srcskip ? d.tsrc : d.tuni;
+        const unsigned bal = __ballot_sync(0xffffffffu, i < d.T && __ldcg(w + base_gt + i) != 0);
         if ((t & 31) == 0 && i < d.T + 31) sbits[i >> 5] = bal;
       }
       __syncthreads();
@@ -1085,7 +1196,10 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       int want = 0;
       if (i < d.T) {
         const size_t gt = base_gt + i;
-        if (kind == SET_ALL) want = 1;
+        if (kind == SET_ALL) {
+          want = 1;
+          d.flag[gt] = 0;
+        }
         else if (kind == SET_INITG) want = (i % d.initg) == 0;  // one init task per tile group
         else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1, uniform source
           const int tu = __ldcg(d.tuni + gt), tsr = __ldcg(d.tsrc + gt), r1 = __ldcg(d.recv1 + gt);
@@ -1117,20 +1231,32 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         } else if (kind == SET_FLAG) {
           want = __ldcg(d.flag + gt);
           if (want) d.flag[gt] = 0;
-          if (md == M_SEED && __ldcg(d.tfix + gt)) want = 0;  // a relax cannot change it
+          if (unibits && !((sbits[i >> 5] >> (i & 31)) & 1)) {
+            const int ty = i / d.TX, tx = i - ty * d.TX;
+            for (int dy = -1; dy <= 1; ++dy)
+              for (int dx = -1; dx <= 1; ++dx) {
+                const int ny = ty + dy, nx = tx + dx;
+                if ((dy == 0 && dx == 0) || ny < 0 || ny >= d.TY || nx < 0 || nx >= d.TX) continue;
+                if (dy != 0 && dx != 0 && c.K4) continue;  // no diagonal arcs
+                const int n = ny * d.TX + nx;
+                want |= (sbits[n >> 5] >> (n & 31)) & 1;
+              }
+          }
+          if ((md == M_SEED || md == M_INIT) && __ldcg(d.tfix + gt)) want = 0;  // a relax cannot change it
         }
         else want = __ldcg(d.tact + gt) && __ldcg(d.tminh + gt) <= hcap;
         if (want && (kind == SET_FLAG || kind == SET_TACT)) d.treq[gt] = 1;
       }
-      // seed / closure-seed tasks take groups of BULK_G consecutive tiles (the task skips
+      // seed / closure-seed tasks take groups of d.bulkg consecutive tiles (the task skips
       // the tiles of its group that are not in the set): the group leader enqueues
-      const bool grouped = kind == SET_SEED || kind == SET_CSEED;
+      const bool grouped = (kind == SET_SEED || kind == SET_CSEED) && d.bulkg > 1;
       int gcnt = 1;
       if (grouped) {
+        const int bg = d.bulkg;
         const unsigned bal = __ballot_sync(0xffffffffu, want);
-        const int lane = t & 31, lead = lane & ~(BULK_G - 1);
-        want = (lane == lead) && ((bal >> lead) & ((1u << BULK_G) - 1));
-        gcnt = min(BULK_G, d.T - i);
+        const int lane = t & 31, lead = lane & ~(bg - 1);
+        want = (lane == lead) && ((bal >> lead) & ((1u << bg) - 1));
+        gcnt = min(bg, d.T - i);
       }
       if (t == 0) bc[5] = 0;
       __syncthreads();
@@ -1250,7 +1376,11 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     __syncthreads();
     int cls = 0;
     switch (md) {
-      case M_INIT: task_init<K>(d, io, gt, c.vec != 0, smem); cls = 0; break;
+      case M_INIT:
+        task_init<K>(d, io, gt, c.vec != 0, smem);
+        init_seed_group<K>(d, gt, smem);
+        cls = 0;
+        break;
       case M_SEED:
         for (int j = 0; j < gcnt; ++j) {
           if (j) __syncthreads();
@@ -1368,14 +1498,14 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
 // fit the slots (no refills) then never uses the init ring, whose non-blocking claim lets
 // idle CTAs overshoot it (C3 sequence steps of 8 VGA frames: 4x slower with the initial
 // groups on the init ring).
-__global__ void k_setup(Dev d, int nframes) {
+__global__ void k_setup(Dev d, IO io, Ctl c) {
   const int G = (d.T + d.initg - 1) / d.initg;  // init tasks per frame
   const size_t ntask = (size_t)d.nslot * G;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ntask; i += (size_t)gridDim.x * blockDim.x) {
     const size_t s = i / G, g = i - s * G;
     d.q[i] = qent(M_INIT, s * d.T + g * d.initg);
     if (g == 0) {
-      d.sfr[s] = (int)s;
+      slot_assign(d, io, c, (int)s, c.seqL ? (int)s * c.seqL : (int)s);  // slot s: frame s / sequence s
       d.fmode[s] = M_INIT;
       d.fout[s] = G;
     }
@@ -1386,20 +1516,19 @@ __global__ void k_setup(Dev d, int nframes) {
   }
 }
 
-// Aborted (watchdog / host timeout): frames not finished get F = -1, status GC_ERR_NOCONV.
+// Aborted (watchdog / host timeout): frames not finished get F = -1, status GC_ERR_NOCONV
+// (flow_out was preset to -1 and stats to 0 before the launch: a frame still reading -1 with
+// status 0 did not finish); the frames in progress report their counters so far.
 __global__ void k_abort(Dev d, IO io, int nframes) {
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < d.nslot; s += gridDim.x * blockDim.x) {
-    if (d.fmode[s] == M_IDLE) continue;
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  for (int s = i0; s < d.nslot; s += stride) {
+    if (d.fmode[s] == M_IDLE || !io.stats) continue;
     const int f = d.sfr[s];
-    io.flow[f] = -1;
-    if (io.stats) {  // the counters so far (push tasks, global relabels, BFS relax tasks)
-      for (int i = 0; i < 3; ++i) io.stats[f * 4 + i] = d.fstat[s * 4 + i];
-      io.stats[f * 4 + 3] = 5;
-    }
+    for (int i = 0; i < 3; ++i) io.stats[f * 4 + i] = d.fstat[s * 4 + i];
   }
-  const int first = d.gctr[0];
-  for (int f = first + blockIdx.x * blockDim.x + threadIdx.x; f < nframes; f += gridDim.x * blockDim.x) {
-    io.flow[f] = -1;
+  for (int f = i0; f < nframes; f += stride) {
+    if (io.flow[f] != -1) continue;
+    if (io.stats && io.stats[f * 4 + 3] == 2) continue;  // range error: finished
     if (io.stats) io.stats[f * 4 + 3] = 5;
   }
 }

@@ -60,6 +60,8 @@ struct gc_ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr};       // staging buffer b filled
   cudaEvent_t ev_free[2] = {nullptr, nullptr};     // staging buffer b solved and read back
   size_t words_bytes = 0;
+  int32_t* fbuf = nullptr;  // sequence mode: ping-pong flow buffers of the slots
+  size_t fbuf_bytes = 0;
 };
 
 namespace {
@@ -88,7 +90,7 @@ size_t frame_bytes(int K, size_t T) {
   b += T * K * 64;                // reach
   b += T * 8 + 13 * T * 4;        // neg0 + tile flags
   b += 2 * T * 4 * 2;             // queues (capacity >= 2 x tiles in flight)
-  b += 4 * 24 + 8 * 4;            // frame words
+  b += 4 * 24 + 8 * 6;            // frame words
   return b + 16 * 256;            // alignment slack
 }
 
@@ -108,13 +110,25 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.TY = (H + TS - 1) / TS; d.TX = (W + TS - 1) / TS; d.T = d.TY * d.TX;
   d.nslot = nslot;
   d.hmax = d.T * TPX + 2;
-  d.initg = d.T / 32 < 1 ? 1 : (d.T / 32 > 32 ? 32 : d.T / 32);
+  // Tiles per init task and per seed / closure-seed task: large groups amortise the per-task
+  // cost when many frames are in flight (C4), single tiles spread a latency-bound call's few
+  // frames over the CTAs (C3 sequences: 8 VGA frames in flight)
+  {
+    const long long inflight = (long long)nslot * d.T, ctas = c->grid_max > 0 ? c->grid_max : 592;
+    long long g = d.T / 32;
+    const long long g2 = inflight / (4 * ctas);
+    if (g2 < g) g = g2;
+    d.initg = (int)(g < 1 ? 1 : (g > 32 ? 32 : g));
+    const long long b = inflight / (8 * ctas);
+    d.bulkg = b >= 8 ? 8 : (b >= 4 ? 4 : (b >= 2 ? 2 : 1));
+  }
   if (const char* ev = knob("GC_INITG")) d.initg = atoi(ev) > 0 && atoi(ev) <= INIT_GMAX ? atoi(ev) : d.initg;
+  if (const char* ev = knob("GC_BULKG")) d.bulkg = atoi(ev) == 1 || atoi(ev) == 2 || atoi(ev) == 4 || atoi(ev) == 8 ? atoi(ev) : d.bulkg;
   const size_t T = d.T, ns = (size_t)nslot * T, K = c->K;
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
   // per-frame words and the queue counters first: contiguous, so one memset clears them
-  char* fw = take((size_t)nslot * (4 * 24 + 8 * 4) + 64 * 4);  // <= 24 int + 4 u64 per slot
+  char* fw = take((size_t)nslot * (4 * 24 + 8 * 6) + 64 * 4);  // <= 24 int + 6 u64 per slot
   int32_t* w = (int32_t*)fw;
   d.fmode = w; w += nslot;
   d.sfr = w; w += nslot;
@@ -137,6 +151,8 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.frel = u; u += nslot;
   d.sumct = u; u += nslot;
   d.sumneg = u; u += nslot;
+  d.swf = (const int32_t**)u; u += nslot;  // per-slot flow pointers (k_setup / refills assign)
+  d.sfs = (int32_t**)u; u += nslot;
   u = (unsigned long long*)align_up((size_t)u, 16);
   d.qhead = u; u += 1;
   d.qtail = u; u += 1;
@@ -145,6 +161,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.ntask = u; u += 1;
   c->words_bytes = (char*)u - fw;
   d.treq = (int32_t*)take(ns * 4);
+  d.flag = (int32_t*)take(ns * 4);  // zeroed per call with treq, sent, got (init-seeds set flags)
   d.sent = (uint32_t*)take(ns * K * 64 * 4);
   d.got = (uint32_t*)take(ns * K * 64 * 4);
   *sentgot_bytes = (char*)(d.got + ns * K * 64) - (char*)d.treq;
@@ -165,7 +182,6 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.neg0 = (long long*)take(ns * 8);
   d.mat = (int32_t*)take(ns * 4);
   d.tact = (int32_t*)take(ns * 4);
-  d.flag = (int32_t*)take(ns * 4);
   d.recv1 = (int32_t*)take(ns * 4);
   d.tuni = (int32_t*)take(ns * 4);
   d.tfix = (int32_t*)take(ns * 4);
@@ -266,11 +282,29 @@ double now_s() {
 
 // Solve `nframes` frames of geometry H x W with the slots the pool holds: slots are refilled
 // on the device as frames finish (continuous batching).
+// Sequence mode (seqL > 0, gc_solve_sequences): nframes = seqS x seqL frames, frame t of a
+// sequence solved after frame t-1 in the same slot (warm-started from its flows if seqWarm).
 template <int K>
-gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaStream_t st, Launcher& L) {
-  const int nslot = chunk_frames(c, H, W) < nframes ? chunk_frames(c, H, W) : nframes;
+gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaStream_t st, Launcher& L, int seqS = 0,
+                      int seqL = 0, int seqWarm = 0) {
+  const int units = seqL ? seqS : nframes;  // slots serve frames, or whole sequences
+  const int nslot = chunk_frames(c, H, W) < units ? chunk_frames(c, H, W) : units;
   size_t sg_bytes = 0, q_bytes = 0;
   Dev d = carve(c, nslot, H, W, &sg_bytes, &q_bytes);
+  if (seqL && seqWarm) {  // ping-pong flow buffers, two per slot
+    const size_t need = (size_t)nslot * 2 * (K / 2) * H * W * 4;
+    if (need > c->fbuf_bytes) {
+      if (c->fbuf) cudaFree(c->fbuf);
+      c->fbuf = nullptr;
+      c->fbuf_bytes = 0;
+      if (cudaMalloc(&c->fbuf, need) != cudaSuccess) { cudaGetLastError(); c->err = "flow buffers"; return GC_ERR_OOM; }
+      c->fbuf_bytes = need;
+    }
+    d.fbuf = c->fbuf;
+  }
+  // unfinished frames read F = -1 and status 0 until the kernel writes them (k_abort relies on it)
+  if (!ck(c, cudaMemsetAsync(io.flow, 0xff, (size_t)nframes * 8, st), "memset")) return GC_ERR_CUDA;
+  if (io.stats && !ck(c, cudaMemsetAsync(io.stats, 0, (size_t)nframes * 16, st), "memset")) return GC_ERR_CUDA;
   const size_t smem = solve_smem_bytes<K>();
   const size_t ns = (size_t)nslot * d.T;
   int grid = c->grid_max;  // computed per context (its device) in gc_create
@@ -279,8 +313,6 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   if (!ck(c, cudaMemsetAsync(d.fmode, 0, c->words_bytes, st), "memset")) return GC_ERR_CUDA;
   if (!ck(c, cudaMemsetAsync(d.treq, 0, sg_bytes, st), "memset")) return GC_ERR_CUDA;
   if (!ck(c, cudaMemsetAsync(d.q, 0xff, q_bytes, st), "memset")) return GC_ERR_CUDA;
-  k_setup<<<(unsigned)((ns + NTH - 1) / NTH < 4096 ? (ns + NTH - 1) / NTH : 4096), NTH, 0, st>>>(d, nframes);
-  ++L.n;
   Ctl ctl;
   ctl.relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
   ctl.vis_budget = c->vis_mult * d.T;
@@ -297,6 +329,9 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   ctl.rounds = c->rounds;
   ctl.nframes = nframes;
   ctl.K4 = K == 4;
+  ctl.seqL = seqL;
+  ctl.seqS = seqS;
+  ctl.seqWarm = seqWarm;
   // int4 loads in the init pass when every caller row is 16-byte aligned
   ctl.vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
             ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
@@ -304,6 +339,8 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   const double mt = (double)c->max_launches * (double)ns;
   ctl.max_tasks = mt > 9e18 ? (long long)9e18 : (long long)mt;
   *c->habort = 0;
+  k_setup<<<(unsigned)((ns + NTH - 1) / NTH < 4096 ? (ns + NTH - 1) / NTH : 4096), NTH, 0, st>>>(d, io, ctl);
+  ++L.n;
   // the launch's device time, always measured (gc_get_kernel_ms): two events per launch
   if (c->evnext + 2 > c->evpool.size()) {
     for (int i = 0; i < 16; ++i) {
@@ -349,7 +386,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
             base[d.gctr - d.fmode + 2], base[d.done - d.fmode], base[d.done - d.fmode + 1]);
   }
   if (aborted) {
-    k_abort<<<(nslot + NTH - 1) / NTH, NTH, 0, st>>>(d, io, nframes);
+    k_abort<<<(nframes + NTH - 1) / NTH < 4096 ? (nframes + NTH - 1) / NTH : 4096, NTH, 0, st>>>(d, io, nframes);
     ++L.n;
     if (!ck(c, cudaStreamSynchronize(st), "abort")) return GC_ERR_CUDA;
     if (c->hpin[3]) {
@@ -520,6 +557,7 @@ void gc_destroy(gc_ctx* c) {
   if (c->habort) cudaFreeHost(c->habort);
   if (c->dtiles) cudaFree(c->dtiles);
   if (c->trace) cudaFree(c->trace);
+  if (c->fbuf) cudaFree(c->fbuf);
   delete c;
 }
 
@@ -620,6 +658,39 @@ gc_status gc_solve_batch(gc_ctx* c, const gc_batch* b, void* stream) {
     res = (K == 8) ? solve_chunk<8>(c, io, b->n, H, W, st, L) : solve_chunk<4>(c, io, b->n, H, W, st, L);
   }
   (void)plane;
+  c->last_launches = L.n;
+  resolve_timing(c);
+  if (c->prof) resolve_profile(c);
+  if (res == GC_ERR_RANGE && c->err.empty()) c->err = "capacity out of range [0, GC_CAP_MAX] in some frame";
+  if (res == GC_ERR_NOCONV && c->err.empty()) c->err = "max_launches exceeded before convergence";
+  return res;
+}
+
+gc_status gc_solve_sequences(gc_ctx* c, const gc_seq_batch* b, void* stream) {
+  if (!c) return GC_ERR_ARG;
+  if (!b) { c->err = "sequence batch is NULL"; return GC_ERR_ARG; }
+  const long long nf = (long long)b->S * b->L;
+  if (b->S < 0 || b->L <= 0 || b->H <= 0 || b->W <= 0 || b->H > c->max_h || b->W > c->max_w || nf > (1ll << 30)) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "bad dims S=%d L=%d H=%d W=%d (max %dx%d)", b->S, b->L, b->H, b->W, c->max_h, c->max_w);
+    c->err = buf;
+    return GC_ERR_ARG;
+  }
+  if (nf > 0 && (!b->cap_s || !b->cap_t || !b->cap_nb || !b->flow_out || !b->mask_out)) {
+    c->err = "NULL required pointer";
+    return GC_ERR_ARG;
+  }
+  c->err.clear();
+  cudaSetDevice(c->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  Launcher L{c, st};
+  gc_status res = GC_OK;
+  if (nf > 0) {
+    IO io{b->cap_s, b->cap_t, b->cap_nb, b->warm_flow, b->flow_out, b->mask_out, b->flow_state_out, b->stats_out};
+    const int w = b->warm != 0;
+    res = (c->K == 8) ? solve_chunk<8>(c, io, (int)nf, b->H, b->W, st, L, b->S, b->L, w)
+                      : solve_chunk<4>(c, io, (int)nf, b->H, b->W, st, L, b->S, b->L, w);
+  }
   c->last_launches = L.n;
   resolve_timing(c);
   if (c->prof) resolve_profile(c);

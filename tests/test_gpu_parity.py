@@ -390,3 +390,39 @@ def test_serpentine_lane64_parity(torch, gc):
     g = solver(gc, 4)
     F, mask = g.solve(*to_dev(torch, cs, ct, nb))
     check_against_oracle(cs, ct, nb, F.cpu().numpy(), mask.cpu().numpy(), "bk")
+
+
+# ----------------------------------------------------------------------------- sequences
+@pytest.mark.parametrize("K,S,L,H,W,mb", [(4, 3, 5, 96, 128, 0), (8, 5, 4, 70, 90, 2), (4, 2, 7, 33, 65, 1)])
+def test_sequences_warm_equals_cold_equals_oracle(torch, gc, K, S, L, H, W, mb):
+    """gc_solve_sequences: S sequences of L frames in one device pass; frame t warm-started
+    from frame t-1's flows (warm=1) and the same schedule cold (warm=0) give the oracle's F and
+    mask on every frame -- also with fewer slots than sequences (max_batch < S: a slot takes the
+    next sequence when its sequence ends) and a garbage warm start for frame 0; the last
+    frames' exported flows are certified (flow certificate)."""
+    rng = np.random.default_rng(40 + K)
+    cs, ct, nb = synth.gen_host("blob", 31 + K, 0, S * L, H, W, K, seq_len=L)
+    cs, ct, nb = (a.reshape((S, L) + a.shape[1:]) for a in (cs, ct, nb))
+    g = solver(gc, K, 128, 128, max_batch=mb) if mb else solver(gc, K, 128, 128)
+    dcs, dct, dnb = to_dev(torch, cs, ct, nb)
+    wf0 = rng.integers(-(1 << 31), (1 << 31) - 1, size=(S, K // 2, H, W), dtype=np.int64).astype(np.int32)
+    Fw, mw, fsw, stw = g.solve_sequences(dcs, dct, dnb, warm=True, warm_flow=to_dev(torch, wf0)[0], flow_state=True,
+                                         stats=True)
+    Fc, mc = g.solve_sequences(dcs, dct, dnb, warm=False)
+    assert torch.equal(Fw, Fc) and torch.equal(mw, mc)
+    assert (stw[..., 3] == 0).all()
+    F, m = Fw.cpu().numpy().reshape(-1), mw.cpu().numpy().reshape(S * L, H, W)
+    check_against_oracle(cs.reshape((S * L,) + cs.shape[2:]), ct.reshape((S * L,) + ct.shape[2:]),
+                         nb.reshape((S * L,) + nb.shape[2:]), F, m, "bk")
+    fs = fsw.cpu().numpy()
+    for j in range(S):
+        ok, Ff = cut_cert(cs[j, L - 1], ct[j, L - 1], nb[j, L - 1], fs[j])
+        assert ok and Ff == int(F[j * L + L - 1]), j
+
+
+def test_sequences_arg_errors(torch, gc):
+    g = solver(gc, 4, 64, 64)
+    b = gc.gc_seq_batch(2, 0, 10, 10, None, None, None, None, None, None, None, None, 1)
+    assert gc.gc_solve_sequences(g.ctx, b, 0) == 1
+    b = gc.gc_seq_batch(2, 3, 10, 10, None, None, None, None, None, None, None, None, 1)
+    assert gc.gc_solve_sequences(g.ctx, b, 0) == 1

@@ -107,6 +107,22 @@ def test_c3_warm_sequences_every_frame(torch, gc):
     g.close()
 
 
+def test_c3_sequence_pass_every_frame(torch, gc):
+    """C3 through gc_solve_sequences, the bench's warm schedule: 8 sequences x 120 VGA frames in
+    ONE device pass, frame t of a sequence warm-started from the flows frame t-1 exported.
+    warm == cold (the same pass with warm=0) == oracle on all 960 frames."""
+    S, L, H, W = 8, 120, 480, 640
+    cs, ct, nb = synth.gen_torch("blob", synth.BASE_SEED + 2, 0, S * L, H, W, 4, seq_len=L)
+    g = gc.GridCut(neighborhood=4, max_h=H, max_w=W)
+    sh = lambda a: a.view((S, L) + tuple(a.shape[1:]))  # noqa: E731
+    Fw, mw = g.solve_sequences(sh(cs), sh(ct), sh(nb), warm=True)
+    Fc, mc = g.solve_sequences(sh(cs), sh(ct), sh(nb), warm=False)
+    assert torch.equal(Fw, Fc) and torch.equal(mw, mc)
+    n = oracle_compare(cs, ct, nb, Fw.reshape(-1), mw.reshape(S * L, H, W), label="C3 seq")
+    print(f"C3 sequences: warm == cold == BK on {n} frames")
+    g.close()
+
+
 def test_c5_all_frames_certified(torch, gc):
     """C5 as bench.py --config c5 runs it: 8 frames of 3840x2160 serpentine caps (64-px lanes)
     in one call.  The oracle needs hours per frame, so every frame is certified without it

@@ -1,1 +1,2 @@
-make -s all; python tools/frame0_probe.py > gpurun_out/frame0.txt 2>&1; cat gpurun_out/frame0.txt
+make -s all
+python tools/trace_probe.py c4 1 f0alone > gpurun_out/trace_f0alone.txt 2>&1

@@ -70,23 +70,35 @@ def main():
     import paper_1008_0502_b200 as gc
     import synth
     cfgname = sys.argv[1] if len(sys.argv) > 1 else "c4"
+    seqmode = None
+    if cfgname in ("c3warm", "c3cold"):  # gc_solve_sequences, 8 x 120 VGA frames
+        seqmode = cfgname == "c3warm"
+        cfgname = "c3"
     cfg = dict(bench.CONFIGS[cfgname])
     n = int(sys.argv[2]) if len(sys.argv) > 2 else cfg["frames"]
     tag = sys.argv[3] if len(sys.argv) > 3 else cfgname
     H, W, K = cfg["H"], cfg["W"], cfg["K"]
     if cfg["kind"] == "serpentine":
         synth.set_serpentine_params(lane=64, big=1 << 20)
-    cs, ct, nb = synth.gen_torch(cfg["kind"], synth.BASE_SEED + cfg["seed_off"], 0, n, H, W, K)
+    if seqmode is not None:
+        n = 960
+    cs, ct, nb = synth.gen_torch(cfg["kind"], synth.BASE_SEED + cfg["seed_off"], 0, n, H, W, K,
+                                 seq_len=120 if seqmode is not None else 0)
     g = gc.GridCut(neighborhood=K, max_h=H, max_w=W)
+    if seqmode is not None:
+        cs, ct, nb = (a.view((8, 120) + tuple(a.shape[1:])) for a in (cs, ct, nb))
+        run = lambda: g.solve_sequences(cs, ct, nb, warm=seqmode)  # noqa: E731
+    else:
+        run = lambda: g.solve(cs, ct, nb)  # noqa: E731
     for _ in range(2):
-        g.solve(cs, ct, nb)
+        run()
     torch.cuda.synchronize()
     g.kernel_ms(reset=True)
-    g.solve(cs, ct, nb)
+    run()
     plain = g.kernel_ms(reset=True)
     g.set_profiling(2)
     gc.debug_trace(g.ctx, 1, reset=True)
-    g.solve(cs, ct, nb)
+    run()
     torch.cuda.synchronize()
     prof_ms = g.kernel_ms(reset=True)
     tr = gc.debug_trace(g.ctx)
@@ -94,7 +106,7 @@ def main():
     np.save(os.path.join(ROOT, "gpurun_out", f"trace_{tag}.npy"), tr)
     nctas = int(((tr[:, 2] >> np.uint64(32)) & np.uint64(0xffff)).max()) + 1
     s = summarize(tr, nctas)
-    s.update({"config": cfgname, "frames": n, "plain_kernel_ms": round(plain, 3), "traced_kernel_ms": round(prof_ms, 3),
+    s.update({"config": cfgname + ("" if seqmode is None else (" seq warm" if seqmode else " seq cold")), "frames": n, "plain_kernel_ms": round(plain, 3), "traced_kernel_ms": round(prof_ms, 3),
               "ctas": nctas})
     tl = s.pop("timeline")
     print(json.dumps(s))
