@@ -6,6 +6,10 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude
 ifeq ($(DEV),1)
 NVFLAGS += -DGC_DEV_KNOBS
 endif
+# make CHECKS=1: device invariant checks (GC_CHECK) compiled in
+ifeq ($(CHECKS),1)
+NVFLAGS += -DGC_CHECKS
+endif
 PKG := paper_1008_0502_b200
 
 all: $(PKG)/libgc.so synth/libsynth.so oracle/liboracle.so

@@ -25,6 +25,7 @@
 // read through L2 (the library is compiled with -dlcm=cg), the caps through the read-only
 // path.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the TMA descriptors of the init stream)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -102,6 +103,9 @@ struct Dev {
   int32_t* fbe;     // [nslot] global relabels started (BFS epoch)
   int32_t* fcap;    // [nslot] height cap of the running push phase (higher pixels are frozen)
   int32_t* fbnd;    // [nslot] distance bound of the running global relabel (HINF: exact)
+  int32_t* sep;     // [nslot] closure attempts of the slot in this call (all its frames): the
+                    //         reach-mark epoch is sep % 255 + 1; the slot's marks are cleared
+                    //         when it wraps, so a mark never aliases an earlier attempt's
   int32_t* fstat;   // [nslot][4] push tasks, global relabels, BFS relax tasks, -
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]
@@ -144,6 +148,24 @@ struct IO {
 };
 
 __device__ __forceinline__ size_t NS(const Dev& d) { return (size_t)d.nslot * d.T; }
+
+// Checked builds (make CHECKS=1; compute-sanitizer is not available on the GPU pool): device
+// invariants that guard every index the scheduler derives from shared state.  A failed check
+// records its source line in gctr[3] (>= 2) and stops the kernel through the abort flag; the
+// host returns GC_ERR_CUDA "device check failed at line N".  Compiled out otherwise.
+#ifdef GC_CHECKS
+#define GC_CHECK(d, cond)                                              \
+  do {                                                                 \
+    if (!(cond)) {                                                     \
+      atomicCAS(&(d).gctr[3], 0, 2 + __LINE__);                        \
+      *(volatile int*)&(d).done[1] = 1;                                \
+    }                                                                  \
+  } while (0)
+#else
+#define GC_CHECK(d, cond) \
+  do {                    \
+  } while (0)
+#endif
 __device__ __forceinline__ int32_t* Rp(const Dev& d, int K, size_t gt, int k) {
   const size_t s = (unsigned)gt / (unsigned)d.T, tile = gt - s * d.T;
   return d.r + ((s * K + k) * d.T + tile) * TPX;
@@ -788,7 +810,6 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
         if (x0 + i < W) mk[i] = (uint8_t)((mw >> (8 * i)) & 1u);
     }
   }
-  if (t < K * 16) reinterpret_cast<uint32_t*>(d.reach + gt * K * 64)[t] = 0u;
   // warp partials (no barrier: warps run ahead to the next tile's loads); sums with REDUX on
   // 32-bit halves (per-thread sums are < 2^31, warp sums may not be)
   const unsigned long long us = (unsigned long long)sct, un = (unsigned long long)neg;
@@ -877,18 +898,114 @@ __device__ __forceinline__ void init_prefetch(const Dev& d, const FramePtrs& P, 
 
 template <int K>
 constexpr size_t init_smem_bytes() {
-  return INIT_GMAX * sizeof(InitPart) + INIT_GMAX * sizeof(int) + (2 + K) * NTH * 16;
+  return INIT_GMAX * sizeof(InitPart) + INIT_GMAX * sizeof(int) + 128 + (2 + K) * NTH * 16;
+}
+
+// ---- TMA (cp.async.bulk.tensor) staging of the init stream.  Tensor maps over the caller's
+// cap arrays (host-built per call, gc_solver.cu): cs, ct as [n][H][W] (rank 3), nb as
+// [n][K][H][W] (rank 4), boxes of 32 x 4 pixels (x 1 frame, x K planes): one box set per WARP,
+// i.e. the 4 tile rows the warp owns (thread t owns row t/8, columns 4(t%8)..+3).  Each warp
+// has its own mbarrier and a 512 x (2+K)-byte stage; lane 0 arms the barrier with the stage's
+// byte count and issues the next tile's three loads as soon as the warp has moved the current
+// one into registers, so no CTA barrier is needed (the warps stream independently) and no
+// thread spends issue slots or registers on addresses.  Boxes reaching past the frame edge
+// are zero-filled by the TMA unit.
+struct Tmaps {
+  CUtensorMap cs, ct, nb;
+  int on;  // maps valid (cold frames, 16-byte aligned rows)
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+// Lane 0 of warp w: arm the warp's barrier and load rows 4w..4w+3 of tile (ty, tx) of frame fr.
+template <int K>
+__device__ __forceinline__ void tma_issue_rows(const Tmaps& tm, char* stage, uint64_t* bar, int fr, int ty, int tx,
+                                               int w) {
+  mbar_expect_tx(bar, (2 + K) * 512);
+  const int x = tx * TS, y = ty * TS + 4 * w;
+  tma_load_3d(stage, &tm.cs, x, y, fr, bar);
+  tma_load_3d(stage + 512, &tm.ct, x, y, fr, bar);
+  tma_load_4d(stage + 1024, &tm.nb, x, y, 0, fr, bar);
 }
 
 template <int K>
-__device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, int* smem) {
+__device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, int* smem,
+                                          const Tmaps& tm, uint64_t* mbar, unsigned& tpar) {
   const int s = (int)((unsigned)gt0 / (unsigned)d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
   const int n = min(d.initg, d.T - tile0);
   const FramePtrs P = frame_ptrs(d, io, s, K);
   InitPart* part = reinterpret_cast<InitPart*>(smem);        // [n]
   int* uni_s = reinterpret_cast<int*>(part + INIT_GMAX);     // [n]
   int a[4], b[4], c[K][4];
-  if (vec && !P.wf) {
+  if (tm.on && !P.wf) {
+    // cold frames, aligned rows: TMA row boxes per warp, tile i + 1's arriving while tile i is
+    // computed from registers
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    char* stage = reinterpret_cast<char*>(((uintptr_t)(uni_s + INIT_GMAX) + 127) & ~(uintptr_t)127) + w * (2 + K) * 512;
+    uint64_t* bar = mbar + w;
+    const int fr = (int)P.fr;
+    if (lane == 0) tma_issue_rows<K>(tm, stage, bar, fr, tile0 / d.TX, tile0 % d.TX, w);
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) {
+      mbar_wait(bar, tpar);
+      tpar ^= 1u;
+      {
+        const int4* sv = reinterpret_cast<const int4*>(stage) + lane;
+        int4 v = sv[0];
+        a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+        v = sv[32];
+        b[0] = v.x; b[1] = v.y; b[2] = v.z; b[3] = v.w;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          v = sv[(2 + k) * 32];
+          c[k][0] = v.x; c[k][1] = v.y; c[k][2] = v.z; c[k][3] = v.w;
+        }
+      }
+      __syncwarp();  // the warp's stage is free for the next tile
+      if (i + 1 < n && lane == 0) {
+        const int tile = tile0 + i + 1;
+        tma_issue_rows<K>(tm, stage, bar, fr, tile / d.TX, tile % d.TX, w);
+      }
+      if (P.fs) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
+      else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i);
+    }
+  } else if (vec && !P.wf) {
     // cold frames, aligned rows: tile i + 1's caps stream into shared memory (cp.async,
     // each thread its own slots, so no barrier) while tile i is computed from registers
     int4* pf = reinterpret_cast<int4*>(uni_s + INIT_GMAX);  // [(2 + K) * NTH]

@@ -78,6 +78,7 @@ __device__ __forceinline__ int relabel_bound(const Dev& d, const Ctl& c, int ce)
 }
 
 __device__ __forceinline__ void slot_assign(const Dev& d, const IO& io, const Ctl& c, int s, int f) {
+  GC_CHECK(d, s >= 0 && s < d.nslot && f >= 0 && f < c.nframes);
   const size_t pl = (size_t)d.H * d.W * (c.K4 ? 2 : 4);
   d.sfr[s] = f;
   d.fbe[s] = 1;  // the frame's first global relabel is seeded by its init tasks
@@ -388,7 +389,7 @@ __device__ __forceinline__ void task_relax(const Dev& d, size_t gt, int* hs, int
 // pass writes it; they are in every closure): a tile a push touched (mat) rewrites all its
 // bytes in its closure seed, an untouched tile only writes the closure pixels beyond its
 // excess pixels ("extras", flagged in tmk so that the next attempt rewrites the tile).
-__device__ __forceinline__ int closure_epoch(const Dev& d, int s) { return __ldcg(d.cep + s) % 255 + 1; }
+__device__ __forceinline__ int closure_epoch(const Dev& d, int s) { return __ldcg(d.sep + s) % 255 + 1; }
 
 template <int K>
 __device__ __forceinline__ void closure_fixpoint(volatile uint8_t* ms, const uint8_t* os, int (&mm)[4]) {
@@ -499,7 +500,7 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
     const int r1 = __ldcg(d.recv1 + gt), fe = __ldcg(d.ferr + s), cf = __ldcg(d.cfail + s);
     const int tu = __ldcg(d.tuni + gt), mt = __ldcg(d.mat + gt), tm = __ldcg(d.tmk + gt);
     const int tsr = __ldcg(d.tsrc + gt);
-    const int cp = __ldcg(d.cep + s);
+    const int cp = __ldcg(d.sep + s);
     bc[0] = r1;
     // 2: range error (mask all 0, F = -1); 1: skip -- the attempt already failed, or (a tile of
     // the group outside the task set) an untouched uniform sink tile without extra mask bytes;
@@ -1018,6 +1019,7 @@ enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_
 
 __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
   const int f = d.sfr[s];
+  GC_CHECK(d, f >= 0 && f < c.nframes && d.fout[s] >= 1);
   int st = 0;
   long long F = (long long)d.sumct[s] - (long long)d.sumneg[s];
   if (d.ferr[s]) { st = 2; F = -1; atomicAdd(&d.gctr[2], 1); }
@@ -1165,6 +1167,12 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         d.fbe[s] += 1;
         d.fbnd[s] = relabel_bound(d, c, d.cep[s]);
       }
+      bc[1] = 0;
+      if (nm == M_CSEED) {  // a new closure attempt: the next reach-mark epoch of the slot
+        const int se = d.sep[s] + 1;
+        d.sep[s] = se;
+        bc[1] = (se % 255) == 0;  // wrapped: clear the slot's marks first
+      }
       bc[3] = d.fbe[s];
       d.fmode[s] = nm;
       bc[4] = kind;
@@ -1173,6 +1181,13 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     __syncthreads();
     const int kind = bc[4];
     if (kind == SET_NONE) break;
+    if (bc[1]) {  // reach-mark epoch wrapped (every 255 attempts of a slot): clear its marks
+      uint32_t* rm = reinterpret_cast<uint32_t*>(d.reach + (size_t)s * d.T * (c.K4 ? 4 : 8) * 64);
+      const size_t words = (size_t)d.T * (c.K4 ? 4 : 8) * 16;
+      for (size_t i = t; i < words; i += NTH) rm[i] = 0u;
+      fence_gpu();
+      __syncthreads();
+    }
     // enqueue the phase's first task set, NTH tiles at a time
     const size_t base_gt = (size_t)s * d.T;
     // closure seeds: an untouched uniform source tile whose neighbours are all uniform source
@@ -1282,6 +1297,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     }
     if (t == 0) {
       const int left = atomicSub(&d.fout[s], 1) - 1;
+      GC_CHECK(d, left >= 0);
       if (left == 0) atomicAdd(&d.fout[s], 1);  // every task already done (or none): go on
       bc[4] = left;
     }
@@ -1293,8 +1309,14 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
 
 // ---------------------------------------------------------------- the persistent kernel
 template <int K>
-__global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ Dev d, const __grid_constant__ IO io, const __grid_constant__ Ctl c) {
-  extern __shared__ __align__(16) int smem[];
+__global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ Dev d, const __grid_constant__ IO io,
+                                                         const __grid_constant__ Ctl c, const __grid_constant__ Tmaps tm) {
+  extern __shared__ __align__(128) int smem[];
+  __shared__ uint64_t mbar[NTH / 32];  // one TMA barrier per warp (init stream)
+  unsigned tpar = 0;                   // the warp's barrier phase
+  if ((threadIdx.x & 31) == 0) mbar_init(&mbar[threadIdx.x >> 5], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
   __shared__ int bc[8];
   __shared__ long long red[NTH / 32];
   __shared__ uint32_t task_s;
@@ -1359,6 +1381,8 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     }
     const size_t gt = v & 0x00ffffffu;
     const int s = (int)((unsigned)gt / (unsigned)d.T);
+    GC_CHECK(d, gt < NS(d) && (v >> 28) <= M_CLOS && s < d.nslot);
+    GC_CHECK(d, gt + ((v >> 24) & 15) < NS(d) && (unsigned)d.sfr[s] < (unsigned)c.nframes);
     const int md = (int)(v >> 28);
     const int gcnt = (int)((v >> 24) & 15) + 1;
     const bool reqd = md == M_BFS || md == M_PUSH || md == M_CLOS;  // request-driven phase
@@ -1377,7 +1401,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     int cls = 0;
     switch (md) {
       case M_INIT:
-        task_init<K>(d, io, gt, c.vec != 0, smem);
+        task_init<K>(d, io, gt, c.vec != 0, smem, tm, mbar, tpar);
         init_seed_group<K>(d, gt, smem);
         cls = 0;
         break;
@@ -1433,6 +1457,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
         const int b = t - 1;
         if (((bc[1] >> b) & 1) && !(b >= 4 && K == 4)) {
           const long long n = side_tile(d, gt, b);
+          GC_CHECK(d, n < (long long)NS(d) && (n < 0 || (size_t)n / d.T == (size_t)s));
           if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) {
             if (atomicAdd(&d.treq[n], 1) == 0) {
               atomicAdd(&d.fout[s], 1);
@@ -1445,7 +1470,11 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     }
     if (t == 0) {
       int last = 0;
-      if (!reqd || rem <= 0) last = atomicSub(&d.fout[s], 1) == 1;
+      if (!reqd || rem <= 0) {
+        const int before = atomicSub(&d.fout[s], 1);
+        GC_CHECK(d, before >= 1);
+        last = before == 1;
+      }
       bc[3] = last;
       if (prof) {
         uint64_t w1;

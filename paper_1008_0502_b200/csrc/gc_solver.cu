@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "gc.h"
 #include "gc_phases.cuh"
 
@@ -36,6 +38,7 @@ struct gc_ctx {
   int wave = 0;                   // push cap: heights above the lowest active one + wave freeze
                                   // (doubled from 1 per failed certificate attempt)
   int selfrun = 0;                // 1: a push tile re-runs itself only after progress
+  int tma = 1;                    // TMA staging of the init stream when the layout allows
   int grid = 0;                   // k_solve CTAs of the last launch
   int grid_max = 0;               // persistent grid of k_solve<K> on this context's device
   std::string err;
@@ -90,7 +93,7 @@ size_t frame_bytes(int K, size_t T) {
   b += T * K * 64;                // reach
   b += T * 8 + 13 * T * 4;        // neg0 + tile flags
   b += 2 * T * 4 * 2;             // queues (capacity >= 2 x tiles in flight)
-  b += 4 * 24 + 8 * 6;            // frame words
+  b += 4 * 25 + 8 * 6;            // frame words
   return b + 16 * 256;            // alignment slack
 }
 
@@ -128,7 +131,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
   // per-frame words and the queue counters first: contiguous, so one memset clears them
-  char* fw = take((size_t)nslot * (4 * 24 + 8 * 6) + 64 * 4);  // <= 24 int + 6 u64 per slot
+  char* fw = take((size_t)nslot * (4 * 25 + 8 * 6) + 64 * 4);  // <= 25 int + 6 u64 per slot
   int32_t* w = (int32_t*)fw;
   d.fmode = w; w += nslot;
   d.sfr = w; w += nslot;
@@ -144,6 +147,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.fbe = w; w += nslot;
   d.fcap = w; w += nslot;
   d.fbnd = w; w += nslot;
+  d.sep = w; w += nslot;
   d.fstat = w; w += 4 * nslot;
   d.gctr = w; w += 4;
   d.done = w; w += 4;
@@ -164,7 +168,9 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.flag = (int32_t*)take(ns * 4);  // zeroed per call with treq, sent, got (init-seeds set flags)
   d.sent = (uint32_t*)take(ns * K * 64 * 4);
   d.got = (uint32_t*)take(ns * K * 64 * 4);
-  *sentgot_bytes = (char*)(d.got + ns * K * 64) - (char*)d.treq;
+  d.reach = (uint8_t*)(d.got + ns * K * 64);  // zeroed per call with treq .. got (epochs: Dev::sep)
+  *sentgot_bytes = (char*)(d.reach + ns * K * 64) - (char*)d.treq;
+  take(ns * K * 64);
   const size_t qcap = pow2_at_least(2 * ns + 1024);
   d.q = (uint32_t*)take(qcap * 4);
   d.qmask = (uint32_t)(qcap - 1);
@@ -178,7 +184,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.r = (int32_t*)take(ns * K * TPX * 4);
   d.fl = (uint16_t*)take(ns * TPX * 2);
   d.hedge = (int32_t*)take(ns * 128 * 4);
-  d.reach = (uint8_t*)take(ns * K * 64);
+
   d.neg0 = (long long*)take(ns * 8);
   d.mat = (int32_t*)take(ns * 4);
   d.tact = (int32_t*)take(ns * 4);
@@ -274,6 +280,41 @@ int chunk_frames(gc_ctx* c, int H, int W) {
   return (int)n;
 }
 
+// TMA descriptors of the init stream (gc_kernels.cuh Tmaps): cs / ct as rank-3 [n][H][W],
+// nb as rank-4 [n][K][H][W] int32 tensors, 32 x 4-pixel boxes (one warp's rows of a tile).
+// Needs 16-byte aligned bases and W % 4 == 0 (strides multiple of 16 bytes): ctl.vec.
+bool make_tmaps(gc_ctx* c, const IO& io, int nframes, int H, int W, int K, Tmaps* tm) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+      cudaGetLastError();
+  }
+  if (!enc) return false;
+  (void)c;
+  const cuuint64_t plane = (cuuint64_t)H * W * 4;
+  const cuuint64_t d3[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)nframes};
+  const cuuint64_t s3[2] = {(cuuint64_t)W * 4, plane};
+  const cuuint32_t b3[3] = {32, 4, 1};
+  const cuuint64_t d4[4] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)K, (cuuint64_t)nframes};
+  const cuuint64_t s4[3] = {(cuuint64_t)W * 4, plane, plane * K};
+  const cuuint32_t b4[4] = {32, 4, (cuuint32_t)K, 1};
+  const cuuint32_t e[4] = {1, 1, 1, 1};
+  auto one = [&](CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* str,
+                 const cuuint32_t* box) {
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_INT32, rank, const_cast<void*>(base), dims, str, box, e,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  return one(&tm->cs, io.cs, 3, d3, s3, b3) && one(&tm->ct, io.ct, 3, d3, s3, b3) && one(&tm->nb, io.nb, 4, d4, s4, b4);
+}
+
 double now_s() {
   timespec ts;
   clock_gettime(CLOCK_MONOTONIC, &ts);
@@ -339,6 +380,9 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   const double mt = (double)c->max_launches * (double)ns;
   ctl.max_tasks = mt > 9e18 ? (long long)9e18 : (long long)mt;
   *c->habort = 0;
+  Tmaps tm;
+  memset(&tm, 0, sizeof(tm));
+  tm.on = ctl.vec && c->tma && make_tmaps(c, io, nframes, H, W, K, &tm);
   k_setup<<<(unsigned)((ns + NTH - 1) / NTH < 4096 ? (ns + NTH - 1) / NTH : 4096), NTH, 0, st>>>(d, io, ctl);
   ++L.n;
   // the launch's device time, always measured (gc_get_kernel_ms): two events per launch
@@ -352,7 +396,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   cudaEvent_t e0 = c->evpool[c->evnext++];
   cudaEvent_t e1 = c->evpool[c->evnext++];
   cudaEventRecord(e0, st);
-  k_solve<K><<<grid, NTH, smem, st>>>(d, io, ctl);
+  k_solve<K><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
   ++L.n;
   cudaEventRecord(e1, st);
   c->pending.push_back({0, {e0, e1}});
@@ -389,6 +433,12 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
     k_abort<<<(nframes + NTH - 1) / NTH < 4096 ? (nframes + NTH - 1) / NTH : 4096, NTH, 0, st>>>(d, io, nframes);
     ++L.n;
     if (!ck(c, cudaStreamSynchronize(st), "abort")) return GC_ERR_CUDA;
+    if (c->hpin[3] >= 2) {
+      char buf[96];
+      snprintf(buf, sizeof(buf), "device check failed at gc_*.cuh line %d", c->hpin[3] - 2);
+      c->err = buf;
+      return GC_ERR_CUDA;
+    }
     if (c->hpin[3]) {
       c->err = "internal inconsistency: a closure after the BFS certificate reached a node with e < 0";
       return GC_ERR_CUDA;
@@ -494,6 +544,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (const char* ev = knob("GC_STALLX")) c->stallx = atoi(ev);
   if (const char* ev = knob("GC_WAVE")) c->wave = atoi(ev);
   if (const char* ev = knob("GC_SELFRUN")) c->selfrun = atoi(ev);
+  if (const char* ev = knob("GC_TMA")) c->tma = atoi(ev);
   if (const char* ev = getenv("GC_TIMEOUT_S")) c->timeout_s = atof(ev);
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
   if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
