@@ -292,6 +292,135 @@ def run_warm(args, cfg):
         dist.destroy_process_group()
 
 
+def run_energy(args, cfg):
+    """NEXT-1: the same frames given as the energy of PAPER.md §4 -- RGB image,
+    prior and colour GMMs -- instead of capacities; gc_solve_energy builds the caps inside the
+    solve's init pass.  One step = one gc_solve_energy call over this rank's frames.  The e2e leg
+    uploads 5 B/px (image + prior) instead of the 4(2+K) B/px of caps."""
+    import numpy as np
+    import torch
+
+    import paper_1008_0502_b200 as gc
+    import synth
+    from paper_1008_0502_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    H, W, K, n = cfg["H"], cfg["W"], cfg["K"], cfg["frames"]
+    seed = synth.BASE_SEED + cfg["seed_off"]
+    t_first, n = shard.frame_range(rank, world, n)
+    img, pri = synth.gen_energy_torch(seed, t_first, n, H, W, device=dev)
+    bg, ob = synth.energy_gmms()
+    gm = torch.from_numpy(gc.gmm_table([(bg, ob)] * n)).to(dev)
+    P = synth.ENERGY_PARAMS
+    kw = dict(lam=P["lam"], sigma=P["sigma"], kappa=P["kappa"], eps=P["eps"], scale=P["scale"])
+    flow = torch.empty(n, dtype=torch.int64, device=dev)
+    mask = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
+    g = gc.GridCut(neighborhood=K, max_h=H, max_w=W)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        g.solve_energy(img, pri, gm, out=(flow, mask), **kw)
+    torch.cuda.synchronize()
+    clk = ClockSampler(None)
+    clk.start()
+    time.sleep(0.3)
+    g.kernel_ms(reset=True)
+    g.profile(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        g.solve_energy(img, pri, gm, out=(flow, mask), **kw)
+        launches += g.launches()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    kms = g.kernel_ms(reset=True)
+    nl = max(g.profile(reset=True)["init"][0], 1)
+    clocks = clk.stop()
+    ms = shard.max_over_ranks(e0.elapsed_time(e1), dev, world)
+    px = world * n * H * W * args.steps
+    peak, peak_src = load_peak()
+    bpx = 3 + 2 + 1  # read RGB + prior code, write the mask
+    avg = kms / nl
+    achieved = bpx * n * H * W * args.steps / nl / (avg * 1e-3) / 1e9
+    # e2e: pinned host image + prior in, mask + flow out, through GridCut.solve_energy
+    ne = min(args.e2e_frames, n)
+    himg = torch.empty((ne, H, W, 3), dtype=torch.uint8, pin_memory=True)
+    hpri = torch.empty((ne, H, W), dtype=torch.uint16, pin_memory=True)
+    himg.copy_(img[:ne]); hpri.copy_(pri[:ne])
+    hmask = torch.empty((ne, H, W), dtype=torch.uint8, pin_memory=True)
+    hflow = torch.empty(ne, dtype=torch.int64, pin_memory=True)
+    dimg = torch.empty_like(img[:ne]); dpri = torch.empty_like(pri[:ne])
+    dflow = torch.empty(ne, dtype=torch.int64, device=dev)
+    dmask = torch.empty((ne, H, W), dtype=torch.uint8, device=dev)
+    gme = gm[: ne * 2 * ctypes_sizeof_gmm(gc)]
+
+    def e2e_step():
+        dimg.copy_(himg, non_blocking=True)
+        dpri.copy_(hpri, non_blocking=True)
+        g.solve_energy(dimg, dpri, gme, out=(dflow, dmask), **kw)
+        hmask.copy_(dmask, non_blocking=True)
+        hflow.copy_(dflow, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ems = shard.max_over_ranks(e2.elapsed_time(e3), dev, world)
+    assert np.array_equal(hflow.numpy(), flow[:ne].cpu().numpy())
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        from oracle import energy as oen
+        m = 4
+        rgb, pr = synth.gen_energy_host(seed, 0, m, H, W)
+        t0 = time.perf_counter()
+        capsl = [oen.caps(rgb[i], pr[i], bg, ob, K) for i in range(m)]
+        cs = np.stack([c[0] for c in capsl]); ct = np.stack([c[1] for c in capsl]); nb = np.stack([c[2] for c in capsl])
+        oracle.solve_batch(cs, ct, nb, "bk", threads=min(host_cores(), m))
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(m * H * W / dt / 1e6, 3), "unit": "Mpixel/s", "cores": min(host_cores(), m),
+               "kind": "oracle", "sample": f"{m} frames: oracle/energy.py caps (numpy float64, one core) + BK "
+                                            f"on {min(host_cores(), m)} threads, {cpu_model()}", "seconds": round(dt, 2)}
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(px / (ms * 1e-3) / 1e6, 1), "unit": "Mpixel/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+int32",
+               "data": "synthetic (seeded saliency-blob frames as RGB + prior, synth/; generated on device)",
+               "config": {"workload": f"{cfg['workload']} from the energy (NEXT-1: RGB image, prior, colour GMMs -> "
+                                      f"caps in the init pass)", "H": H, "W": W, "K": K, "frames_per_rank": n,
+                          "parallelism": f"frame-sharded dp{world}", "l2": "inputs >> 126 MB L2"},
+               "fps": round(world * n * args.steps / (ms * 1e-3), 1),
+               "roofline": {"bound": "hbm", "kernel": f"k_solve<{K},energy>", "unit": "GB/s", "peak": peak,
+                            "achieved": round(achieved, 1), "frac": round(achieved / peak, 4),
+                            "bytes_rule": f"{bpx} B/px compulsory (read RGB + prior code, write the mask)",
+                            "avg_launch_ms": round(avg, 4), "traffic": None, "peak_source": peak_src},
+               "e2e": {"value": round(world * ne * H * W * args.steps / (ems * 1e-3) / 1e6, 1), "unit": "Mpixel/s",
+                       "h2d_bytes_per_step": int(ne * H * W * 5), "d2h_bytes_per_step": int(ne * H * W + ne * 8),
+                       "frames_per_step": ne,
+                       "note": "GridCut.solve_energy: pinned host image + prior H2D, mask + flow D2H in the timed region"},
+               "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def ctypes_sizeof_gmm(gc):
+    import ctypes
+    return ctypes.sizeof(gc.gc_gmm)
+
+
 def verify_shard(cfg, seed, t_first, cs, ct, nb, flow, mask, nverify, world):
     """--verify: every frame of this rank's shard (or the first `nverify`) against the CPU oracle
     (Boykov-Kolmogorov), bit-exact in F and mask, outside the timed region.  The caps are the
@@ -334,6 +463,8 @@ def main():
                          "(0: all frames; default: off)")
     ap.add_argument("--cross-check", type=int, default=8, metavar="M",
                     help="N > 1: each rank re-solves the first M frames of the next rank's shard")
+    ap.add_argument("--energy", action="store_true",
+                    help="NEXT-1: frames given as RGB image + prior + colour GMMs; caps built in the solve's init pass")
     ap.add_argument("--warm", action="store_true",
                     help="sequence mode (C3): S sequences x L frames, frame t warm-started from t-1")
     ap.add_argument("--seqs", type=int, default=8)
@@ -350,6 +481,8 @@ def main():
         return run_reference(args, cfg)
     if args.warm:
         return run_warm(args, cfg)
+    if args.energy:
+        return run_energy(args, cfg)
 
     import numpy as np
     import torch

@@ -143,6 +143,59 @@ gc_status gc_solve_batch_host(gc_ctx* ctx, const gc_batch* batch, void* stream);
 gc_status gc_frame_digest(gc_ctx* ctx, int n, int H, int W, const int64_t* flow, const uint8_t* mask,
                           int64_t* out, void* stream);
 
+/* ---- NEXT-1: the energy of PAPER.md §4 -> capacities, built inside the
+ * solve's init pass (no cap arrays in HBM or over PCIe: 5 B/px of input instead of 4(2+K)).
+ *
+ * Colour likelihood p(C|A) of one label: a Gaussian mixture over RGB with
+ * M <= GC_GMM_MAX components; lognorm[m] = log w_m - 1/2 log((2 pi)^3 det S_m) is computed on
+ * the host ("only the normalization term of each Gaussian density is calculated on CPU",
+ * P:584-585) by gc_gmm_prepare, prec[m] = S_m^-1 as (xx, xy, xz, yy, yz, zz). */
+#define GC_GMM_MAX 4
+typedef struct {
+  int M, pad;
+  double lognorm[GC_GMM_MAX];
+  double mean[GC_GMM_MAX][3];
+  double prec[GC_GMM_MAX][6];
+} gc_gmm;
+
+/* Host helper: fills *out from M weights (> 0), means [M][3] and full covariances [M][3][3]
+ * (symmetric positive definite) in double precision.  GC_ERR_ARG on M outside 1..GC_GMM_MAX,
+ * a non-positive weight or a covariance that is not positive definite.  No device work. */
+gc_status gc_gmm_prepare(int M, const double* weights, const double* means, const double* covs, gc_gmm* out);
+
+/* Energy parameters (per call).  For frame f, pixel v with colour C = (R,G,B) and prior code
+ * u = prior[f][v]: p = clamp(u / 65535, eps, 1 - eps) (p(A=1) from the prior),
+ *   c(s,v) = q(-log p(C|A=0) - log(1 - p))     (psi1 + xi1 of label 0)
+ *   c(v,t) = q(-log p(C|A=1) - log p)           (psi1 + xi1 of label 1)
+ * and for the n-link of direction k (distance 1, or sqrt 2 for diagonals), with the integer
+ * luma I = (77 R + 150 G + 29 B + 128) >> 8 ("I_x denotes the intensity"):
+ *   c_k(v) = q(lambda exp(-((I_v - I_{v+d_k}) / 255)^2 / (2 sigma^2)) / dist + kappa)
+ * (psi2 + xi2; reading c5), q(x) = floor(scale x + 0.5)
+ * clamped to [0, GC_CAP_MAX].  Evaluated in double precision.  n-links are symmetric. */
+typedef struct {
+  double lambda, sigma, kappa, eps, scale;
+} gc_energy_params;
+
+typedef struct {
+  int n, H, W;
+  const uint8_t* image;      /* [n][H][W][3] RGB (device)                                    */
+  const uint16_t* prior;     /* [n][H][W] prior code u: p(A=1) = u / 65535 (device)          */
+  const gc_gmm* gmm;         /* [n][2] colour GMMs of label 0 and label 1 (device)           */
+  gc_energy_params params;
+  const int32_t* warm_flow;  /* as gc_batch                                                   */
+  int64_t* flow_out;         /* [n]                                                           */
+  uint8_t* mask_out;         /* [n][H][W]                                                     */
+  int32_t* flow_state_out;   /* NULL or [n][K/2][H][W]                                        */
+  int32_t* stats_out;        /* NULL or [n][4]                                                */
+  int32_t* caps_out;         /* NULL, or [n][2+K][H][W]: the capacities the solve used (cs, ct,
+                                n-link planes; off-grid entries 0), for inspection / parity   */
+} gc_energy_batch;
+
+/* Solves every frame of the energy batch exactly as gc_solve_batch solves the capacities
+ * defined above (same outputs, errors and semantics; GC_ERR_ARG also for NULL image / prior /
+ * gmm, sigma <= 0, eps outside (0, 0.5) or scale <= 0).  Device pointers. */
+gc_status gc_solve_energy(gc_ctx* ctx, const gc_energy_batch* batch, void* stream);
+
 /* Message for the last failing call on this context ("" if none).  Never NULL. */
 const char* gc_last_error(const gc_ctx* ctx);
 

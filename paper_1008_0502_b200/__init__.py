@@ -16,6 +16,7 @@ import os
 import numpy as np
 
 __all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_solve_sequences",
+           "gc_solve_energy", "gc_gmm_prepare",
            "gc_frame_digest", "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "CAP_MAX",
            "STATUS", "lib_path"]
 
@@ -51,6 +52,27 @@ class gc_seq_batch(ctypes.Structure):
                 ("flow_state_out", ctypes.c_void_p), ("stats_out", ctypes.c_void_p), ("warm", ctypes.c_int)]
 
 
+GMM_MAX = 4
+
+
+class gc_gmm(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int), ("pad", ctypes.c_int), ("lognorm", ctypes.c_double * GMM_MAX),
+                ("mean", (ctypes.c_double * 3) * GMM_MAX), ("prec", (ctypes.c_double * 6) * GMM_MAX)]
+
+
+class gc_energy_params(ctypes.Structure):
+    _fields_ = [("lambda_", ctypes.c_double), ("sigma", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("eps", ctypes.c_double), ("scale", ctypes.c_double)]
+
+
+class gc_energy_batch(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int),
+                ("image", ctypes.c_void_p), ("prior", ctypes.c_void_p), ("gmm", ctypes.c_void_p),
+                ("params", gc_energy_params),
+                ("warm_flow", ctypes.c_void_p), ("flow_out", ctypes.c_void_p), ("mask_out", ctypes.c_void_p),
+                ("flow_state_out", ctypes.c_void_p), ("stats_out", ctypes.c_void_p), ("caps_out", ctypes.c_void_p)]
+
+
 _lib.gc_create.argtypes = [ctypes.POINTER(gc_config), ctypes.POINTER(ctypes.c_void_p)]
 _lib.gc_create.restype = ctypes.c_int
 _lib.gc_destroy.argtypes = [ctypes.c_void_p]
@@ -59,6 +81,10 @@ _lib.gc_solve_batch.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_batch), ctype
 _lib.gc_solve_batch.restype = ctypes.c_int
 _lib.gc_solve_sequences.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_seq_batch), ctypes.c_void_p]
 _lib.gc_solve_sequences.restype = ctypes.c_int
+_lib.gc_solve_energy.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_energy_batch), ctypes.c_void_p]
+_lib.gc_solve_energy.restype = ctypes.c_int
+_lib.gc_gmm_prepare.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(gc_gmm)]
+_lib.gc_gmm_prepare.restype = ctypes.c_int
 _lib.gc_solve_batch_host.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_batch), ctypes.c_void_p]
 _lib.gc_solve_batch_host.restype = ctypes.c_int
 _lib.gc_last_error.argtypes = [ctypes.c_void_p]
@@ -80,7 +106,7 @@ _lib.gc_frame_digest.restype = ctypes.c_int
 
 EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
             "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "gc_frame_digest",
-            "gc_solve_sequences")
+            "gc_solve_sequences", "gc_solve_energy", "gc_gmm_prepare")
 
 
 class GcError(RuntimeError):
@@ -107,6 +133,32 @@ def gc_solve_batch(ctx, batch: gc_batch, stream: int) -> int:
 
 def gc_solve_sequences(ctx, batch: gc_seq_batch, stream: int) -> int:
     return _lib.gc_solve_sequences(ctx, ctypes.byref(batch), ctypes.c_void_p(stream))
+
+
+def gc_solve_energy(ctx, batch: gc_energy_batch, stream: int) -> int:
+    return _lib.gc_solve_energy(ctx, ctypes.byref(batch), ctypes.c_void_p(stream))
+
+
+def gc_gmm_prepare(weights, means, covs) -> gc_gmm:
+    """gc_gmm of one label from M weights, means [M,3], covariances [M,3,3] (host, double)."""
+    w = np.ascontiguousarray(weights, np.float64)
+    mu = np.ascontiguousarray(means, np.float64)
+    cv = np.ascontiguousarray(covs, np.float64)
+    out = gc_gmm()
+    st = _lib.gc_gmm_prepare(int(w.shape[0]), w.ctypes.data, mu.ctypes.data, cv.ctypes.data, ctypes.byref(out))
+    if st != 0:
+        raise GcError(st, "gc_gmm_prepare: bad mixture")
+    return out
+
+
+def gmm_table(pairs):
+    """[n][2] gc_gmm array (label 0, label 1 per frame) as raw bytes (uint8 numpy), from a list
+    of (bg, obj) tuples of (weights, means, covs)."""
+    arr = (gc_gmm * (2 * len(pairs)))()
+    for i, (bg, ob) in enumerate(pairs):
+        arr[2 * i] = gc_gmm_prepare(*bg)
+        arr[2 * i + 1] = gc_gmm_prepare(*ob)
+    return np.frombuffer(bytes(arr), np.uint8).copy()
 
 
 def gc_solve_batch_host(ctx, batch: gc_batch, stream: int) -> int:
@@ -258,6 +310,41 @@ class GridCut:
             res.append(fs)
         if stats:
             res.append(stt)
+        return tuple(res)
+
+    def solve_energy(self, image, prior, gmm, lam=10.0, sigma=0.1, kappa=0.05, eps=1e-6, scale=64.0, warm_flow=None,
+                     flow_state=False, stats=False, caps=False, stream=None, allow=(), out=None):
+        """gc_solve_energy: image [n,H,W,3] uint8, prior [n,H,W] uint16 (torch CUDA tensors), gmm a
+        CUDA uint8 tensor holding the [n][2] gc_gmm table (gmm_table).  Returns flow, mask
+        (+ flow state, + stats, + the caps [n, 2+K, H, W] the solve built)."""
+        import torch
+        n, H, W, _ = image.shape
+        K = self.K
+        assert image.dtype == torch.uint8 and prior.dtype == torch.uint16 and gmm.dtype == torch.uint8
+        assert prior.shape == (n, H, W) and gmm.numel() == n * 2 * ctypes.sizeof(gc_gmm)
+        for t in (image, prior, gmm):
+            assert t.is_cuda and t.is_contiguous()
+        dev = image.device
+        if out is None:
+            flow = torch.empty(n, dtype=torch.int64, device=dev)
+            mask = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
+        else:
+            flow, mask = out
+        fs = torch.empty((n, K // 2, H, W), dtype=torch.int32, device=dev) if flow_state else None
+        stt = torch.empty((n, 4), dtype=torch.int32, device=dev) if stats else None
+        cp = torch.empty((n, 2 + K, H, W), dtype=torch.int32, device=dev) if caps else None
+        b = gc_energy_batch(n, H, W, _ptr(image), _ptr(prior), _ptr(gmm),
+                            gc_energy_params(lam, sigma, kappa, eps, scale), _ptr(warm_flow), _ptr(flow),
+                            _ptr(mask), _ptr(fs), _ptr(stt), _ptr(cp))
+        s = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
+        self.last_status = self._check(gc_solve_energy(self.ctx, b, s), allow)
+        res = [flow, mask]
+        if flow_state:
+            res.append(fs)
+        if stats:
+            res.append(stt)
+        if caps:
+            res.append(cp)
         return tuple(res)
 
     def solve_host(self, cap_s, cap_t, cap_nb, warm_flow=None, flow_state=False, stats=False, stream=0,

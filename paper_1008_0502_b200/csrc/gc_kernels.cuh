@@ -84,6 +84,11 @@ struct Dev {
   int32_t* tsk;     // [NS]   global relabel (fbe) in which the tile's seed was skipped (its
                     //        border heights, all 1 in frame, are final for that relabel)
   // per frame slot (state machine): zero-initialised by one memset
+  const int32_t** scs;  // [nslot] the slot's frame's cap planes: c(s,v) [H][W], c(v,t) [H][W] and
+  const int32_t** sct;  //         the n-links [K][H][W] -- the caller's arrays, or (energy mode)
+  const int32_t** snb;  //         the slot's cap buffer the init pass builds them into
+  int32_t* capbuf;      // energy mode: [nslot][2+K][H][W] capacities built from the energy, or
+  int capbyframe;       //   (capbyframe) the caller's caps_out [n][2+K][H][W], indexed by frame
   const int32_t** swf;  // [nslot] warm-start flows of the slot's frame ([K/2][H][W]) or NULL
   int32_t** sfs;        // [nslot] where the slot's frame exports its flows ([K/2][H][W]) or NULL
   int32_t* fbuf;        // sequence mode, warm: [nslot][2][K/2][H][W] ping-pong flow buffers (frame
@@ -136,6 +141,15 @@ struct Dev {
 
 enum { M_INIT = 0, M_SEED = 1, M_BFS = 2, M_PUSH = 3, M_CSEED = 4, M_CLOS = 5, M_IDLE = 8 };
 
+// NEXT-1 energy mode (gc_solve_energy): colour GMM of one label, as include/gc.h's gc_gmm.
+constexpr int GMM_MAX = 4;
+struct Gmm {
+  int M, pad_;
+  double lognorm[GMM_MAX];  // log w_m - 1/2 log((2 pi)^3 det S_m)   (computed on the host)
+  double mean[GMM_MAX][3];
+  double prec[GMM_MAX][6];  // S_m^-1: xx, xy, xz, yy, yz, zz
+};
+
 struct IO {
   const int32_t* cs;
   const int32_t* ct;
@@ -145,6 +159,13 @@ struct IO {
   uint8_t* mask;
   int32_t* fstate;
   int32_t* stats;
+  // energy mode (NULL img: the caller gives the caps): the init pass builds every frame's caps
+  // from its RGB image, prior and colour GMMs into the slot's cap buffer
+  const uint8_t* img;     // [n][H][W][3]
+  const uint16_t* prior;  // [n][H][W]: p(A=1) = prior / 65535
+  const Gmm* gmm;         // [n][2]: label 0 (background), label 1 (object)
+  const int32_t* nlut;    // [2][256]: quantised n-link cap by |dI| (axial, diagonal), built per call
+  double eps, scale;      // prior clamp, quantisation scale
 };
 
 __device__ __forceinline__ size_t NS(const Dev& d) { return (size_t)d.nslot * d.T; }
@@ -338,9 +359,9 @@ __device__ __forceinline__ void tile_from_caps(const Dev& d, const IO& io, int s
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const size_t f = (size_t)d.sfr[s];  // batch frame held by this slot
-  const int32_t* cs = io.cs + f * plane;
-  const int32_t* ct = io.ct + f * plane;
-  const int32_t* nb = io.nb + f * plane * K;
+  const int32_t* cs = d.scs[s];
+  const int32_t* ct = d.sct[s];
+  const int32_t* nb = d.snb[s];
   const int32_t* wf = d.swf[s];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -463,11 +484,11 @@ __device__ __forceinline__ void px_er(const Dev& d, const IO& io, size_t gt, int
   const int H = d.H, W = d.W;
   const size_t plane = (size_t)H * W;
   const size_t f = (size_t)d.sfr[s];
-  const int32_t* nb = io.nb + f * plane * K;
+  const int32_t* nb = d.snb[s];
   const int32_t* wf = d.swf[s];
   const bool in = y < H && x < W;
   const size_t o = (size_t)y * W + x;
-  e = in ? __ldg(io.cs + f * plane + o) - __ldg(io.ct + f * plane + o) : 0;
+  e = in ? __ldg(d.scs[s] + o) - __ldg(d.sct[s] + o) : 0;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int y2 = y + DYk(k), x2 = x + DXk(k);
@@ -509,9 +530,9 @@ __device__ __forceinline__ FramePtrs frame_ptrs(const Dev& d, const IO& io, int 
   const size_t fr = (size_t)d.sfr[s];  // batch frame held by this slot
   FramePtrs p;
   p.fr = fr;
-  p.cs = io.cs + fr * plane;
-  p.ct = io.ct + fr * plane;
-  p.nb = io.nb + fr * plane * K;
+  p.cs = d.scs[s];
+  p.ct = d.sct[s];
+  p.nb = d.snb[s];
   p.wf = d.swf[s];
   p.fs = d.sfs[s];
   return p;
@@ -597,9 +618,9 @@ __device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_
   }
   const size_t plane = (size_t)H * W;
   const size_t f = (size_t)d.sfr[s];
-  const int32_t* cs = io.cs + f * plane;
-  const int32_t* ct = io.ct + f * plane;
-  const int32_t* nb = io.nb + f * plane * K;
+  const int32_t* cs = d.scs[s];
+  const int32_t* ct = d.sct[s];
+  const int32_t* nb = d.snb[s];
   const int32_t* wf = d.swf[s];
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
@@ -720,7 +741,7 @@ struct InitPart {
 template <int K, bool WARM, bool EXPORT>
 __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_t gt, const FramePtrs& P,
                                                const int (&a)[4], const int (&b)[4], const int (&c)[K][4],
-                                               InitPart* part) {
+                                               InitPart* part, bool sym = false) {
   const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
@@ -766,7 +787,8 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
         if (WARM && on) {  // a1w: clamp the previous flow to the new capacities
           const int y2 = y + DYk(k), x2 = x + DXk(k);
           const size_t oq = (size_t)y2 * W + x2;
-          const int cq = __ldg(nb + (k ^ 1) * plane + oq);
+          // energy caps are symmetric (c(q -> p) = c(p -> q)): the neighbour's may not be built yet
+          const int cq = sym ? ck : __ldg(nb + (k ^ 1) * plane + oq);
           if ((k & 1) == 0) {
             const int fv = max(-cq, min(ck, __ldg(wf + (k >> 1) * plane + o0 + i)));
             rk = ck - fv;
@@ -899,6 +921,109 @@ __device__ __forceinline__ void init_prefetch(const Dev& d, const FramePtrs& P, 
 template <int K>
 constexpr size_t init_smem_bytes() {
   return INIT_GMAX * sizeof(InitPart) + INIT_GMAX * sizeof(int) + 128 + (2 + K) * NTH * 16;
+}
+
+// ---- NEXT-1: the energy of §4 -> capacities, in the init pass (energy mode).
+// t-links: c(s,v) = psi1(A=0) + xi1(A=0) = -log p(C|A=0) - log(1 - p),
+//                      c(v,t) = psi1(A=1) + xi1(A=1) = -log p(C|A=1) - log p,
+// with p(C|A) a colour GMM (normalisation terms from the host) and
+// p = clamp(prior / 65535, eps, 1 - eps); n-links (reading c5):
+// B = lambda exp(-(dI/255)^2 / (2 sigma^2)) / dist + kappa on the integer luma
+// I = (77 R + 150 G + 29 B + 128) >> 8, looked up by |dI| in nlut.  q(x) = floor(scale x + 0.5)
+// clamped to [0, GC_CAP_MAX].  Evaluated in double precision (the oracle's precision).
+__device__ __forceinline__ int e_quant(double x, double scale) {
+  const double v = floor(scale * x + 0.5);
+  return v <= 0.0 ? 0 : (v >= (double)CAPMAX ? CAPMAX : (int)v);
+}
+__device__ __forceinline__ double e_gmm_nll(const Gmm& g, double r, double gg, double b) {
+  double v[GMM_MAX], mx = -1e300;
+#pragma unroll
+  for (int m = 0; m < GMM_MAX; ++m) {
+    if (m >= g.M) break;
+    const double dr = r - g.mean[m][0], dg = gg - g.mean[m][1], db = b - g.mean[m][2];
+    const double* P = g.prec[m];
+    const double q = P[0] * dr * dr + P[3] * dg * dg + P[5] * db * db +
+                     2.0 * (P[1] * dr * dg + P[2] * dr * db + P[4] * dg * db);
+    v[m] = g.lognorm[m] - 0.5 * q;
+    mx = fmax(mx, v[m]);
+  }
+  double sum = 0.0;
+#pragma unroll
+  for (int m = 0; m < GMM_MAX; ++m) {
+    if (m >= g.M) break;
+    sum += exp(v[m] - mx);
+  }
+  return -(mx + log(sum));
+}
+__device__ __forceinline__ int e_luma(const uint8_t* px) { return (77 * px[0] + 150 * px[1] + 29 * px[2] + 128) >> 8; }
+
+// Caps of this thread's 4 pixels (row t/8, columns 4(t%8)..+3 of tile (ty, tx)) from the energy,
+// stored into the slot's cap buffer (the later phases read them there); off-frame: 0.
+template <int K>
+__device__ __forceinline__ void energy_caps(const Dev& d, const IO& io, const FramePtrs& P, int ty, int tx, int (&a)[4],
+                                            int (&b)[4], int (&c)[K][4]) {
+  const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
+  const int H = d.H, W = d.W;
+  const size_t plane = (size_t)H * W;
+  const int y = ty * TS + iy, x0 = tx * TS + ix0;
+  const uint8_t* img = io.img + P.fr * plane * 3;
+  const uint16_t* pr = io.prior + P.fr * plane;
+  const Gmm& g0 = io.gmm[2 * P.fr];
+  const Gmm& g1 = io.gmm[2 * P.fr + 1];
+  // luma of the 3 x 6 neighbourhood of the 4 pixels (rows y-1..y+1, columns x0-1..x0+4)
+  int lu[3][6];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int yy = y - 1 + r, xx = x0 - 1 + q;
+      lu[r][q] = ((unsigned)yy < (unsigned)H && (unsigned)xx < (unsigned)W) ? e_luma(img + ((size_t)yy * W + xx) * 3) : 0;
+    }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int x = x0 + i;
+    a[i] = b[i] = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) c[k][i] = 0;
+    if (y >= H || x >= W) continue;
+    const uint8_t* pxl = img + ((size_t)y * W + x) * 3;
+    const double R = pxl[0], G = pxl[1], B = pxl[2];
+    double p = (double)__ldg(pr + (size_t)y * W + x) / 65535.0;
+    p = fmin(fmax(p, io.eps), 1.0 - io.eps);
+    a[i] = e_quant(e_gmm_nll(g0, R, G, B) - log(1.0 - p), io.scale);  // c(s,v): label 0
+    b[i] = e_quant(e_gmm_nll(g1, R, G, B) - log(p), io.scale);        // c(v,t): label 1
+    const int lc = lu[1][i + 1];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int y2 = y + DYk(k), x2 = x + DXk(k);
+      if ((unsigned)y2 >= (unsigned)H || (unsigned)x2 >= (unsigned)W) continue;
+      const int dI = abs(lc - lu[1 + DYk(k)][i + 1 + DXk(k)]);
+      c[k][i] = __ldg(io.nlut + (k >= 4 ? 256 : 0) + dI);
+    }
+  }
+  // the slot's cap buffer, frame layout (16-byte stores when the row allows)
+  if (y < H) {
+    const size_t o0 = (size_t)y * W + x0;
+    int32_t* cs = const_cast<int32_t*>(P.cs);
+    int32_t* ct = const_cast<int32_t*>(P.ct);
+    int32_t* nb = const_cast<int32_t*>(P.nb);
+    if (x0 + 3 < W && (W & 3) == 0) {
+      *reinterpret_cast<int4*>(cs + o0) = make_int4(a[0], a[1], a[2], a[3]);
+      *reinterpret_cast<int4*>(ct + o0) = make_int4(b[0], b[1], b[2], b[3]);
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        *reinterpret_cast<int4*>(nb + k * plane + o0) = make_int4(c[k][0], c[k][1], c[k][2], c[k][3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (x0 + i >= W) continue;
+        cs[o0 + i] = a[i];
+        ct[o0 + i] = b[i];
+#pragma unroll
+        for (int k = 0; k < K; ++k) nb[k * plane + o0 + i] = c[k][i];
+      }
+    }
+  }
 }
 
 // ---- TMA (cp.async.bulk.tensor) staging of the init stream.  Tensor maps over the caller's
@@ -1042,6 +1167,29 @@ __device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0
       else if (P.fs) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
       else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i);
     }
+  }
+  __syncthreads();
+  init_finalize(d, gt0, n, part, uni_s);
+}
+
+// Energy-mode init pass over a group of tiles (out of line: its double-precision working set
+// would otherwise share the register allocation of the streaming cap path).
+template <int K>
+__device__ __forceinline__ void task_init_energy(const Dev& d, const IO& io, size_t gt0, int* smem) {
+  const int s = (int)((unsigned)gt0 / (unsigned)d.T), tile0 = (int)(gt0 - (size_t)s * d.T);
+  const int n = min(d.initg, d.T - tile0);
+  const FramePtrs P = frame_ptrs(d, io, s, K);
+  InitPart* part = reinterpret_cast<InitPart*>(smem);        // [n]
+  int* uni_s = reinterpret_cast<int*>(part + INIT_GMAX);     // [n]
+  int a[4], b[4], c[K][4];
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
+    energy_caps<K>(d, io, P, ty, tx, a, b, c);
+    if (P.wf && P.fs) tile_init_regs<K, true, true>(d, io, gt0 + i, P, a, b, c, part + i, true);
+    else if (P.wf) tile_init_regs<K, true, false>(d, io, gt0 + i, P, a, b, c, part + i, true);
+    else if (P.fs) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i, true);
+    else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i, true);
   }
   __syncthreads();
   init_finalize(d, gt0, n, part, uni_s);

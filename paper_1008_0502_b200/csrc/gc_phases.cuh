@@ -80,7 +80,18 @@ __device__ __forceinline__ int relabel_bound(const Dev& d, const Ctl& c, int ce)
 __device__ __forceinline__ void slot_assign(const Dev& d, const IO& io, const Ctl& c, int s, int f) {
   GC_CHECK(d, s >= 0 && s < d.nslot && f >= 0 && f < c.nframes);
   const size_t pl = (size_t)d.H * d.W * (c.K4 ? 2 : 4);
+  const size_t plane = (size_t)d.H * d.W, K = c.K4 ? 4 : 8;
   d.sfr[s] = f;
+  if (d.capbuf) {  // energy mode: the init pass builds the caps into the slot's buffer
+    int32_t* cb = d.capbuf + (size_t)(d.capbyframe ? f : s) * (2 + K) * plane;
+    d.scs[s] = cb;
+    d.sct[s] = cb + plane;
+    d.snb[s] = cb + 2 * plane;
+  } else {
+    d.scs[s] = io.cs + (size_t)f * plane;
+    d.sct[s] = io.ct + (size_t)f * plane;
+    d.snb[s] = io.nb + (size_t)f * plane * K;
+  }
   d.fbe[s] = 1;  // the frame's first global relabel is seeded by its init tasks
   d.fbnd[s] = relabel_bound(d, c, 0);
   if (!c.seqL) {
@@ -679,7 +690,7 @@ __device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t g
     for (int k = 0; k < K; k += 2) {
       const int y2 = y + DYk(k), x2 = x + DXk(k);
       int f = 0;
-      if (y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = io.nb[fr * plane * K + k * plane + o] - r[k];
+      if (y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) f = d.snb[s][k * plane + o] - r[k];
       fsp[(k >> 1) * plane + o] = f;
     }
   }
@@ -1308,7 +1319,9 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
 }
 
 // ---------------------------------------------------------------- the persistent kernel
-template <int K>
+// EN: energy mode (NEXT-1, the init pass builds the caps from the energy) -- a kernel of its own
+// so that the cap-streaming kernel carries none of its code or registers.
+template <int K, bool EN = false>
 __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ Dev d, const __grid_constant__ IO io,
                                                          const __grid_constant__ Ctl c, const __grid_constant__ Tmaps tm) {
   extern __shared__ __align__(128) int smem[];
@@ -1401,7 +1414,8 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
     int cls = 0;
     switch (md) {
       case M_INIT:
-        task_init<K>(d, io, gt, c.vec != 0, smem, tm, mbar, tpar);
+        if constexpr (EN) task_init_energy<K>(d, io, gt, smem);
+        else task_init<K>(d, io, gt, c.vec != 0, smem, tm, mbar, tpar);
         init_seed_group<K>(d, gt, smem);
         cls = 0;
         break;

@@ -65,6 +65,9 @@ struct gc_ctx {
   size_t words_bytes = 0;
   int32_t* fbuf = nullptr;  // sequence mode: ping-pong flow buffers of the slots
   size_t fbuf_bytes = 0;
+  int32_t* capbuf = nullptr;  // energy mode: the slots' cap buffers
+  size_t capbuf_bytes = 0;
+  int32_t* elut = nullptr;    // energy mode: n-link LUT [2][256]
 };
 
 namespace {
@@ -93,7 +96,7 @@ size_t frame_bytes(int K, size_t T) {
   b += T * K * 64;                // reach
   b += T * 8 + 13 * T * 4;        // neg0 + tile flags
   b += 2 * T * 4 * 2;             // queues (capacity >= 2 x tiles in flight)
-  b += 4 * 25 + 8 * 6;            // frame words
+  b += 4 * 25 + 8 * 9;            // frame words
   return b + 16 * 256;            // alignment slack
 }
 
@@ -131,7 +134,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
   // per-frame words and the queue counters first: contiguous, so one memset clears them
-  char* fw = take((size_t)nslot * (4 * 25 + 8 * 6) + 64 * 4);  // <= 25 int + 6 u64 per slot
+  char* fw = take((size_t)nslot * (4 * 25 + 8 * 9) + 64 * 4);  // <= 25 int + 9 u64 per slot
   int32_t* w = (int32_t*)fw;
   d.fmode = w; w += nslot;
   d.sfr = w; w += nslot;
@@ -155,7 +158,10 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.frel = u; u += nslot;
   d.sumct = u; u += nslot;
   d.sumneg = u; u += nslot;
-  d.swf = (const int32_t**)u; u += nslot;  // per-slot flow pointers (k_setup / refills assign)
+  d.scs = (const int32_t**)u; u += nslot;  // per-slot cap / flow pointers (k_setup / refills assign)
+  d.sct = (const int32_t**)u; u += nslot;
+  d.snb = (const int32_t**)u; u += nslot;
+  d.swf = (const int32_t**)u; u += nslot;
   d.sfs = (int32_t**)u; u += nslot;
   u = (unsigned long long*)align_up((size_t)u, 16);
   d.qhead = u; u += 1;
@@ -327,7 +333,7 @@ double now_s() {
 // sequence solved after frame t-1 in the same slot (warm-started from its flows if seqWarm).
 template <int K>
 gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaStream_t st, Launcher& L, int seqS = 0,
-                      int seqL = 0, int seqWarm = 0) {
+                      int seqL = 0, int seqWarm = 0, int32_t* caps_out = nullptr) {
   const int units = seqL ? seqS : nframes;  // slots serve frames, or whole sequences
   const int nslot = chunk_frames(c, H, W) < units ? chunk_frames(c, H, W) : units;
   size_t sg_bytes = 0, q_bytes = 0;
@@ -342,6 +348,24 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
       c->fbuf_bytes = need;
     }
     d.fbuf = c->fbuf;
+  }
+  if (io.img) {  // energy mode: caps built into the caller's caps_out, else the slots' buffers
+    if (caps_out) {
+      d.capbuf = caps_out;
+      d.capbyframe = 1;
+    } else {
+      const size_t need = (size_t)nslot * (2 + K) * H * W * 4;
+      if (need > c->capbuf_bytes) {
+        if (c->capbuf) cudaFree(c->capbuf);
+        c->capbuf = nullptr;
+        c->capbuf_bytes = 0;
+        if (cudaMalloc(&c->capbuf, need) != cudaSuccess) { cudaGetLastError(); c->err = "cap buffers"; return GC_ERR_OOM; }
+        c->capbuf_bytes = need;
+      }
+      d.capbuf = c->capbuf;
+    }
+    if (caps_out && !ck(c, cudaMemsetAsync(caps_out, 0, (size_t)nframes * (2 + K) * H * W * 4, st), "memset"))
+      return GC_ERR_CUDA;  // off-grid entries stay 0
   }
   // unfinished frames read F = -1 and status 0 until the kernel writes them (k_abort relies on it)
   if (!ck(c, cudaMemsetAsync(io.flow, 0xff, (size_t)nframes * 8, st), "memset")) return GC_ERR_CUDA;
@@ -375,14 +399,15 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   ctl.seqWarm = seqWarm;
   // int4 loads in the init pass when every caller row is 16-byte aligned
   ctl.vec = (W % 4 == 0) && ((uintptr_t)io.cs % 16 == 0) && ((uintptr_t)io.ct % 16 == 0) &&
-            ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0);
+            ((uintptr_t)io.nb % 16 == 0) && (!io.wf || (uintptr_t)io.wf % 16 == 0) &&
+            (!d.capbuf || (uintptr_t)d.capbuf % 16 == 0);
   // watchdog: max_launches "sweeps" of the tiles in flight
   const double mt = (double)c->max_launches * (double)ns;
   ctl.max_tasks = mt > 9e18 ? (long long)9e18 : (long long)mt;
   *c->habort = 0;
   Tmaps tm;
   memset(&tm, 0, sizeof(tm));
-  tm.on = ctl.vec && c->tma && make_tmaps(c, io, nframes, H, W, K, &tm);
+  tm.on = ctl.vec && c->tma && !io.img && make_tmaps(c, io, nframes, H, W, K, &tm);
   k_setup<<<(unsigned)((ns + NTH - 1) / NTH < 4096 ? (ns + NTH - 1) / NTH : 4096), NTH, 0, st>>>(d, io, ctl);
   ++L.n;
   // the launch's device time, always measured (gc_get_kernel_ms): two events per launch
@@ -396,7 +421,8 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   cudaEvent_t e0 = c->evpool[c->evnext++];
   cudaEvent_t e1 = c->evpool[c->evnext++];
   cudaEventRecord(e0, st);
-  k_solve<K><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
+  if (io.img) k_solve<K, true><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
+  else k_solve<K><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
   ++L.n;
   cudaEventRecord(e1, st);
   c->pending.push_back({0, {e0, e1}});
@@ -471,6 +497,19 @@ gc_status worst(gc_status a, gc_status b) {
   if (a == GC_ERR_RANGE || b == GC_ERR_RANGE) return GC_ERR_RANGE;
   if (a == GC_ERR_NOCONV || b == GC_ERR_NOCONV) return GC_ERR_NOCONV;
   return a != GC_OK ? a : b;
+}
+
+static_assert(sizeof(gc_gmm) == sizeof(Gmm), "gc_gmm and the device Gmm share one layout");
+
+// NEXT-1: the n-link cap by |dI| (0..255) for axial (row 0) and diagonal (row 1) arcs, in
+// double precision (include/gc.h gc_energy_params).
+__global__ void k_energy_lut(double lambda, double sigma, double kappa, double scale, int32_t* lut) {
+  const int j = blockIdx.x, dI = threadIdx.x;
+  const double x = dI / 255.0;
+  const double dist = j ? sqrt(2.0) : 1.0;
+  const double B = lambda * exp(-(x * x) / (2.0 * sigma * sigma)) / dist + kappa;
+  const double v = floor(scale * B + 0.5);
+  lut[j * 256 + dI] = v <= 0.0 ? 0 : (v >= (double)CAPMAX ? CAPMAX : (int)v);
 }
 
 // a6: per-frame digest of solved frames (gc_frame_digest): F, popcount and a 64-bit hash of
@@ -583,6 +622,9 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
     const size_t smem = c->K == 8 ? solve_smem_bytes<8>() : solve_smem_bytes<4>();
     cudaError_t e = c->K == 8 ? cudaFuncSetAttribute(k_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                               : cudaFuncSetAttribute(k_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = c->K == 8 ? cudaFuncSetAttribute(k_solve<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                    : cudaFuncSetAttribute(k_solve<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     c->grid_max = c->K == 8 ? persistent_grid(c, k_solve<8>, smem) : persistent_grid(c, k_solve<4>, smem);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -609,6 +651,8 @@ void gc_destroy(gc_ctx* c) {
   if (c->dtiles) cudaFree(c->dtiles);
   if (c->trace) cudaFree(c->trace);
   if (c->fbuf) cudaFree(c->fbuf);
+  if (c->capbuf) cudaFree(c->capbuf);
+  if (c->elut) cudaFree(c->elut);
   delete c;
 }
 
@@ -692,6 +736,64 @@ gc_status gc_frame_digest(gc_ctx* c, int n, int H, int W, const int64_t* flow, c
   if (!ck(c, cudaStreamSynchronize(st), "k_digest")) return GC_ERR_CUDA;
   c->last_launches = 1;
   return GC_OK;
+}
+
+gc_status gc_gmm_prepare(int M, const double* w, const double* mean, const double* cov, gc_gmm* out) {
+  if (M < 1 || M > GC_GMM_MAX || !w || !mean || !cov || !out) return GC_ERR_ARG;
+  memset(out, 0, sizeof(*out));
+  out->M = M;
+  for (int m = 0; m < M; ++m) {
+    const double* S = cov + 9 * m;
+    if (!(w[m] > 0)) return GC_ERR_ARG;
+    // inverse and determinant of the symmetric 3x3 S by cofactors (double precision)
+    const double a = S[0], b = S[1], cc = S[2], e = S[4], f = S[5], i = S[8];
+    const double A = e * i - f * f, B = -(b * i - f * cc), C = b * f - e * cc;
+    const double det = a * A + b * B + cc * C;
+    if (!(det > 0) || !(a > 0) || !(a * e - b * b > 0)) return GC_ERR_ARG;  // Sylvester: positive definite
+    const double E = a * i - cc * cc, F = -(a * f - b * cc), I = a * e - b * b;
+    out->prec[m][0] = A / det; out->prec[m][1] = B / det; out->prec[m][2] = C / det;
+    out->prec[m][3] = E / det; out->prec[m][4] = F / det; out->prec[m][5] = I / det;
+    for (int j = 0; j < 3; ++j) out->mean[m][j] = mean[3 * m + j];
+    out->lognorm[m] = log(w[m]) - 0.5 * (3.0 * log(2.0 * M_PI) + log(det));
+  }
+  return GC_OK;
+}
+
+gc_status gc_solve_energy(gc_ctx* c, const gc_energy_batch* b, void* stream) {
+  if (!c) return GC_ERR_ARG;
+  if (!b) { c->err = "energy batch is NULL"; return GC_ERR_ARG; }
+  const gc_energy_params& p = b->params;
+  if (b->n < 0 || b->H <= 0 || b->W <= 0 || b->H > c->max_h || b->W > c->max_w) {
+    c->err = "bad dims";
+    return GC_ERR_ARG;
+  }
+  if (b->n > 0 && (!b->image || !b->prior || !b->gmm || !b->flow_out || !b->mask_out)) {
+    c->err = "NULL required pointer";
+    return GC_ERR_ARG;
+  }
+  if (!(p.sigma > 0) || !(p.eps > 0 && p.eps < 0.5) || !(p.scale > 0) || !(p.lambda >= 0) || !(p.kappa >= 0)) {
+    c->err = "bad energy parameters";
+    return GC_ERR_ARG;
+  }
+  c->err.clear();
+  cudaSetDevice(c->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  Launcher L{c, st};
+  gc_status res = GC_OK;
+  if (b->n > 0) {
+    if (!c->elut && !ck(c, cudaMalloc(&c->elut, 2 * 256 * 4), "lut alloc")) return GC_ERR_OOM;
+    k_energy_lut<<<2, 256, 0, st>>>(p.lambda, p.sigma, p.kappa, p.scale, c->elut);
+    ++L.n;
+    IO io{nullptr, nullptr, nullptr, b->warm_flow, b->flow_out, b->mask_out, b->flow_state_out, b->stats_out,
+          b->image, b->prior, reinterpret_cast<const Gmm*>(b->gmm), c->elut, p.eps, p.scale};
+    res = (c->K == 8) ? solve_chunk<8>(c, io, b->n, b->H, b->W, st, L, 0, 0, 0, b->caps_out)
+                      : solve_chunk<4>(c, io, b->n, b->H, b->W, st, L, 0, 0, 0, b->caps_out);
+  }
+  c->last_launches = L.n;
+  resolve_timing(c);
+  if (c->prof) resolve_profile(c);
+  if (res == GC_ERR_NOCONV && c->err.empty()) c->err = "max_launches exceeded before convergence";
+  return res;
 }
 
 gc_status gc_solve_batch(gc_ctx* c, const gc_batch* b, void* stream) {

@@ -42,6 +42,12 @@ def lib():
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         L.sy_set_random_params.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.sy_set_serp_params.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.sy_gen_energy_host.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        L.sy_gen_energy_host.restype = None
+        L.sy_gen_energy_cuda.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.sy_gen_energy_cuda.restype = ctypes.c_int
         _LIB = L
     return _LIB
 
@@ -121,3 +127,42 @@ def offgrid_mask(H: int, W: int, K: int):
         y2, x2 = y + DY[k], x + DX[k]
         out[k] = (y2 < 0) | (y2 >= H) | (x2 < 0) | (x2 >= W)
     return out
+
+
+# ---------------------------------------------------------------- energy inputs (NEXT-1)
+def gen_energy_host(seed: int, t0: int, n: int, H: int, W: int, seq_len: int = 0):
+    """Blob frames as energy inputs: RGB image [n,H,W,3] uint8 and prior code [n,H,W] uint16."""
+    rgb = np.empty((n, H, W, 3), np.uint8)
+    prior = np.empty((n, H, W), np.uint16)
+    lib().sy_gen_energy_host(seed, t0, n, H, W, int(seq_len), rgb.ctypes.data, prior.ctypes.data)
+    return rgb, prior
+
+
+def gen_energy_torch(seed: int, t0: int, n: int, H: int, W: int, seq_len: int = 0, device="cuda"):
+    """CUDA twin of gen_energy_host (bit-identical)."""
+    import torch
+    rgb = torch.empty((n, H, W, 3), dtype=torch.uint8, device=device)
+    prior = torch.empty((n, H, W), dtype=torch.uint16, device=device)
+    rc = lib().sy_gen_energy_cuda(seed, t0, n, H, W, int(seq_len), ctypes.c_void_p(rgb.data_ptr()),
+                                  ctypes.c_void_p(prior.data_ptr()),
+                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"sy_gen_energy_cuda failed rc={rc}")
+    return rgb, prior
+
+
+def energy_gmms():
+    """The colour model of the synthetic blob frames as two 2-component RGB GMMs (weights [2],
+    means [2,3], covariances [2,3,3]) for label 0 (background ~ 80-120 grey) and label 1
+    (objects ~ 200 grey); grey colours make the channels strongly correlated.  Input data for
+    gc_solve_energy (the paper fits these with EM, P:293-301, P:580-582 -- out of scope)."""
+    J = np.ones((3, 3))
+    I3 = np.eye(3)
+    bg = (np.array([0.6, 0.4]), np.array([[100.0, 100.0, 100.0], [85.0, 88.0, 92.0]]),
+          np.stack([30.0 ** 2 * (0.95 * J + 0.05 * I3), 20.0 ** 2 * (0.9 * J + 0.1 * I3)]))
+    ob = (np.array([0.7, 0.3]), np.array([[200.0, 200.0, 200.0], [190.0, 205.0, 195.0]]),
+          np.stack([25.0 ** 2 * (0.95 * J + 0.05 * I3), 20.0 ** 2 * (0.85 * J + 0.15 * I3)]))
+    return bg, ob
+
+
+ENERGY_PARAMS = dict(lam=10.0, sigma=0.1, kappa=0.05, eps=1e-6, scale=64.0)  # reading c5 / c9 / c11

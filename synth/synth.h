@@ -252,6 +252,21 @@ SY_HD void sy_pixel(const sy_luts* L, const sy_frame* f, int K, int garbage, int
   }
 }
 
+/* ---- energy inputs (NEXT-1, gc_solve_energy): the same blob frame as RGB + prior code --------
+ * RGB = the frame intensity I (sy_intensity) plus per-channel hash noise in [-4, 4]; prior code
+ * u = round(0.95 (i + 0.5) / SY_NP x 65535) of the frame's prior index i (the value the cap
+ * generator's t-link LUT uses), 0 in the frame-edge band.  Integer only.          */
+SY_HD void sy_energy_pixel(const sy_luts* L, const sy_frame* f, int y, int x, uint8_t* rgb, uint16_t* prior) {
+  int I = sy_intensity(f, y, x);
+  uint64_t h = sy_hash(f->seed, f->frame, y, x, 40);
+  for (int c = 0; c < 3; ++c) {
+    int v = I + (int)((h >> (8 * c)) % 9u) - 4;
+    rgb[c] = (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+  }
+  int pi = sy_prior_index(L, f, y, x);
+  *prior = pi >= SY_NP ? (uint16_t)0 : (uint16_t)(((int64_t)(2 * pi + 1) * 62258 + SY_NP) / (2 * SY_NP));
+}
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -263,6 +278,9 @@ void sy_gen_host(int kind, uint64_t seed, int t0, int n, int H, int W, int K, in
                  int32_t* cs, int32_t* ct, int32_t* cnb);
 void sy_set_random_params(int rmax_t, int rmax_n, int rzero_pct);
 void sy_set_serp_params(int lane, int big);
+void sy_gen_energy_host(uint64_t seed, int t0, int n, int H, int W, int seq_len, uint8_t* rgb, uint16_t* prior);
+int sy_gen_energy_cuda(uint64_t seed, int t0, int n, int H, int W, int seq_len, uint8_t* rgb, uint16_t* prior,
+                       void* stream);
 /* CUDA twin (synth_cuda.cu): device pointers, returns 0 on success */
 int sy_gen_cuda(int kind, uint64_t seed, int t0, int n, int H, int W, int K, int garbage, int seq_len,
                 int32_t* cs, int32_t* ct, int32_t* cnb, void* stream);

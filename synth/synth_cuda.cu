@@ -64,3 +64,48 @@ extern "C" int sy_gen_cuda(int kind, uint64_t seed, int t0, int n, int H, int W,
   }
   return 0;
 }
+
+__global__ void sy_energy_kernel(const sy_luts* __restrict__ L, const sy_frame* __restrict__ frames, int H, int W,
+                                 uint8_t* rgb, uint16_t* prior) {
+  __shared__ sy_frame f;
+  int i = blockIdx.z;
+  if (threadIdx.x == 0 && threadIdx.y == 0) f = frames[i];
+  __syncthreads();
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= W || y >= H) return;
+  int64_t o = (int64_t)i * H * W + (int64_t)y * W + x;
+  sy_energy_pixel(L, &f, y, x, rgb + 3 * o, prior + o);
+}
+
+extern "C" int sy_gen_energy_cuda(uint64_t seed, int t0, int n, int H, int W, int seq_len, uint8_t* rgb,
+                                  uint16_t* prior, void* stream) {
+  int32_t dummy;
+  (void)dummy;
+  if (sy_gen_cuda(SY_KIND_BLOB, seed, t0, 0, H, W, 4, 0, seq_len, nullptr, nullptr, nullptr, stream) != 0) return 2;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) return 0;
+  const int CH = 65535;
+  for (int base = 0; base < n; base += CH) {
+    int m = n - base < CH ? n - base : CH;
+    sy_frame* hf = (sy_frame*)malloc(sizeof(sy_frame) * m);
+    for (int i = 0; i < m; ++i) {
+      int t = t0 + base + i;
+      int seq_t = seq_len > 0 ? (t % seq_len) : t;
+      sy_make_frame(&hf[i], SY_KIND_BLOB, seed, H, W, t, seq_t);
+    }
+    sy_frame* df = nullptr;
+    if (cudaMalloc(&df, sizeof(sy_frame) * m) != cudaSuccess) { free(hf); return 2; }
+    cudaMemcpyAsync(df, hf, sizeof(sy_frame) * m, cudaMemcpyHostToDevice, st);
+    dim3 blk(32, 8, 1);
+    dim3 grd((W + 31) / 32, (H + 7) / 8, m);
+    int64_t plane = (int64_t)H * W;
+    sy_energy_kernel<<<grd, blk, 0, st>>>(g_dev_luts, df, H, W, rgb + base * plane * 3, prior + base * plane);
+    cudaError_t e = cudaGetLastError();
+    cudaStreamSynchronize(st);
+    cudaFree(df);
+    free(hf);
+    if (e != cudaSuccess) { fprintf(stderr, "sy_gen_energy_cuda: %s\n", cudaGetErrorString(e)); return 3; }
+  }
+  return 0;
+}

@@ -134,3 +134,21 @@ void sy_gen_host(int kind, uint64_t seed, int t0, int n, int H, int W, int K, in
       }
   }
 }
+
+void sy_gen_energy_host(uint64_t seed, int t0, int n, int H, int W, int seq_len, uint8_t* rgb, uint16_t* prior) {
+  static sy_luts L;
+  static int built = 0;
+  if (!built) { sy_build_luts(&L); built = 1; }
+  int64_t plane = (int64_t)H * W;
+  for (int i = 0; i < n; ++i) {
+    int t = t0 + i;
+    int seq_t = seq_len > 0 ? (t % seq_len) : t;
+    sy_frame f;
+    sy_make_frame(&f, SY_KIND_BLOB, seed, H, W, t, seq_t);
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        int64_t o = (int64_t)i * plane + (int64_t)y * W + x;
+        sy_energy_pixel(&L, &f, y, x, rgb + 3 * o, prior + o);
+      }
+  }
+}
