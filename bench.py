@@ -416,6 +416,74 @@ def run_energy(args, cfg):
         dist.destroy_process_group()
 
 
+def run_prior(args, cfg):
+    """NEXT-2: gc_prior_update over this rank's frames -- the previous mask
+    smoothed (radius-12 Gaussian, sigma 4) and fused with the saliency prior by the §6 weights
+    (P:411-438).  Masks: the synthetic frames' prior > 1/2 (blob shapes); q: their prior codes."""
+    import torch
+
+    import paper_1008_0502_b200 as gc
+    import synth
+    from paper_1008_0502_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    H, W, n = cfg["H"], cfg["W"], cfg["frames"]
+    seed = synth.BASE_SEED + cfg["seed_off"]
+    t_first, n = shard.frame_range(rank, world, n)
+    img, q = synth.gen_energy_torch(seed, t_first, n, H, W, device=dev)
+    del img
+    mask = (q.to(torch.int32) > 32768).to(torch.uint8)
+    wfv, _ = gc.gc_kalman_step(0.03 ** 2, 0.035 ** 2, 6.0308884908e-4)
+    wf = torch.full((n,), wfv, dtype=torch.int32, device=dev)
+    params = gc.prior_params(4.0, 12, 8)
+    out = torch.empty_like(q)
+    g = gc.GridCut(neighborhood=4, max_h=H, max_w=W)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        g.prior_update(mask, q, wf, params, out=out)
+    torch.cuda.synchronize()
+    clk = ClockSampler(None)
+    clk.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        g.prior_update(mask, q, wf, params, out=out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = shard.max_over_ranks(e0.elapsed_time(e1), dev, world)
+    px = world * n * H * W * args.steps
+    peak, peak_src = load_peak()
+    bpx = 1 + 2 + 2
+    ach = bpx * n * H * W * args.steps / (ms * 1e-3) / 1e9 / world * world
+    if rank == 0:
+        res = {"metric": METRIC, "value": round(px / (ms * 1e-3) / 1e6, 1), "unit": "Mpixel/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+               "data": "synthetic (blob masks and saliency prior codes, synth/; on device)",
+               "config": {"workload": f"NEXT-2 prior update (P:411-438) on {cfg['workload'].split(',')[0]} frames, "
+                                      f"{n} per rank, Gaussian radius 12 sigma 4, edge band 8",
+                          "H": H, "W": W, "frames_per_rank": n, "parallelism": f"frame-sharded dp{world}",
+                          "l2": "inputs >> 126 MB L2"},
+               "roofline": {"bound": "hbm", "kernel": "k_prior", "unit": "GB/s", "peak": peak,
+                            "achieved": round(ach / world, 1), "frac": round(ach / world / peak, 4),
+                            "bytes_rule": "5 B/px (read mask + saliency code, write the prior code)",
+                            "traffic": None, "peak_source": peak_src},
+               "gpu_launches": args.steps, "clocks": clocks}
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 def ctypes_sizeof_gmm(gc):
     import ctypes
     return ctypes.sizeof(gc.gc_gmm)
@@ -465,6 +533,7 @@ def main():
                     help="N > 1: each rank re-solves the first M frames of the next rank's shard")
     ap.add_argument("--energy", action="store_true",
                     help="NEXT-1: frames given as RGB image + prior + colour GMMs; caps built in the solve's init pass")
+    ap.add_argument("--prior", action="store_true", help="NEXT-2: the on-device prior update (gc_prior_update)")
     ap.add_argument("--warm", action="store_true",
                     help="sequence mode (C3): S sequences x L frames, frame t warm-started from t-1")
     ap.add_argument("--seqs", type=int, default=8)
@@ -483,6 +552,8 @@ def main():
         return run_warm(args, cfg)
     if args.energy:
         return run_energy(args, cfg)
+    if args.prior:
+        return run_prior(args, cfg)
 
     import numpy as np
     import torch

@@ -196,6 +196,39 @@ typedef struct {
  * gmm, sigma <= 0, eps outside (0, 0.5) or scale <= 0).  Device pointers. */
 gc_status gc_solve_energy(gc_ctx* ctx, const gc_energy_batch* batch, void* stream);
 
+/* ---- NEXT-2: the prior update of PAPER.md §6 on the device.
+ * For frame t: f(A_{t-1}, x) = the previous segmentation mask smoothed by a separable Gaussian
+ * (P:420-424), fused with the saliency prior q(A_t = 1) by the Kalman-style estimate as printed
+ * (reading c10):
+ *   p(A_t = 1) = w_f f + (1 - w_f) q,  w_f = s1 / (s1 + s2 + v(t-1)),
+ *   v(t) = s1 (s2 + v(t-1)) / (s1 + s2 + v(t-1))          (s1 = sigma_1^2, s2 = sigma_2^2)
+ * and p = 0 in a frame-edge band.  Exact integer arithmetic on the device:
+ *   R(y,x) = sum_i taps[|i|] mask(y, clamp(x+i)),  S(y,x) = sum_j taps[|j|] R(clamp(y+j), x)
+ *   (replicated border), G = sum_{|i|<=radius} taps[|i|], f = S / G^2,
+ *   prior(y,x) = 0 in the band, else (wf S 65535 + (4096 - wf) q G^2 + 2048 G^2) / (4096 G^2)
+ *   (integer division) -- i.e. round(65535 (w_f f + (1 - w_f) q / 65535)) with w_f = wf / 4096.
+ * wf comes from gc_kalman_step, taps from gc_gauss_taps (host helpers, double precision). */
+#define GC_PRIOR_RMAX 16
+typedef struct {
+  int radius;                      /* 0..GC_PRIOR_RMAX                                        */
+  int taps[GC_PRIOR_RMAX + 1];     /* taps[0..radius] >= 0, taps[0] > 0, each <= 1024           */
+  int band;                        /* >= 0 px                                                 */
+} gc_prior_params;
+
+/* taps[i] = floor(1024 exp(-i^2 / (2 sigma^2)) + 0.5), i = 0..radius; GC_ERR_ARG for sigma <= 0
+ * or radius outside 0..GC_PRIOR_RMAX.  Host only. */
+gc_status gc_gauss_taps(double sigma, int radius, int* taps);
+
+/* One step of the §6 recursion: *wf_q12 = floor(4096 s1 / (s1 + s2 + v_prev) + 0.5), *v_next as
+ * above.  GC_ERR_ARG unless s1 > 0, s2 >= 0, v_prev >= 0.  Host only. */
+gc_status gc_kalman_step(double s1, double s2, double v_prev, int* wf_q12, double* v_next);
+
+/* n frames: mask_prev [n][H][W] uint8 (0/1; nonzero counts as 1), q [n][H][W] uint16 saliency
+ * prior codes, wf [n] int32 (0..4096) -> prior_out [n][H][W] uint16 codes for gc_solve_energy.
+ * Device pointers; GC_ERR_ARG for bad dims, NULL pointers or bad params. */
+gc_status gc_prior_update(gc_ctx* ctx, int n, int H, int W, const uint8_t* mask_prev, const uint16_t* q,
+                          const int32_t* wf, const gc_prior_params* params, uint16_t* prior_out, void* stream);
+
 /* Message for the last failing call on this context ("" if none).  Never NULL. */
 const char* gc_last_error(const gc_ctx* ctx);
 

@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 __all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_solve_sequences",
-           "gc_solve_energy", "gc_gmm_prepare",
+           "gc_solve_energy", "gc_gmm_prepare", "gc_gauss_taps", "gc_kalman_step", "gc_prior_update",
            "gc_frame_digest", "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "CAP_MAX",
            "STATUS", "lib_path"]
 
@@ -73,6 +73,13 @@ class gc_energy_batch(ctypes.Structure):
                 ("flow_state_out", ctypes.c_void_p), ("stats_out", ctypes.c_void_p), ("caps_out", ctypes.c_void_p)]
 
 
+PRIOR_RMAX = 16
+
+
+class gc_prior_params(ctypes.Structure):
+    _fields_ = [("radius", ctypes.c_int), ("taps", ctypes.c_int * (PRIOR_RMAX + 1)), ("band", ctypes.c_int)]
+
+
 _lib.gc_create.argtypes = [ctypes.POINTER(gc_config), ctypes.POINTER(ctypes.c_void_p)]
 _lib.gc_create.restype = ctypes.c_int
 _lib.gc_destroy.argtypes = [ctypes.c_void_p]
@@ -85,6 +92,15 @@ _lib.gc_solve_energy.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_energy_batch
 _lib.gc_solve_energy.restype = ctypes.c_int
 _lib.gc_gmm_prepare.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(gc_gmm)]
 _lib.gc_gmm_prepare.restype = ctypes.c_int
+_lib.gc_gauss_taps.argtypes = [ctypes.c_double, ctypes.c_int, ctypes.c_void_p]
+_lib.gc_gauss_taps.restype = ctypes.c_int
+_lib.gc_kalman_step.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_int),
+                                ctypes.POINTER(ctypes.c_double)]
+_lib.gc_kalman_step.restype = ctypes.c_int
+_lib.gc_prior_update.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(gc_prior_params), ctypes.c_void_p,
+                                 ctypes.c_void_p]
+_lib.gc_prior_update.restype = ctypes.c_int
 _lib.gc_solve_batch_host.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_batch), ctypes.c_void_p]
 _lib.gc_solve_batch_host.restype = ctypes.c_int
 _lib.gc_last_error.argtypes = [ctypes.c_void_p]
@@ -106,7 +122,8 @@ _lib.gc_frame_digest.restype = ctypes.c_int
 
 EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
             "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "gc_frame_digest",
-            "gc_solve_sequences", "gc_solve_energy", "gc_gmm_prepare")
+            "gc_solve_sequences", "gc_solve_energy", "gc_gmm_prepare", "gc_gauss_taps", "gc_kalman_step",
+            "gc_prior_update")
 
 
 class GcError(RuntimeError):
@@ -159,6 +176,38 @@ def gmm_table(pairs):
         arr[2 * i] = gc_gmm_prepare(*bg)
         arr[2 * i + 1] = gc_gmm_prepare(*ob)
     return np.frombuffer(bytes(arr), np.uint8).copy()
+
+
+def gc_gauss_taps(sigma: float, radius: int):
+    taps = (ctypes.c_int * (PRIOR_RMAX + 1))()
+    st = _lib.gc_gauss_taps(float(sigma), int(radius), taps)
+    if st != 0:
+        raise GcError(st, "gc_gauss_taps: bad arguments")
+    return [taps[i] for i in range(radius + 1)]
+
+
+def gc_kalman_step(s1: float, s2: float, v_prev: float):
+    """(wf in 1/4096, v_next) of one step of the Sec. 6 recursion as printed."""
+    wf = ctypes.c_int()
+    v = ctypes.c_double()
+    st = _lib.gc_kalman_step(float(s1), float(s2), float(v_prev), ctypes.byref(wf), ctypes.byref(v))
+    if st != 0:
+        raise GcError(st, "gc_kalman_step: bad arguments")
+    return wf.value, v.value
+
+
+def prior_params(sigma: float, radius: int, band: int) -> gc_prior_params:
+    p = gc_prior_params()
+    p.radius = radius
+    p.band = band
+    for i, v in enumerate(gc_gauss_taps(sigma, radius)):
+        p.taps[i] = v
+    return p
+
+
+def gc_prior_update(ctx, n, H, W, mask_prev, q, wf, params, prior_out, stream) -> int:
+    return _lib.gc_prior_update(ctx, n, H, W, ctypes.c_void_p(mask_prev), ctypes.c_void_p(q), ctypes.c_void_p(wf),
+                                ctypes.byref(params), ctypes.c_void_p(prior_out), ctypes.c_void_p(stream))
 
 
 def gc_solve_batch_host(ctx, batch: gc_batch, stream: int) -> int:
@@ -346,6 +395,19 @@ class GridCut:
         if caps:
             res.append(cp)
         return tuple(res)
+
+    def prior_update(self, mask_prev, q, wf, params, out=None, stream=None):
+        """gc_prior_update: mask_prev [n,H,W] uint8, q [n,H,W] uint16, wf [n] int32 (CUDA tensors),
+        params a gc_prior_params (prior_params) -> prior [n,H,W] uint16 on the device."""
+        import torch
+        n, H, W = mask_prev.shape
+        assert mask_prev.dtype == torch.uint8 and q.dtype == torch.uint16 and wf.dtype == torch.int32
+        for t in (mask_prev, q, wf):
+            assert t.is_cuda and t.is_contiguous()
+        pr = torch.empty((n, H, W), dtype=torch.uint16, device=mask_prev.device) if out is None else out
+        s = torch.cuda.current_stream(mask_prev.device).cuda_stream if stream is None else stream
+        self._check(gc_prior_update(self.ctx, n, H, W, _ptr(mask_prev), _ptr(q), _ptr(wf), params, _ptr(pr), s))
+        return pr
 
     def solve_host(self, cap_s, cap_t, cap_nb, warm_flow=None, flow_state=False, stats=False, stream=0,
                    allow=(), out=None):

@@ -512,6 +512,64 @@ __global__ void k_energy_lut(double lambda, double sigma, double kappa, double s
   lut[j * 256 + dI] = v <= 0.0 ? 0 : (v >= (double)CAPMAX ? CAPMAX : (int)v);
 }
 
+// NEXT-2: prior update (include/gc.h gc_prior_update).  One CTA per 64 x 64 output block of a
+// frame: the mask block and its radius halo (replicated border) in shared memory, the row
+// pass into shared memory as exact integers, the column pass and the integer Kalman blend in
+// registers; 16 output pixels per thread, coalesced 2-byte stores.  HBM-bound stencil.
+struct PriorP {
+  int radius, band;
+  int taps[GC_PRIOR_RMAX + 1];
+  long long G2;
+};
+constexpr int PB = 64;                       // output block side
+constexpr int PS = PB + 2 * GC_PRIOR_RMAX;   // staged side
+__global__ void __launch_bounds__(256) k_prior(int H, int W, const uint8_t* __restrict__ mask,
+                                               const uint16_t* __restrict__ q, const int32_t* __restrict__ wf,
+                                               const __grid_constant__ PriorP p, uint16_t* __restrict__ out) {
+  __shared__ uint8_t ms[PS][PS];
+  __shared__ int rs[PS][PB];
+  const int f = blockIdx.z, oy = blockIdx.y * PB, ox = blockIdx.x * PB, R = p.radius, t = threadIdx.x;
+  const size_t plane = (size_t)H * W;
+  const uint8_t* m = mask + (size_t)f * plane;
+  const int S = PB + 2 * R;
+  // staged rows: a warp per row, lanes over columns (no integer division)
+  for (int r = t >> 5; r < S; r += 8) {
+    const int yy = min(max(oy - R + r, 0), H - 1);
+    const uint8_t* row = m + (size_t)yy * W;
+    for (int cc = t & 31; cc < S; cc += 32) ms[r][cc] = row[min(max(ox - R + cc, 0), W - 1)] != 0;
+  }
+  __syncthreads();
+  for (int r = t >> 6; r < S; r += 4) {  // row pass: 64 threads per staged row, one output column each
+    const int cc = t & 63;
+    int acc = p.taps[0] * ms[r][cc + R];
+    for (int k = 1; k <= R; ++k) acc += p.taps[k] * (ms[r][cc + R - k] + ms[r][cc + R + k]);
+    rs[r][cc] = acc;
+  }
+  __syncthreads();
+  const unsigned long long w = (unsigned long long)wf[f];
+  const unsigned long long D = 4096ull * (unsigned long long)p.G2;  // < 2^43
+  const double invD = 1.0 / (double)D;
+  for (int i = t; i < PB * PB; i += 256) {  // column pass + blend
+    const int r = i >> 6, c = i & 63, y = oy + r, x = ox + c;
+    if (y >= H || x >= W) continue;
+    int s = p.taps[0] * rs[r + R][c];  // S <= G^2 < 2^31 (G <= 33 x 1024)
+    for (int k = 1; k <= R; ++k) s += p.taps[k] * (rs[r + R - k][c] + rs[r + R + k][c]);
+    const size_t o = (size_t)f * plane + (size_t)y * W + x;
+    uint16_t code = 0;
+    if (y >= p.band && x >= p.band && y < H - p.band && x < W - p.band) {
+      const unsigned long long num = w * (unsigned long long)s * 65535ull +
+                                     (4096ull - w) * q[o] * (unsigned long long)p.G2 + 2048ull * (unsigned long long)p.G2;
+      // exact floor(num / D) without a 64-bit divide: a double estimate (off by at most one:
+      // the quotient is <= 65535) corrected with exact 64-bit products
+      unsigned long long qt = (unsigned long long)((double)num * invD);
+      if (qt * D > num) --qt;
+      else if ((qt + 1) * D <= num) ++qt;
+      code = (uint16_t)qt;
+    }
+    out[o] = code;
+  }
+}
+
 // a6: per-frame digest of solved frames (gc_frame_digest): F, popcount and a 64-bit hash of
 // the mask, H(m) = sum over set pixels p of splitmix64(p + 1) mod 2^64 (order-independent, so
 // blocks reduce in any order).  grid (blocks per frame, n); out zeroed before the launch.
@@ -756,6 +814,56 @@ gc_status gc_gmm_prepare(int M, const double* w, const double* mean, const doubl
     for (int j = 0; j < 3; ++j) out->mean[m][j] = mean[3 * m + j];
     out->lognorm[m] = log(w[m]) - 0.5 * (3.0 * log(2.0 * M_PI) + log(det));
   }
+  return GC_OK;
+}
+
+gc_status gc_gauss_taps(double sigma, int radius, int* taps) {
+  if (!(sigma > 0) || radius < 0 || radius > GC_PRIOR_RMAX || !taps) return GC_ERR_ARG;
+  for (int i = 0; i <= radius; ++i) taps[i] = (int)floor(1024.0 * exp(-(double)i * i / (2.0 * sigma * sigma)) + 0.5);
+  return GC_OK;
+}
+
+gc_status gc_kalman_step(double s1, double s2, double v_prev, int* wf_q12, double* v_next) {
+  if (!(s1 > 0) || !(s2 >= 0) || !(v_prev >= 0) || !wf_q12) return GC_ERR_ARG;
+  const double den = s1 + s2 + v_prev;
+  *wf_q12 = (int)floor(4096.0 * s1 / den + 0.5);
+  if (v_next) *v_next = s1 * (s2 + v_prev) / den;
+  return GC_OK;
+}
+
+gc_status gc_prior_update(gc_ctx* c, int n, int H, int W, const uint8_t* mask_prev, const uint16_t* q,
+                          const int32_t* wf, const gc_prior_params* pp, uint16_t* prior_out, void* stream) {
+  if (!c) return GC_ERR_ARG;
+  if (n < 0 || H <= 0 || W <= 0 || !pp || (n > 0 && (!mask_prev || !q || !wf || !prior_out))) {
+    c->err = "gc_prior_update: bad arguments";
+    return GC_ERR_ARG;
+  }
+  PriorP p;
+  p.radius = pp->radius;
+  p.band = pp->band;
+  long long G = 0;
+  if (p.radius < 0 || p.radius > GC_PRIOR_RMAX || p.band < 0 || pp->taps[0] <= 0) {
+    c->err = "gc_prior_update: bad params";
+    return GC_ERR_ARG;
+  }
+  for (int i = 0; i <= GC_PRIOR_RMAX; ++i) {
+    p.taps[i] = i <= p.radius ? pp->taps[i] : 0;
+    if (p.taps[i] < 0 || p.taps[i] > 1024) { c->err = "gc_prior_update: bad taps"; return GC_ERR_ARG; }
+    G += (i == 0 ? 1 : 2) * (long long)p.taps[i];
+  }
+  p.G2 = G * G;
+  if (n == 0) return GC_OK;
+  cudaSetDevice(c->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t plane = (size_t)H * W;
+  for (int f0 = 0; f0 < n; f0 += 65535) {  // gridDim.z <= 65535 frames per launch
+    const int m = n - f0 < 65535 ? n - f0 : 65535;
+    k_prior<<<dim3((W + PB - 1) / PB, (H + PB - 1) / PB, m), 256, 0, st>>>(H, W, mask_prev + f0 * plane, q + f0 * plane,
+                                                                            wf + f0, p, prior_out + f0 * plane);
+    if (!ck(c, cudaGetLastError(), "k_prior launch")) return GC_ERR_CUDA;
+  }
+  if (!ck(c, cudaStreamSynchronize(st), "k_prior")) return GC_ERR_CUDA;
+  c->last_launches = 1;
   return GC_OK;
 }
 
