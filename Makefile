@@ -14,8 +14,10 @@ PKG := paper_1008_0502_b200
 
 all: $(PKG)/libgc.so synth/libsynth.so oracle/liboracle.so
 
-$(PKG)/libgc.so: $(PKG)/csrc/gc_solver.cu $(wildcard $(PKG)/csrc/*.cuh) include/gc.h Makefile
-	$(NVCC) $(NVFLAGS) -Xptxas -v -Xptxas -dlcm=cg -shared -cudart static -o $@ $(PKG)/csrc/gc_solver.cu 2> build_gc_ptxas.log || (cat build_gc_ptxas.log; false)
+$(PKG)/libgc.so: $(PKG)/csrc/gc_solver.cu $(PKG)/csrc/gc_saliency.cu $(wildcard $(PKG)/csrc/*.cuh) include/gc.h Makefile
+	$(NVCC) $(NVFLAGS) -Xptxas -v -Xptxas -dlcm=cg -c -o $(PKG)/csrc/gc_solver.o $(PKG)/csrc/gc_solver.cu 2> build_gc_ptxas.log || (cat build_gc_ptxas.log; false)
+	$(NVCC) $(NVFLAGS) -fmad=false -c -o $(PKG)/csrc/gc_saliency.o $(PKG)/csrc/gc_saliency.cu
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(PKG)/csrc/gc_solver.o $(PKG)/csrc/gc_saliency.o
 
 synth/libsynth.so: synth/synth_host.c synth/synth_cuda.cu synth/synth.h
 	gcc -O2 -fPIC -c synth/synth_host.c -o synth/synth_host.o
@@ -26,6 +28,6 @@ oracle/liboracle.so: oracle/oracle.cpp
 	g++ -O2 -std=c++17 -fPIC -shared -pthread -o $@ oracle/oracle.cpp
 
 clean:
-	rm -f $(PKG)/libgc.so synth/libsynth.so synth/*.o oracle/liboracle.so build_gc_ptxas.log
+	rm -f $(PKG)/libgc.so $(PKG)/csrc/*.o synth/libsynth.so synth/*.o oracle/liboracle.so build_gc_ptxas.log
 
 .PHONY: all clean

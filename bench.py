@@ -484,6 +484,78 @@ def run_prior(args, cfg):
         dist.destroy_process_group()
 
 
+def run_saliency(args, cfg):
+    """NEXT-4: gc_saliency (Itti-style map) over C4-geometry frames
+    with motion (previous frame), 64 frames per call (the pyramids take ~88 MB per 1080p frame);
+    output: the level-4 map and the full-resolution prior code."""
+    import torch
+
+    import paper_1008_0502_b200 as gc
+    import synth
+    from paper_1008_0502_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    H, W = cfg["H"], cfg["W"]
+    n = 64
+    seed = synth.BASE_SEED + cfg["seed_off"]
+    t_first, _ = shard.frame_range(rank, world, n)
+    img, _ = synth.gen_energy_torch(seed, t_first, n + 1, H, W, device=dev)
+    cur, prev = img[1:].contiguous(), img[:-1].contiguous()
+    g = gc.GridCut(neighborhood=4, max_h=H, max_w=W)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        g.saliency(cur, prev)
+    torch.cuda.synchronize()
+    clk = ClockSampler(None)
+    clk.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        g.saliency(cur, prev)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = shard.max_over_ranks(e0.elapsed_time(e1), dev, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import saliency as osal
+        rgb = img[:2].cpu().numpy()
+        t0 = time.perf_counter()
+        osal.saliency(rgb[1], rgb[0])
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(H * W / dt / 1e6, 3), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
+               "sample": f"1 frame, oracle/saliency.py (numpy float32, one core), {cpu_model()}", "seconds": round(dt, 2)}
+    if rank == 0:
+        peak, peak_src = load_peak()
+        bpx = 3 + 3 + 2  # read the frame and the previous frame, write the prior code
+        ach = bpx * n * H * W * args.steps / (ms * 1e-3) / 1e9
+        res = {"metric": METRIC, "value": round(world * n * H * W * args.steps / (ms * 1e-3) / 1e6, 1),
+               "unit": "Mpixel/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic (blob frames as RGB, synth/; on device)",
+               "config": {"workload": f"NEXT-4 saliency (P:516-570) on {cfg['workload'].split(',')[0]} frames, "
+                                      f"{n} per call, with motion", "H": H, "W": W, "frames_per_rank": n,
+                          "parallelism": f"frame-sharded dp{world}"},
+               "roofline": {"bound": "hbm", "kernel": "gc_saliency (18 kernels per map set)", "unit": "GB/s",
+                            "peak": peak, "achieved": round(ach, 1), "frac": round(ach / peak, 4),
+                            "bytes_rule": f"{bpx} B/px compulsory (two RGB frames in, the prior code out); "
+                                          "the pyramids and feature maps stay in HBM / L2", "traffic": None,
+                            "peak_source": peak_src},
+               "cpu_baseline": cpu, "gpu_launches": None, "clocks": clocks}
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 def ctypes_sizeof_gmm(gc):
     import ctypes
     return ctypes.sizeof(gc.gc_gmm)
@@ -534,6 +606,7 @@ def main():
     ap.add_argument("--energy", action="store_true",
                     help="NEXT-1: frames given as RGB image + prior + colour GMMs; caps built in the solve's init pass")
     ap.add_argument("--prior", action="store_true", help="NEXT-2: the on-device prior update (gc_prior_update)")
+    ap.add_argument("--saliency", action="store_true", help="NEXT-4: the saliency front-end (gc_saliency)")
     ap.add_argument("--warm", action="store_true",
                     help="sequence mode (C3): S sequences x L frames, frame t warm-started from t-1")
     ap.add_argument("--seqs", type=int, default=8)
@@ -554,6 +627,8 @@ def main():
         return run_energy(args, cfg)
     if args.prior:
         return run_prior(args, cfg)
+    if args.saliency:
+        return run_saliency(args, cfg)
 
     import numpy as np
     import torch

@@ -229,6 +229,37 @@ gc_status gc_kalman_step(double s1, double s2, double v_prev, int* wf_q12, doubl
 gc_status gc_prior_update(gc_ctx* ctx, int n, int H, int W, const uint8_t* mask_prev, const uint16_t* q,
                           const int32_t* wf, const gc_prior_params* params, uint16_t* prior_out, void* stream);
 
+/* ---- NEXT-4: the Itti-style saliency map of PAPER.md §3 / §7.2 on the
+ * device: level-0 features I = (r+g+b)/3, RG = (r-g)/I, BY = (b-(r+g)/2)/I (0 where
+ * I < 0.1), M = |I - I_prev| (r, g, b = byte / 255); Gaussian pyramids (levels 0..8, [1 4 6 4 1]/16
+ * separable blur with clamped border, decimation by 2 rounding up); orientation maps |G_theta * I|
+ * with the four 9 x 9 filters of gc_gabor_kernels on I's levels 2..8; centre-surround maps
+ * |L_c - up(L_s)| for c in {2,3,4}, s = c + {3,4} (bilinear, pixel centres); the normalisation
+ * N(.) = rescale to [0,1], times (1 - m)^2 with m the mean of the local maxima (window radius 7)
+ * other than the global one ("global and local [extrema]", DESIGN.md c21); each map
+ * brought to level 4 by blur-decimation and summed per class (intensity, colour, orientation --
+ * N of each orientation's sum first --, motion); saliency = N(mean of the four N(class)).
+ * Float32 with the operation order fixed and no fused multiply-add, exact reductions: the result
+ * is a deterministic function of the input (the oracle reproduces it bit for bit).
+ * image / prev: [n][H][W][3] RGB (prev NULL: no motion); sal_out: NULL or [n][h4][w4] float at
+ * level 4 (gc_saliency_dims); q_out: NULL or [n][H][W] uint16 = floor(65535 s + 0.5) of the
+ * bilinearly upsampled saliency (a prior code for gc_prior_update).  Device pointers;
+ * GC_ERR_ARG for bad dims / NULL pointers, GC_ERR_OOM if the pyramids (~88 MB per 1080p frame)
+ * do not fit. */
+typedef struct {
+  int n, H, W;
+  const uint8_t* image;
+  const uint8_t* prev;
+  float* sal_out;
+  uint16_t* q_out;
+} gc_saliency_batch;
+gc_status gc_saliency(gc_ctx* ctx, const gc_saliency_batch* batch, void* stream);
+/* Level-4 size: h4 = H rounded up 4 times by halving, likewise w4.  Host only. */
+gc_status gc_saliency_dims(int H, int W, int* h4, int* w4);
+/* The four orientation filters [4][9][9] float (theta = 0, 45, 90, 135 degrees): even Gabor,
+ * sigma 2, wavelength 6, aspect 0.5, mean removed (DESIGN.md c19).  Host only. */
+gc_status gc_gabor_kernels(float* out);
+
 /* Message for the last failing call on this context ("" if none).  Never NULL. */
 const char* gc_last_error(const gc_ctx* ctx);
 

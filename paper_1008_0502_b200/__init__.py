@@ -17,6 +17,7 @@ import numpy as np
 
 __all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_solve_sequences",
            "gc_solve_energy", "gc_gmm_prepare", "gc_gauss_taps", "gc_kalman_step", "gc_prior_update",
+           "gc_saliency", "gc_saliency_dims", "gc_gabor_kernels",
            "gc_frame_digest", "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "CAP_MAX",
            "STATUS", "lib_path"]
 
@@ -80,6 +81,11 @@ class gc_prior_params(ctypes.Structure):
     _fields_ = [("radius", ctypes.c_int), ("taps", ctypes.c_int * (PRIOR_RMAX + 1)), ("band", ctypes.c_int)]
 
 
+class gc_saliency_batch(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("image", ctypes.c_void_p),
+                ("prev", ctypes.c_void_p), ("sal_out", ctypes.c_void_p), ("q_out", ctypes.c_void_p)]
+
+
 _lib.gc_create.argtypes = [ctypes.POINTER(gc_config), ctypes.POINTER(ctypes.c_void_p)]
 _lib.gc_create.restype = ctypes.c_int
 _lib.gc_destroy.argtypes = [ctypes.c_void_p]
@@ -101,6 +107,12 @@ _lib.gc_prior_update.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ct
                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(gc_prior_params), ctypes.c_void_p,
                                  ctypes.c_void_p]
 _lib.gc_prior_update.restype = ctypes.c_int
+_lib.gc_saliency.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_saliency_batch), ctypes.c_void_p]
+_lib.gc_saliency.restype = ctypes.c_int
+_lib.gc_saliency_dims.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+_lib.gc_saliency_dims.restype = ctypes.c_int
+_lib.gc_gabor_kernels.argtypes = [ctypes.c_void_p]
+_lib.gc_gabor_kernels.restype = ctypes.c_int
 _lib.gc_solve_batch_host.argtypes = [ctypes.c_void_p, ctypes.POINTER(gc_batch), ctypes.c_void_p]
 _lib.gc_solve_batch_host.restype = ctypes.c_int
 _lib.gc_last_error.argtypes = [ctypes.c_void_p]
@@ -123,7 +135,7 @@ _lib.gc_frame_digest.restype = ctypes.c_int
 EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
             "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "gc_frame_digest",
             "gc_solve_sequences", "gc_solve_energy", "gc_gmm_prepare", "gc_gauss_taps", "gc_kalman_step",
-            "gc_prior_update")
+            "gc_prior_update", "gc_saliency", "gc_saliency_dims", "gc_gabor_kernels")
 
 
 class GcError(RuntimeError):
@@ -208,6 +220,24 @@ def prior_params(sigma: float, radius: int, band: int) -> gc_prior_params:
 def gc_prior_update(ctx, n, H, W, mask_prev, q, wf, params, prior_out, stream) -> int:
     return _lib.gc_prior_update(ctx, n, H, W, ctypes.c_void_p(mask_prev), ctypes.c_void_p(q), ctypes.c_void_p(wf),
                                 ctypes.byref(params), ctypes.c_void_p(prior_out), ctypes.c_void_p(stream))
+
+
+def gc_saliency(ctx, batch: gc_saliency_batch, stream: int) -> int:
+    return _lib.gc_saliency(ctx, ctypes.byref(batch), ctypes.c_void_p(stream))
+
+
+def gc_saliency_dims(H: int, W: int):
+    h4, w4 = ctypes.c_int(), ctypes.c_int()
+    st = _lib.gc_saliency_dims(H, W, ctypes.byref(h4), ctypes.byref(w4))
+    if st != 0:
+        raise GcError(st, "gc_saliency_dims: bad dims")
+    return h4.value, w4.value
+
+
+def gc_gabor_kernels():
+    out = np.zeros((4, 9, 9), np.float32)
+    _lib.gc_gabor_kernels(out.ctypes.data)
+    return out
 
 
 def gc_solve_batch_host(ctx, batch: gc_batch, stream: int) -> int:
@@ -408,6 +438,24 @@ class GridCut:
         s = torch.cuda.current_stream(mask_prev.device).cuda_stream if stream is None else stream
         self._check(gc_prior_update(self.ctx, n, H, W, _ptr(mask_prev), _ptr(q), _ptr(wf), params, _ptr(pr), s))
         return pr
+
+    def saliency(self, image, prev=None, q=True, stream=None):
+        """gc_saliency: image (and prev) [n,H,W,3] uint8 CUDA tensors -> saliency [n,h4,w4]
+        float32 (and the full-resolution prior code [n,H,W] uint16 if q)."""
+        import torch
+        n, H, W, _ = image.shape
+        assert image.dtype == torch.uint8 and image.is_cuda and image.is_contiguous()
+        if prev is not None:
+            assert prev.shape == image.shape and prev.dtype == torch.uint8 and prev.is_contiguous()
+        h4, w4 = gc_saliency_dims(H, W)
+        sal = torch.empty((n, h4, w4), dtype=torch.float32, device=image.device)
+        qo = torch.empty((n, H, W), dtype=torch.uint16, device=image.device) if q else None
+        b = gc_saliency_batch(n, H, W, _ptr(image), _ptr(prev), _ptr(sal), _ptr(qo))
+        s = torch.cuda.current_stream(image.device).cuda_stream if stream is None else stream
+        st = gc_saliency(self.ctx, b, s)
+        if st != 0:
+            raise GcError(st, "gc_saliency failed")
+        return (sal, qo) if q else sal
 
     def solve_host(self, cap_s, cap_t, cap_nb, warm_flow=None, flow_state=False, stats=False, stream=0,
                    allow=(), out=None):

@@ -47,6 +47,9 @@ def test_struct_layout_matches_header():
     assert [n for n, _ in gc.gc_energy_batch._fields_] == names
     import ctypes
     assert ctypes.sizeof(gc.gc_gmm) == 8 + 8 * 4 + 24 * 4 + 48 * 4
+    body = re.search(r"typedef struct \{([^{}]*)\} gc_saliency_batch;", src, re.S).group(1)
+    names = re.findall(r"\*?\s*([a-z_A-Z0-9]+)\s*[,;]", body)
+    assert [n for n, _ in gc.gc_saliency_batch._fields_] == names
     body = re.search(r"typedef struct \{([^{}]*)\} gc_prior_params;", src, re.S).group(1)
     names = re.findall(r"int\s+([a-z_A-Z]+)", body)
     assert [n for n, _ in gc.gc_prior_params._fields_] == names
