@@ -501,26 +501,43 @@ __device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t g
 // tile's share of sum max(0,-e) up to date.  An untouched uniform source tile (every pixel
 // e > 0: closure = the whole tile, mask already written) only marks its border arcs.  A
 // frame with out-of-range caps gets an all-0 mask here (gc.h).
-template <int K>
-__device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
-                                           long long* red, int* bc) {
-  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
-  const int s = (int)((unsigned)gt / (unsigned)d.T);
-  if (t == 0) {
-    // every word at once (independent loads, one round trip)
+// The words the closure seeds of a group of tiles decide on, loaded for the whole group at once
+// (thread j: tile gt0 + j; one round trip instead of one per tile): gw[j] = {mode, mat | recv1,
+// every mask byte rewritten, epoch, recv1}.  mode 2: range error (mask all 0, F = -1); 1: skip --
+// the attempt already failed, or (a tile of the group outside the task set) an untouched uniform
+// sink tile without extra mask bytes; 3: untouched uniform source tile (border marks only);
+// 0: full closure seed.  Block-wide; ends with a barrier.
+__device__ __forceinline__ void cseed_group_words(const Dev& d, size_t gt0, int gcnt, int (*gw)[5]) {
+  const int t = threadIdx.x;
+  if (t < gcnt) {
+    const size_t gt = gt0 + t;
+    const int s = (int)((unsigned)gt / (unsigned)d.T);
+    // every word at once (independent loads)
     const int r1 = __ldcg(d.recv1 + gt), fe = __ldcg(d.ferr + s), cf = __ldcg(d.cfail + s);
     const int tu = __ldcg(d.tuni + gt), mt = __ldcg(d.mat + gt), tm = __ldcg(d.tmk + gt);
     const int tsr = __ldcg(d.tsrc + gt);
     const int cp = __ldcg(d.sep + s);
-    bc[0] = r1;
-    // 2: range error (mask all 0, F = -1); 1: skip -- the attempt already failed, or (a tile of
-    // the group outside the task set) an untouched uniform sink tile without extra mask bytes;
-    // 3: untouched uniform source tile (border marks only); 0: full closure seed
-    bc[2] = fe ? 2 : ((cf > 0) | ((tu != 0) & (mt == 0) & (r1 == 0) & (tm == 0))) ? 1
-                                                                                  : ((tsr != 0) & (mt == 0) & (r1 == 0)) ? 3 : 0;
-    bc[3] = mt | r1;        // e, r materialised: rewrite every mask byte, recompute the deficit
-    bc[5] = (mt | r1) | tm; // every mask byte of the tile is (re)written
-    bc[4] = cp % 255 + 1;   // closure epoch (closure_epoch)
+    gw[t][0] = fe ? 2 : ((cf > 0) | ((tu != 0) & (mt == 0) & (r1 == 0) & (tm == 0))) ? 1
+                                                                                     : ((tsr != 0) & (mt == 0) & (r1 == 0)) ? 3 : 0;
+    gw[t][1] = mt | r1;       // e, r materialised: rewrite every mask byte, recompute the deficit
+    gw[t][2] = (mt | r1) | tm;  // every mask byte of the tile is (re)written
+    gw[t][3] = cp % 255 + 1;  // closure epoch (closure_epoch)
+    gw[t][4] = r1;
+  }
+  __syncthreads();
+}
+
+template <int K>
+__device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt, uint8_t* ms, uint8_t* os,
+                                           long long* red, int* bc, const int* gw) {
+  const int t = threadIdx.x, ix = t & 31, iy0 = t >> 5;
+  const int s = (int)((unsigned)gt / (unsigned)d.T);
+  if (t == 0) {
+    bc[0] = gw[4];
+    bc[2] = gw[0];
+    bc[3] = gw[1];
+    bc[5] = gw[2];
+    bc[4] = gw[3];
   }
   __syncthreads();
   const int mode = bc[2];
@@ -1432,13 +1449,20 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
         cls = 1;
         break;
       case M_PUSH: task_push<K>(d, io, gt, c, smem, bc, red); cls = 2; break;
-      case M_CSEED:
+      case M_CSEED: {
+        __shared__ int gw[16][5];
+        cseed_group_words(d, gt, gcnt, gw);
+        bool first = true;
         for (int j = 0; j < gcnt; ++j) {
-          if (j) __syncthreads();
-          task_cseed<K>(d, io, gt + j, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, red, bc);
+          if (gw[j][0] == 1) continue;  // skipped tile: no barrier, no round trip
+          if (!first) __syncthreads();
+          first = false;
+          task_cseed<K>(d, io, gt + j, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, red, bc,
+                        gw[j]);
         }
         cls = 4;
         break;
+      }
       case M_CLOS:
         task_crelax<K>(d, io, gt, reinterpret_cast<uint8_t*>(smem), reinterpret_cast<uint8_t*>(smem) + TPX, bc);
         cls = 4;
