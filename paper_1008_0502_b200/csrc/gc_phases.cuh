@@ -1234,92 +1234,139 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       }
       __syncthreads();
     }
-    for (int b0 = 0; kind != SET_EMPTY && b0 < d.T; b0 += NTH) {
-      const int i = b0 + t;
-      int want = 0;
-      if (i < d.T) {
+    // batches of TB x NTH tiles: every tile word of the batch loaded at once (one round trip),
+    // the decisions, a block-wide scan of the entries, ONE reservation of queue slots and task
+    // counts for the whole batch, the entries written -- a few round trips per batch instead of
+    // three per 256 tiles
+    constexpr int TB = 8;
+    __shared__ int wsum[NTH / 32];
+    for (int bb = 0; kind != SET_EMPTY && bb < d.T; bb += TB * NTH) {
+      int w0[TB], w1[TB], w2[TB], w3[TB];
+#pragma unroll
+      for (int c2 = 0; c2 < TB; ++c2) {  // loads only (independent)
+        const int i = bb + c2 * NTH + t;
+        w0[c2] = w1[c2] = w2[c2] = w3[c2] = 0;
+        if (i >= d.T) continue;
         const size_t gt = base_gt + i;
-        if (kind == SET_ALL) {
-          want = 1;
-          d.flag[gt] = 0;
-        }
-        else if (kind == SET_INITG) want = (i % d.initg) == 0;  // one init task per tile group
-        else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1, uniform source
-          const int tu = __ldcg(d.tuni + gt), tsr = __ldcg(d.tsrc + gt), r1 = __ldcg(d.recv1 + gt);
-          want = !((tu | tsr) && !r1);  // tiles have no sink pixel: h = HINF until relaxed
-          if (!want && tu) d.tsk[gt] = bc[3];
-          if (!want && !tu) {
-            d.tss[gt] = bc[3];
-            d.tact[gt] = 0;
-          }
-          d.flag[gt] = 0;
-        } else if (kind == SET_CSEED) {  // untouched uniform sink tiles are never in the closure
-          const int tu = __ldcg(d.tuni + gt), mt = __ldcg(d.mat + gt), r1 = __ldcg(d.recv1 + gt);
-          const int tm = __ldcg(d.tmk + gt);
-          want = !(tu && !mt && !r1) || tm != 0;  // mask bytes of a failed attempt are rewritten
-          if (want && srcskip && !mt && !r1 && !tm && ((sbits[i >> 5] >> (i & 31)) & 1)) {
-            const int ty = i / d.TX, tx = i - ty * d.TX;
-            bool inner = true;
-            for (int dy = -1; dy <= 1; ++dy)
-              for (int dx = -1; dx <= 1; ++dx) {
-                const int ny = ty + dy, nx = tx + dx;
-                if ((dy == 0 && dx == 0) || ny < 0 || ny >= d.TY || nx < 0 || nx >= d.TX) continue;
-                if (dy != 0 && dx != 0 && c.K4) continue;  // no diagonal arcs
-                const int n = ny * d.TX + nx;
-                inner &= ((sbits[n >> 5] >> (n & 31)) & 1) != 0;
-              }
-            if (inner) want = 0;
-          }
-          d.flag[gt] = 0;
+        if (kind == SET_SEED) {
+          w0[c2] = __ldcg(d.tuni + gt); w1[c2] = __ldcg(d.tsrc + gt); w2[c2] = __ldcg(d.recv1 + gt);
+        } else if (kind == SET_CSEED) {
+          w0[c2] = __ldcg(d.tuni + gt); w1[c2] = __ldcg(d.mat + gt); w2[c2] = __ldcg(d.recv1 + gt);
+          w3[c2] = __ldcg(d.tmk + gt);
         } else if (kind == SET_FLAG) {
-          want = __ldcg(d.flag + gt);
-          if (want) d.flag[gt] = 0;
-          if (unibits && !((sbits[i >> 5] >> (i & 31)) & 1)) {
-            const int ty = i / d.TX, tx = i - ty * d.TX;
-            for (int dy = -1; dy <= 1; ++dy)
-              for (int dx = -1; dx <= 1; ++dx) {
-                const int ny = ty + dy, nx = tx + dx;
-                if ((dy == 0 && dx == 0) || ny < 0 || ny >= d.TY || nx < 0 || nx >= d.TX) continue;
-                if (dy != 0 && dx != 0 && c.K4) continue;  // no diagonal arcs
-                const int n = ny * d.TX + nx;
-                want |= (sbits[n >> 5] >> (n & 31)) & 1;
-              }
-          }
-          if ((md == M_SEED || md == M_INIT) && __ldcg(d.tfix + gt)) want = 0;  // a relax cannot change it
+          w0[c2] = __ldcg(d.flag + gt); w1[c2] = (md == M_SEED || md == M_INIT) ? __ldcg(d.tfix + gt) : 0;
+        } else if (kind == SET_TACT) {
+          w0[c2] = __ldcg(d.tact + gt); w1[c2] = __ldcg(d.tminh + gt);
         }
-        else want = __ldcg(d.tact + gt) && __ldcg(d.tminh + gt) <= hcap;
-        if (want && (kind == SET_FLAG || kind == SET_TACT)) d.treq[gt] = 1;
       }
-      // seed / closure-seed tasks take groups of d.bulkg consecutive tiles (the task skips
-      // the tiles of its group that are not in the set): the group leader enqueues
-      const bool grouped = (kind == SET_SEED || kind == SET_CSEED) && d.bulkg > 1;
-      int gcnt = 1;
-      if (grouped) {
-        const int bg = d.bulkg;
-        const unsigned bal = __ballot_sync(0xffffffffu, want);
-        const int lane = t & 31, lead = lane & ~(bg - 1);
-        want = (lane == lead) && ((bal >> lead) & ((1u << bg) - 1));
-        gcnt = min(bg, d.T - i);
+      unsigned wbits = 0;   // bit c2: this thread enqueues an entry for chunk c2
+#pragma unroll
+      for (int c2 = 0; c2 < TB; ++c2) {  // decisions and their side effects
+        const int i = bb + c2 * NTH + t;
+        int want = 0;
+        if (i < d.T) {
+          const size_t gt = base_gt + i;
+          if (kind == SET_ALL) {
+            want = 1;
+            d.flag[gt] = 0;
+          } else if (kind == SET_INITG) {
+            want = (i % d.initg) == 0;  // one init task per tile group
+          } else if (kind == SET_SEED) {  // untouched uniform sink tiles keep h = 1, uniform source
+            const int tu = w0[c2], tsr = w1[c2], r1 = w2[c2];
+            want = !((tu | tsr) && !r1);  // tiles have no sink pixel: h = HINF until relaxed
+            if (!want && tu) d.tsk[gt] = bc[3];
+            if (!want && !tu) {
+              d.tss[gt] = bc[3];
+              d.tact[gt] = 0;
+            }
+            d.flag[gt] = 0;
+          } else if (kind == SET_CSEED) {  // untouched uniform sink tiles are never in the closure
+            const int tu = w0[c2], mt = w1[c2], r1 = w2[c2], tm = w3[c2];
+            want = !(tu && !mt && !r1) || tm != 0;  // mask bytes of a failed attempt are rewritten
+            if (want && srcskip && !mt && !r1 && !tm && ((sbits[i >> 5] >> (i & 31)) & 1)) {
+              const int ty = i / d.TX, tx = i - ty * d.TX;
+              bool inner = true;
+              for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                  const int ny = ty + dy, nx = tx + dx;
+                  if ((dy == 0 && dx == 0) || ny < 0 || ny >= d.TY || nx < 0 || nx >= d.TX) continue;
+                  if (dy != 0 && dx != 0 && c.K4) continue;  // no diagonal arcs
+                  const int n = ny * d.TX + nx;
+                  inner &= ((sbits[n >> 5] >> (n & 31)) & 1) != 0;
+                }
+              if (inner) want = 0;
+            }
+            d.flag[gt] = 0;
+          } else if (kind == SET_FLAG) {
+            want = w0[c2];
+            if (want) d.flag[gt] = 0;
+            if (unibits && !((sbits[i >> 5] >> (i & 31)) & 1)) {
+              const int ty = i / d.TX, tx = i - ty * d.TX;
+              for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                  const int ny = ty + dy, nx = tx + dx;
+                  if ((dy == 0 && dx == 0) || ny < 0 || ny >= d.TY || nx < 0 || nx >= d.TX) continue;
+                  if (dy != 0 && dx != 0 && c.K4) continue;  // no diagonal arcs
+                  const int n = ny * d.TX + nx;
+                  want |= (sbits[n >> 5] >> (n & 31)) & 1;
+                }
+            }
+            if (w1[c2]) want = 0;  // (seed / init relax sets) a relax cannot change it
+          } else {
+            want = w0[c2] && w1[c2] <= hcap;
+          }
+          if (want && (kind == SET_FLAG || kind == SET_TACT)) d.treq[gt] = 1;
+        }
+        // seed / closure-seed tasks take groups of d.bulkg consecutive tiles (the task skips
+        // the tiles of its group that are not in the set): the group leader enqueues
+        if ((kind == SET_SEED || kind == SET_CSEED) && d.bulkg > 1) {
+          const int bg = d.bulkg;
+          const unsigned bal = __ballot_sync(0xffffffffu, want);
+          const int lane = t & 31, lead = lane & ~(bg - 1);
+          want = (lane == lead) && ((bal >> lead) & ((1u << bg) - 1));
+        }
+        wbits |= (unsigned)(want != 0) << c2;
       }
-      if (t == 0) bc[5] = 0;
+      // block-wide exclusive scan of the entry counts
+      const int mine = __popc(wbits);
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((t & 31) >= o) incl += v;
+      }
+      if ((t & 31) == 31) wsum[t >> 5] = incl;
+      fence_gpu();  // this thread's tile-word writes are visible before the entries
       __syncthreads();
-      int li = want ? atomicAdd(&bc[5], 1) : 0;
-      fence_gpu();
-      __syncthreads();
-      const int cnt = bc[5];
-      if (cnt == 0) continue;
+      int wbase = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < NTH / 32; ++w) {
+        const int v = wsum[w];
+        if (w < (t >> 5)) wbase += v;
+        total += v;
+      }
+      if (total == 0) {
+        __syncthreads();
+        continue;
+      }
       if (t == 0) {
-        atomicAdd(&d.fout[s], cnt);
-        const unsigned long long p0 = atomicAdd(kind == SET_INITG ? d.qitail : d.qtail, (unsigned long long)cnt);
+        atomicAdd(&d.fout[s], total);
+        const unsigned long long p0 = atomicAdd(kind == SET_INITG ? d.qitail : d.qtail, (unsigned long long)total);
         bc[6] = (int)(p0 & 0xffffffffu);
         bc[7] = (int)(p0 >> 32);
       }
       __syncthreads();
       const unsigned long long p0 = ((unsigned long long)(uint32_t)bc[7] << 32) | (uint32_t)bc[6];
-      if (want) {
+      unsigned long long pos = p0 + (unsigned long long)(wbase + incl - mine);
+#pragma unroll
+      for (int c2 = 0; c2 < TB; ++c2) {
+        if (!((wbits >> c2) & 1)) continue;
+        const int i = bb + c2 * NTH + t;
+        const int gcnt = ((kind == SET_SEED || kind == SET_CSEED) && d.bulkg > 1) ? min(d.bulkg, d.T - i) : 1;
         const uint32_t ent = qent(bc[2], base_gt + i, gcnt);
-        if (kind == SET_INITG) qi_put(d, p0 + li, ent);
-        else q_put(d, p0 + li, ent);
+        if (kind == SET_INITG) qi_put(d, pos, ent);
+        else q_put(d, pos, ent);
+        ++pos;
       }
       __syncthreads();
     }
