@@ -1038,6 +1038,7 @@ __device__ __forceinline__ void energy_caps(const Dev& d, const IO& io, const Fr
 struct Tmaps {
   CUtensorMap cs, ct, nb;
   int on;  // maps valid (cold frames, 16-byte aligned rows)
+  int pf;  // tiles ahead of the smem load whose rows are prefetched into L2 (0: none)
 };
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -1078,6 +1079,25 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+// Lane 0 of warp w: prefetch rows 4w..4w+3 of tile (ty, tx) into L2 (no barrier, no smem).
+__device__ __forceinline__ void tma_prefetch_rows(const Tmaps& tm, int fr, int ty, int tx, int w) {
+  const int x = tx * TS, y = ty * TS + 4 * w;
+  tma_prefetch_3d(&tm.cs, x, y, fr);
+  tma_prefetch_3d(&tm.ct, x, y, fr);
+  tma_prefetch_4d(&tm.nb, x, y, 0, fr);
+}
+
 // Lane 0 of warp w: arm the warp's barrier and load rows 4w..4w+3 of tile (ty, tx) of frame fr.
 template <int K>
 __device__ __forceinline__ void tma_issue_rows(const Tmaps& tm, char* stage, uint64_t* bar, int fr, int ty, int tx,
@@ -1105,7 +1125,10 @@ __device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0
     char* stage = reinterpret_cast<char*>(((uintptr_t)(uni_s + INIT_GMAX) + 127) & ~(uintptr_t)127) + w * (2 + K) * 512;
     uint64_t* bar = mbar + w;
     const int fr = (int)P.fr;
-    if (lane == 0) tma_issue_rows<K>(tm, stage, bar, fr, tile0 / d.TX, tile0 % d.TX, w);
+    if (lane == 0) {
+      tma_issue_rows<K>(tm, stage, bar, fr, tile0 / d.TX, tile0 % d.TX, w);
+      for (int q = 1; q <= tm.pf && q < n; ++q) tma_prefetch_rows(tm, fr, (tile0 + q) / d.TX, (tile0 + q) % d.TX, w);
+    }
 #pragma unroll 1
     for (int i = 0; i < n; ++i) {
       mbar_wait(bar, tpar);
@@ -1126,6 +1149,8 @@ __device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0
       if (i + 1 < n && lane == 0) {
         const int tile = tile0 + i + 1;
         tma_issue_rows<K>(tm, stage, bar, fr, tile / d.TX, tile % d.TX, w);
+        const int tp = tile + tm.pf;  // keep the L2 prefetch pf tiles ahead
+        if (tm.pf && tp < tile0 + n) tma_prefetch_rows(tm, fr, tp / d.TX, tp % d.TX, w);
       }
       if (P.fs) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
       else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i);

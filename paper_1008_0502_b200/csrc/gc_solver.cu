@@ -39,6 +39,7 @@ struct gc_ctx {
                                   // (doubled from 1 per failed certificate attempt)
   int selfrun = 0;                // 1: a push tile re-runs itself only after progress
   int tma = 1;                    // TMA staging of the init stream when the layout allows
+  int tmapf = 0;                  // ... with an L2 prefetch this many tiles ahead (measured: slower)
   int grid = 0;                   // k_solve CTAs of the last launch
   int grid_max = 0;               // persistent grid of k_solve<K> on this context's device
   std::string err;
@@ -408,6 +409,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   Tmaps tm;
   memset(&tm, 0, sizeof(tm));
   tm.on = ctl.vec && c->tma && !io.img && make_tmaps(c, io, nframes, H, W, K, &tm);
+  tm.pf = c->tmapf;
   k_setup<<<(unsigned)((ns + NTH - 1) / NTH < 4096 ? (ns + NTH - 1) / NTH : 4096), NTH, 0, st>>>(d, io, ctl);
   ++L.n;
   // the launch's device time, always measured (gc_get_kernel_ms): two events per launch
@@ -642,6 +644,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (const char* ev = knob("GC_WAVE")) c->wave = atoi(ev);
   if (const char* ev = knob("GC_SELFRUN")) c->selfrun = atoi(ev);
   if (const char* ev = knob("GC_TMA")) c->tma = atoi(ev);
+  if (const char* ev = knob("GC_TMAPF")) c->tmapf = atoi(ev);
   if (const char* ev = getenv("GC_TIMEOUT_S")) c->timeout_s = atof(ev);
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
   if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
