@@ -1074,9 +1074,16 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
                                         int sbits_words) {
   const int t = threadIdx.x;
   if (t == 0) atomicAdd(&d.fout[s], 1);  // guard: no other CTA can see fout == 0 while we enqueue
+  __shared__ int sw[8];  // the slot's words, loaded at once (one round trip)
   for (;;) {
     fence_gpu();
-    const int md = __ldcg(d.fmode + s);
+    if (t == 0) {
+      const int a0 = __ldcg(d.fmode + s), a1 = __ldcg(d.ferr + s), a2 = __ldcg(d.cep + s), a3 = __ldcg(d.cfail + s);
+      const int a4 = __ldcg(d.fbnd + s);
+      sw[0] = a0; sw[1] = a1; sw[2] = a2; sw[3] = a3; sw[4] = a4;
+    }
+    __syncthreads();
+    const int md = sw[0];
     int nact = 0, hlo = HINF;
     if (md == M_BFS) {
       for (int i = t; i < d.T; i += NTH) {
@@ -1094,10 +1101,9 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     // and pixels above the cap do not take part in the phase at all (frozen): in a typical
     // frame only the excess next to the object boundary has anywhere to go, and the closure
     // certificate proves the rest trapped.  The cap doubles with every failed attempt.
-    const int cepn = __ldcg(d.cep + s);
+    const int cepn = sw[2];
     const long long capw = cepn == 0 ? (long long)c.wave : (long long)max(c.wave, 1) << min(cepn * c.wavesh, 20);
-    const int hcap = md == M_BFS ? (int)min((long long)min(HINF - 1, __ldcg(d.fbnd + s)), (long long)bc[6] + capw)
-                                 : HINF - 1;
+    const int hcap = md == M_BFS ? (int)min((long long)min(HINF - 1, sw[4]), (long long)bc[6] + capw) : HINF - 1;
     if (t == 0) {
       int nm = md, kind = SET_ALL;
       int* st = d.fstat + s * 4;
@@ -1105,9 +1111,9 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       if (md == M_INIT) {
         // the init tasks seeded the first global relabel (init_seed_group): straight to its
         // relax phase; range error: the closure seeds zero the mask
-        nm = d.ferr[s] ? M_CSEED : M_BFS;
-        kind = d.ferr[s] ? SET_ALL : SET_FLAG;
-        if (!d.ferr[s]) st[1] += 1;
+        nm = sw[1] ? M_CSEED : M_BFS;
+        kind = sw[1] ? SET_ALL : SET_FLAG;
+        if (!sw[1]) st[1] += 1;
       } else if (md == M_SEED) {
         nm = M_BFS;
         kind = SET_FLAG;
@@ -1128,16 +1134,16 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           kind = SET_CSEED;
           // an exact relabel without an active node is the termination certificate: the
           // closure cannot fail (marker); after a bounded one it is an ordinary attempt
-          d.cfail[s] = d.fbnd[s] >= HINF ? -1 : 0;
+          d.cfail[s] = sw[4] >= HINF ? -1 : 0;
         }
       } else if (md == M_PUSH) {
         // try to certify at once: the closure of the excess nodes; if it reaches a node with
         // e < 0 the frame returns to a global relabel (epochs are unique within a frame for
         // 250 attempts; beyond that only the BFS certificate leads to the closure)
-        if (d.cep[s] < 250) { nm = M_CSEED; kind = SET_CSEED; }
+        if (sw[2] < 250) { nm = M_CSEED; kind = SET_CSEED; }
         else { nm = M_SEED; kind = SET_SEED; }
       } else if (md == M_CSEED || md == M_CLOS) {
-        const int cf = d.cfail[s];
+        const int cf = sw[3];
         if (cf > 0 && (cf & 1)) {  // a closure after the BFS certificate failed: internal error
           atomicExch(&d.gctr[3], 1);
           *(volatile int*)&d.done[1] = 1;
@@ -1145,7 +1151,8 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           kind = SET_NONE;
         } else if (cf > 0) {  // not maximum yet: next attempt after a global relabel
           d.cfail[s] = 0;
-          d.cep[s] += 1;
+          sw[2] += 1;
+          d.cep[s] = sw[2];
           nm = M_SEED;
           kind = SET_SEED;
         } else if (md == M_CSEED) {
@@ -1197,7 +1204,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       }
       if (nm == M_SEED) {  // a new global relabel, bounded (relabel_bound)
         d.fbe[s] += 1;
-        d.fbnd[s] = relabel_bound(d, c, d.cep[s]);
+        d.fbnd[s] = relabel_bound(d, c, sw[2]);
       }
       bc[1] = 0;
       if (nm == M_CSEED) {  // a new closure attempt: the next reach-mark epoch of the slot
