@@ -266,7 +266,7 @@ def gc_get_profile(ctx, reset: bool = False):
 
 def debug_counters(ctx, reset: bool = False):
     """Development counters of the push phase (profiling only; not part of gc.h)."""
-    out = (ctypes.c_ulonglong * 16)()
+    out = (ctypes.c_ulonglong * 20)()
     _lib.gc_debug_counters(ctx, out, int(bool(reset)))
     return list(out)
 

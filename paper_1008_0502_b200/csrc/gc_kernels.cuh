@@ -1096,6 +1096,7 @@ struct Tmaps {
   CUtensorMap cs, ct, nb;
   int on;  // maps valid (cold frames, 16-byte aligned rows)
   int pf;  // tiles ahead of the smem load whose rows are prefetched into L2 (0: none)
+  int ef;  // load the caps with an L2 evict-first policy (read once: keep the solve's working set)
 };
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -1125,6 +1126,29 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
           (unsigned)__cvta_generic_to_shared(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(bar))
       : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_ef(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(bar)),
+      "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_ef(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                               uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                             uint64_t* bar) {
@@ -1161,9 +1185,16 @@ __device__ __forceinline__ void tma_issue_rows(const Tmaps& tm, char* stage, uin
                                                int w) {
   mbar_expect_tx(bar, (2 + K) * 512);
   const int x = tx * TS, y = ty * TS + 4 * w;
-  tma_load_3d(stage, &tm.cs, x, y, fr, bar);
-  tma_load_3d(stage + 512, &tm.ct, x, y, fr, bar);
-  tma_load_4d(stage + 1024, &tm.nb, x, y, 0, fr, bar);
+  if (tm.ef) {
+    const uint64_t pol = l2_evict_first_policy();
+    tma_load_3d_ef(stage, &tm.cs, x, y, fr, bar, pol);
+    tma_load_3d_ef(stage + 512, &tm.ct, x, y, fr, bar, pol);
+    tma_load_4d_ef(stage + 1024, &tm.nb, x, y, 0, fr, bar, pol);
+  } else {
+    tma_load_3d(stage, &tm.cs, x, y, fr, bar);
+    tma_load_3d(stage + 512, &tm.ct, x, y, fr, bar);
+    tma_load_4d(stage + 1024, &tm.nb, x, y, 0, fr, bar);
+  }
 }
 
 template <int K>

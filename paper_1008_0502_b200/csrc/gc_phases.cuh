@@ -595,9 +595,6 @@ __device__ __forceinline__ void task_cseed(const Dev& d, const IO& io, size_t gt
       mask_write(d, io, gt, mm, wr);
     }
   }
-  if (d.pdbg) {  // development: closure-seed tiles, border-only ones
-    if (t == 0) { atomicAdd(&d.pdbg[9], 1ULL); if (mode == 3) atomicAdd(&d.pdbg[10], 1ULL); }
-  }
   const int sides = block_or_bits(closure_send<K>(d, gt, mm, os, ep, flh), bc);
   if (mat) {
 #pragma unroll
@@ -671,7 +668,6 @@ __device__ __forceinline__ void task_crelax(const Dev& d, const IO& io, size_t g
   }
   any = __syncthreads_or(any);
   fail = __syncthreads_or(fail);
-  if (d.pdbg && t == 0) { atomicAdd(&d.pdbg[11], 1ULL); if (any) atomicAdd(&d.pdbg[12], 1ULL); }
   if (any) mask_write(d, io, gt, mm, nw);
   if (t == 0) {
     if (any) d.tmk[gt] = ep;
@@ -1049,8 +1045,7 @@ __device__ void init_seed_group(const Dev& d, size_t gt0, int* smem) {
 enum { SET_NONE = 0, SET_ALL = 1, SET_FLAG = 2, SET_TACT = 3, SET_SEED = 4, SET_CSEED = 5, SET_EMPTY = 6,
        SET_INITG = 8 };
 
-__device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c) {
-  const int f = d.sfr[s];
+__device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, const Ctl& c, int f) {
   GC_CHECK(d, f >= 0 && f < c.nframes && d.fout[s] >= 1);
   int st = 0;
   long long F = (long long)d.sumct[s] - (long long)d.sumneg[s];
@@ -1070,25 +1065,39 @@ __device__ __forceinline__ void finish_frame(const Dev& d, const IO& io, int s, 
 
 // Run by one CTA when the phase of slot s has no task left (fout[s] == 0): decide the next
 // phase and enqueue its tasks.  Loops while a phase turns out to have no task at all.
-__device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const Ctl& c, int* bc, uint32_t* sbits,
+__device__ __forceinline__ void transition(const Dev& d, const IO& io, int s, const Ctl& c, int* bc, uint32_t* sbits,
                                         int sbits_words) {
   const int t = threadIdx.x;
   if (t == 0) atomicAdd(&d.fout[s], 1);  // guard: no other CTA can see fout == 0 while we enqueue
-  __shared__ int sw[8];  // the slot's words, loaded at once (one round trip)
+  __shared__ int sw[12];  // the slot's words, loaded at once (one round trip)
+  uint64_t tp0 = 0, tp1 = 0;  // development section timers (profiling runs only)
+  const bool tprof = d.pdbg != nullptr && t == 0;
   for (;;) {
+    if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp0)); atomicAdd(&d.pdbg[9], 1ULL); }
     fence_gpu();
     if (t == 0) {
       const int a0 = __ldcg(d.fmode + s), a1 = __ldcg(d.ferr + s), a2 = __ldcg(d.cep + s), a3 = __ldcg(d.cfail + s);
-      const int a4 = __ldcg(d.fbnd + s);
+      const int a4 = __ldcg(d.fbnd + s), a5 = __ldcg(d.fbe + s), a6 = __ldcg(d.fph + s), a7 = __ldcg(d.sep + s);
+      const int a8 = __ldcg(d.fstat + s * 4 + 1), a9 = __ldcg(d.sfr + s);
       sw[0] = a0; sw[1] = a1; sw[2] = a2; sw[3] = a3; sw[4] = a4;
+      sw[5] = a5; sw[6] = a6; sw[7] = a7; sw[8] = a8; sw[9] = a9;
     }
     __syncthreads();
     const int md = sw[0];
     int nact = 0, hlo = HINF;
     if (md == M_BFS) {
-      for (int i = t; i < d.T; i += NTH) {
-        const size_t gt = (size_t)s * d.T + i;
-        if (__ldcg(d.tact + gt)) { nact = 1; hlo = min(hlo, __ldcg(d.tminh + gt)); }
+      for (int b0 = 0; b0 < d.T; b0 += 8 * NTH) {  // 8 tiles per thread per round trip
+        int ta[8], tm[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = b0 + j * NTH + t;
+          const size_t gt = (size_t)s * d.T + i;
+          ta[j] = i < d.T ? __ldcg(d.tact + gt) : 0;
+          tm[j] = i < d.T ? __ldcg(d.tminh + gt) : HINF;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (ta[j]) { nact = 1; hlo = min(hlo, tm[j]); }
       }
       hlo = __reduce_min_sync(0xffffffffu, hlo);
       if (t == 0) bc[6] = HINF;
@@ -1104,6 +1113,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     const int cepn = sw[2];
     const long long capw = cepn == 0 ? (long long)c.wave : (long long)max(c.wave, 1) << min(cepn * c.wavesh, 20);
     const int hcap = md == M_BFS ? (int)min((long long)min(HINF - 1, sw[4]), (long long)bc[6] + capw) : HINF - 1;
+    if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[10], tp1 - tp0); tp0 = tp1; }
     if (t == 0) {
       int nm = md, kind = SET_ALL;
       int* st = d.fstat + s * 4;
@@ -1113,11 +1123,11 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         // relax phase; range error: the closure seeds zero the mask
         nm = sw[1] ? M_CSEED : M_BFS;
         kind = sw[1] ? SET_ALL : SET_FLAG;
-        if (!sw[1]) st[1] += 1;
+        if (!sw[1]) st[1] = sw[8] + 1;
       } else if (md == M_SEED) {
         nm = M_BFS;
         kind = SET_FLAG;
-        st[1] += 1;
+        st[1] = sw[8] + 1;
       } else if (md == M_BFS) {
         if (nact) {
           nm = M_PUSH;
@@ -1128,7 +1138,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           d.fdrain[s] = 0;
           d.fhmin[s] = HINF;
           d.fcap[s] = hcap;
-          d.fph[s] += 1;
+          d.fph[s] = sw[6] + 1;
         } else {
           nm = M_CSEED;
           kind = SET_CSEED;
@@ -1164,12 +1174,12 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         }
       }
       if (finished) {
-        finish_frame(d, io, s, c);
+        finish_frame(d, io, s, c, sw[9]);
         // refill the slot: the next frame of the batch, or in sequence mode the next frame of
         // the slot's sequence, then the first frame of the next sequence not started
         int nf;
         if (c.seqL) {
-          const int f = d.sfr[s];
+          const int f = sw[9];
           if ((f + 1) % c.seqL != 0) {
             nf = f + 1;
           } else {
@@ -1202,22 +1212,25 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           }
         }
       }
+      int fbe = finished ? 1 : sw[5];  // (slot_assign: the next frame starts at relabel 1)
       if (nm == M_SEED) {  // a new global relabel, bounded (relabel_bound)
-        d.fbe[s] += 1;
+        fbe += 1;
+        d.fbe[s] = fbe;
         d.fbnd[s] = relabel_bound(d, c, sw[2]);
       }
       bc[1] = 0;
       if (nm == M_CSEED) {  // a new closure attempt: the next reach-mark epoch of the slot
-        const int se = d.sep[s] + 1;
+        const int se = sw[7] + 1;
         d.sep[s] = se;
         bc[1] = (se % 255) == 0;  // wrapped: clear the slot's marks first
       }
-      bc[3] = d.fbe[s];
+      bc[3] = fbe;
       d.fmode[s] = nm;
       bc[4] = kind;
       bc[2] = nm;
     }
     __syncthreads();
+    if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[11], tp1 - tp0); tp0 = tp1; }
     const int kind = bc[4];
     if (kind == SET_NONE) break;
     if (bc[1]) {  // reach-mark epoch wrapped (every 255 attempts of a slot): clear its marks
@@ -1237,11 +1250,20 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     // seed had an INF halo) -- a bit per tile of tuni
     const bool unibits = kind == SET_FLAG && md == M_INIT;
     if (srcskip || unibits) {
-      for (int b0 = 0; b0 < d.T; b0 += NTH) {
-        const int i = b0 + t;
-        const int32_t* w = srcskip ? d.tsrc : d.tuni;
-        const unsigned bal = __ballot_sync(0xffffffffu, i < d.T && __ldcg(w + base_gt + i) != 0);
-        if ((t & 31) == 0 && i < d.T + 31) sbits[i >> 5] = bal;
+      const int32_t* w = srcskip ? d.tsrc : d.tuni;
+      for (int b0 = 0; b0 < d.T; b0 += 8 * NTH) {  // 8 words per thread per round trip
+        int v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = b0 + j * NTH + t;
+          v[j] = i < d.T ? __ldcg(w + base_gt + i) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = b0 + j * NTH + t;
+          const unsigned bal = __ballot_sync(0xffffffffu, v[j] != 0);
+          if ((t & 31) == 0 && i < d.T + 31) sbits[i >> 5] = bal;
+        }
       }
       __syncthreads();
     }
@@ -1249,6 +1271,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
     // the decisions, a block-wide scan of the entries, ONE reservation of queue slots and task
     // counts for the whole batch, the entries written -- a few round trips per batch instead of
     // three per 256 tiles
+    if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[12], tp1 - tp0); tp0 = tp1; }
     constexpr int TB = 8;
     __shared__ int wsum[NTH / 32];
     for (int bb = 0; kind != SET_EMPTY && bb < d.T; bb += TB * NTH) {
@@ -1270,6 +1293,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
           w0[c2] = __ldcg(d.tact + gt); w1[c2] = __ldcg(d.tminh + gt);
         }
       }
+      asm volatile("" ::: "memory");  // every load above is issued before any store below
       unsigned wbits = 0;   // bit c2: this thread enqueues an entry for chunk c2
 #pragma unroll
       for (int c2 = 0; c2 < TB; ++c2) {  // decisions and their side effects
@@ -1347,8 +1371,10 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         if ((t & 31) >= o) incl += v;
       }
       if ((t & 31) == 31) wsum[t >> 5] = incl;
+      if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[15], tp1 - tp0); tp0 = tp1; }
       fence_gpu();  // this thread's tile-word writes are visible before the entries
       __syncthreads();
+      if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[16], tp1 - tp0); tp0 = tp1; }
       int wbase = 0, total = 0;
 #pragma unroll
       for (int w = 0; w < NTH / 32; ++w) {
@@ -1367,6 +1393,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         bc[7] = (int)(p0 >> 32);
       }
       __syncthreads();
+      if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[17], tp1 - tp0); tp0 = tp1; }
       const unsigned long long p0 = ((unsigned long long)(uint32_t)bc[7] << 32) | (uint32_t)bc[6];
       unsigned long long pos = p0 + (unsigned long long)(wbase + incl - mine);
 #pragma unroll
@@ -1380,7 +1407,9 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
         ++pos;
       }
       __syncthreads();
+      if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[18], tp1 - tp0); tp0 = tp1; }
     }
+    if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[13], tp1 - tp0); tp0 = tp1; }
     if (t == 0) {
       const int left = atomicSub(&d.fout[s], 1) - 1;
       GC_CHECK(d, left >= 0);
@@ -1388,6 +1417,7 @@ __device__ __noinline__ void transition(const Dev& d, const IO& io, int s, const
       bc[4] = left;
     }
     __syncthreads();
+    if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[14], tp1 - tp0); tp0 = tp1; }
     if (bc[4] != 0) break;
   }
   __syncthreads();

@@ -40,6 +40,7 @@ struct gc_ctx {
   int selfrun = 0;                // 1: a push tile re-runs itself only after progress
   int tma = 1;                    // TMA staging of the init stream when the layout allows
   int tmapf = 0;                  // ... with an L2 prefetch this many tiles ahead (measured: slower)
+  int l2ef = 0;                   // ... with an L2 evict-first policy on the cap loads
   int grid = 0;                   // k_solve CTAs of the last launch
   int grid_max = 0;               // persistent grid of k_solve<K> on this context's device
   std::string err;
@@ -53,7 +54,7 @@ struct gc_ctx {
   unsigned long long* dtiles = nullptr;  // device counters [12]: tasks [6], ns [6]
   double prof_ms[6] = {0, 0, 0, 0, 0, 0};
   double kernel_ms = 0;
-  unsigned long long dbg[16] = {0};  // development counters (profiling only)
+  unsigned long long dbg[20] = {0};  // development counters (profiling only)
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   size_t evnext = 0;
@@ -244,9 +245,9 @@ void resolve_timing(gc_ctx* c) {
 // Profiling counters of the last solve (profiling builds of the run only): tasks and summed
 // CTA time per class.
 void resolve_profile(gc_ctx* c) {
-  unsigned long long t[28];
+  unsigned long long t[32];
   if (cudaMemcpy(t, c->dtiles, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
-    for (int i = 0; i < 16; ++i) c->dbg[i] += t[12 + i];
+    for (int i = 0; i < 20; ++i) c->dbg[i] += t[12 + i];
     for (int i = 0; i < 6; ++i) {
       c->prof_tiles[i] += (long long)t[i];
       // CTA-time of the class averaged over the persistent grid: the classes (3 = queue
@@ -410,6 +411,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   memset(&tm, 0, sizeof(tm));
   tm.on = ctl.vec && c->tma && !io.img && make_tmaps(c, io, nframes, H, W, K, &tm);
   tm.pf = c->tmapf;
+  tm.ef = c->l2ef;
   k_setup<<<(unsigned)((ns + NTH - 1) / NTH < 4096 ? (ns + NTH - 1) / NTH : 4096), NTH, 0, st>>>(d, io, ctl);
   ++L.n;
   // the launch's device time, always measured (gc_get_kernel_ms): two events per launch
@@ -645,6 +647,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
   if (const char* ev = knob("GC_SELFRUN")) c->selfrun = atoi(ev);
   if (const char* ev = knob("GC_TMA")) c->tma = atoi(ev);
   if (const char* ev = knob("GC_TMAPF")) c->tmapf = atoi(ev);
+  if (const char* ev = knob("GC_L2EF")) c->l2ef = atoi(ev);
   if (const char* ev = getenv("GC_TIMEOUT_S")) c->timeout_s = atof(ev);
   if (g.max_h < 0 || g.max_w < 0 || g.max_batch < 0) { delete c; return GC_ERR_ARG; }
   if (cudaSetDevice(c->dev) != cudaSuccess) { delete c; return GC_ERR_CUDA; }
@@ -766,7 +769,7 @@ void gc_get_profile(gc_ctx* c, long long* launches, double* ms, long long* tiles
 // Development counters of the push phase (profiling only; not part of gc.h).
 void gc_debug_counters(gc_ctx* c, unsigned long long* out16, int reset) {
   if (!c) return;
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < 20; ++i) {
     if (out16) out16[i] = c->dbg[i];
     if (reset) c->dbg[i] = 0;
   }
