@@ -622,6 +622,74 @@ __device__ __forceinline__ void tile_load_smem(const Dev& d, const IO& io, size_
   const int32_t* ct = d.sct[s];
   const int32_t* nb = d.snb[s];
   const int32_t* wf = d.swf[s];
+  if (K == 4 && vec && wf && ((uintptr_t)wf & 15) == 0) {
+    // warm 4-neighbour, aligned rows: thread t takes row t/8, columns 4(t%8)..+3; every value
+    // the clamp needs in one batch of loads -- its own caps and flows (16-byte), the reverse
+    // caps and flows of the rows above / below (16-byte, same columns) and of the pixels left /
+    // right of its 4 (scalars)
+    const int iy = t >> 3, ix0 = (t & 7) * 4;
+    const int y = ty * TS + iy, x0 = tx * TS + ix0;
+    int ev[4] = {0, 0, 0, 0}, rk[4][4] = {};
+    if (y < H && x0 < W) {
+      const size_t o = (size_t)y * W + x0;
+      const bool up = y > 0, dn = y + 1 < H, lf = x0 > 0, rt = x0 + 4 < W;
+      const int4 zero = make_int4(0, 0, 0, 0);
+      const int4 a = __ldg(reinterpret_cast<const int4*>(cs + o));
+      const int4 b = __ldg(reinterpret_cast<const int4*>(ct + o));
+      const int4 c0 = __ldg(reinterpret_cast<const int4*>(nb + o));              // E
+      const int4 c1 = __ldg(reinterpret_cast<const int4*>(nb + plane + o));      // W
+      const int4 c2 = __ldg(reinterpret_cast<const int4*>(nb + 2 * plane + o));  // S
+      const int4 c3 = __ldg(reinterpret_cast<const int4*>(nb + 3 * plane + o));  // N
+      const int4 f0 = __ldg(reinterpret_cast<const int4*>(wf + o));              // flow E
+      const int4 f1 = __ldg(reinterpret_cast<const int4*>(wf + plane + o));      // flow S
+      const int4 cNdn = dn ? __ldg(reinterpret_cast<const int4*>(nb + 3 * plane + o + W)) : zero;  // c(q->p), q below
+      const int4 cSup = up ? __ldg(reinterpret_cast<const int4*>(nb + 2 * plane + o - W)) : zero;  // c(q->p), q above
+      const int4 f1up = up ? __ldg(reinterpret_cast<const int4*>(wf + plane + o - W)) : zero;      // flow S of q above
+      const int cWr = rt ? __ldg(nb + plane + o + 4) : 0;  // c(q->p), q right of the 4th pixel
+      const int cEl = lf ? __ldg(nb + o - 1) : 0;          // c(q->p), q left of the 1st
+      const int f0l = lf ? __ldg(wf + o - 1) : 0;          // flow E of q left of the 1st
+      const int A[4] = {a.x, a.y, a.z, a.w}, B[4] = {b.x, b.y, b.z, b.w};
+      const int C0[4] = {c0.x, c0.y, c0.z, c0.w}, C1[4] = {c1.x, c1.y, c1.z, c1.w};
+      const int C2[4] = {c2.x, c2.y, c2.z, c2.w}, C3[4] = {c3.x, c3.y, c3.z, c3.w};
+      const int F0[4] = {f0.x, f0.y, f0.z, f0.w}, F1[4] = {f1.x, f1.y, f1.z, f1.w};
+      const int CN[4] = {cNdn.x, cNdn.y, cNdn.z, cNdn.w}, CS[4] = {cSup.x, cSup.y, cSup.z, cSup.w};
+      const int F1U[4] = {f1up.x, f1up.y, f1up.z, f1up.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int x = x0 + i;
+        int e = A[i] - B[i];
+        if (x + 1 < W) {  // E: forward arc, flow stored here
+          const int cq = i < 3 ? C1[i + 1] : cWr;
+          const int fv = max(-cq, min(C0[i], F0[i]));
+          rk[0][i] = C0[i] - fv;
+          e -= fv;
+        }
+        if (x > 0) {  // W: the left neighbour's forward arc
+          const int cq = i > 0 ? C0[i - 1] : cEl, fr = i > 0 ? F0[i - 1] : f0l;
+          const int fv = max(-C1[i], min(cq, fr));
+          rk[1][i] = C1[i] + fv;
+          e += fv;
+        }
+        if (dn) {  // S: forward arc
+          const int fv = max(-CN[i], min(C2[i], F1[i]));
+          rk[2][i] = C2[i] - fv;
+          e -= fv;
+        }
+        if (up) {  // N: the upper neighbour's forward arc
+          const int fv = max(-C3[i], min(CS[i], F1U[i]));
+          rk[3][i] = C3[i] + fv;
+          e += fv;
+        }
+        ev[i] = e;
+      }
+    }
+    reinterpret_cast<int4*>(es)[t] = make_int4(ev[0], ev[1], ev[2], ev[3]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      reinterpret_cast<int4*>(rs + k * TPX)[t] = make_int4(rk[k][0], rk[k][1], rk[k][2], rk[k][3]);
+    __syncthreads();
+    return;
+  }
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
     const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix, lp = (iy0 + 8 * j) * TS + ix;
@@ -747,7 +815,8 @@ constexpr size_t warm_stage_bytes() { return (size_t)WS_PLANES * HS * HS * 4; }
 template <int K, bool WARM, bool EXPORT>
 __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_t gt, const FramePtrs& P,
                                                const int (&a)[4], const int (&b)[4], const int (&c)[K][4],
-                                               InitPart* part, bool sym = false, const int* ws = nullptr) {
+                                               InitPart* part, bool sym = false, const int* ws = nullptr,
+                                               const int (*wq)[4] = nullptr, const int (*wfr)[4] = nullptr) {
   const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
@@ -764,6 +833,9 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
   int uni = 1, src = 1;
   long long sct = 0, neg = 0;
   int fl4[4];
+  int fwv[K / 2][4];  // exported forward flows of the 4 pixels (EXPORT)
+  // 16-byte export stores: the 4 pixels in the frame and the rows aligned
+  const bool ev4 = EXPORT && K == 4 && y < H && x0 + 3 < W && (((uintptr_t)(P.fs + o0)) & 15) == 0 && ((plane & 3) == 0);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int x = x0 + i;
@@ -796,15 +868,15 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
           // energy caps are symmetric (c(q -> p) = c(p -> q)): the neighbour's may not be built yet
           // (staged: the pixel's position in the 34 x 34 blocks and its neighbour's)
           const int hp = (iy + 1) * HS + ix0 + i + 1, hq = hp + DYk(k) * HS + DXk(k);
-          const int cq = sym ? ck : (ws ? ws[(k ^ 1) * HS * HS + hq] : __ldg(nb + (k ^ 1) * plane + oq));
+          const int cq = sym ? ck : (wq ? wq[k][i] : (ws ? ws[(k ^ 1) * HS * HS + hq] : __ldg(nb + (k ^ 1) * plane + oq)));
           if ((k & 1) == 0) {
-            const int fraw = ws ? ws[(4 + (k >> 1)) * HS * HS + hp] : __ldg(wf + (k >> 1) * plane + o0 + i);
+            const int fraw = wfr ? wfr[k][i] : (ws ? ws[(4 + (k >> 1)) * HS * HS + hp] : __ldg(wf + (k >> 1) * plane + o0 + i));
             const int fv = max(-cq, min(ck, fraw));
             rk = ck - fv;
             ev -= fv;
             fw[k >> 1] = fv;
           } else {
-            const int fraw = ws ? ws[(4 + ((k ^ 1) >> 1)) * HS * HS + hq] : __ldg(wf + ((k ^ 1) >> 1) * plane + oq);
+            const int fraw = wfr ? wfr[k][i] : (ws ? ws[(4 + ((k ^ 1) >> 1)) * HS * HS + hq] : __ldg(wf + ((k ^ 1) >> 1) * plane + oq));
             const int fv = max(-ck, min(cq, fraw));
             rk = ck + fv;
             ev += fv;
@@ -817,12 +889,21 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
       uni &= ev < 0;
       src &= ev > 0;
       if (EXPORT) {  // a5: the export of a tile no push ever touches is its initial flow
-        int32_t* fo = P.fs + o0 + i;
 #pragma unroll
-        for (int k = 0; k < K / 2; ++k) fo[k * plane] = fw[k];
+        for (int k = 0; k < K / 2; ++k) fwv[k][i] = fw[k];
+        if (!ev4) {
+          int32_t* fo = P.fs + o0 + i;
+#pragma unroll
+          for (int k = 0; k < K / 2; ++k) fo[k * plane] = fw[k];
+        }
       }
     }
     fl4[i] = f;
+  }
+  if (ev4) {
+#pragma unroll
+    for (int k = 0; k < K / 2; ++k)
+      *reinterpret_cast<int4*>(P.fs + k * plane + o0) = make_int4(fwv[k][0], fwv[k][1], fwv[k][2], fwv[k][3]);
   }
   int bad = (acc & ~CAPMAX) != 0;
   ushort4 w;
@@ -1197,6 +1278,59 @@ __device__ __forceinline__ void tma_issue_rows(const Tmaps& tm, char* stage, uin
   }
 }
 
+// Warm 4-neighbour init loads, aligned rows (thread t: row t/8, columns 4(t%8)..+3): the
+// pixel's caps, and per arc k the reverse cap c(q -> p) (wq) and the stored flow of the arc
+// (wfr: the pixel's own forward flow for E / S, the neighbour's for W / N) -- one batch of
+// independent loads (16-byte rows, the rows above / below, scalars left / right of the 4).
+// Off-frame arcs read 0 (tile_init_regs ignores them).
+__device__ __forceinline__ void warm4_load(const Dev& d, const FramePtrs& P, int ty, int tx, int (&a)[4], int (&b)[4],
+                                           int (&c)[4][4], int (&wq)[4][4], int (&wfr)[4][4]) {
+  const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
+  const int H = d.H, W = d.W;
+  const size_t plane = (size_t)H * W;
+  const int y = ty * TS + iy, x0 = tx * TS + ix0;
+  const int4 zero = make_int4(0, 0, 0, 0);
+  int4 va = zero, vb = zero, c0 = zero, c1 = zero, c2 = zero, c3 = zero, f0 = zero, f1 = zero;
+  int4 cNdn = zero, cSup = zero, f1up = zero;
+  int cWr = 0, cEl = 0, f0l = 0;
+  if (y < H && x0 < W) {
+    const size_t o = (size_t)y * W + x0;
+    const bool up = y > 0, dn = y + 1 < H, lf = x0 > 0, rt = x0 + 4 < W;
+    va = __ldg(reinterpret_cast<const int4*>(P.cs + o));
+    vb = __ldg(reinterpret_cast<const int4*>(P.ct + o));
+    c0 = __ldg(reinterpret_cast<const int4*>(P.nb + o));
+    c1 = __ldg(reinterpret_cast<const int4*>(P.nb + plane + o));
+    c2 = __ldg(reinterpret_cast<const int4*>(P.nb + 2 * plane + o));
+    c3 = __ldg(reinterpret_cast<const int4*>(P.nb + 3 * plane + o));
+    f0 = __ldg(reinterpret_cast<const int4*>(P.wf + o));
+    f1 = __ldg(reinterpret_cast<const int4*>(P.wf + plane + o));
+    if (dn) cNdn = __ldg(reinterpret_cast<const int4*>(P.nb + 3 * plane + o + W));
+    if (up) cSup = __ldg(reinterpret_cast<const int4*>(P.nb + 2 * plane + o - W));
+    if (up) f1up = __ldg(reinterpret_cast<const int4*>(P.wf + plane + o - W));
+    if (rt) cWr = __ldg(P.nb + plane + o + 4);
+    if (lf) cEl = __ldg(P.nb + o - 1);
+    if (lf) f0l = __ldg(P.wf + o - 1);
+  }
+  a[0] = va.x; a[1] = va.y; a[2] = va.z; a[3] = va.w;
+  b[0] = vb.x; b[1] = vb.y; b[2] = vb.z; b[3] = vb.w;
+  c[0][0] = c0.x; c[0][1] = c0.y; c[0][2] = c0.z; c[0][3] = c0.w;
+  c[1][0] = c1.x; c[1][1] = c1.y; c[1][2] = c1.z; c[1][3] = c1.w;
+  c[2][0] = c2.x; c[2][1] = c2.y; c[2][2] = c2.z; c[2][3] = c2.w;
+  c[3][0] = c3.x; c[3][1] = c3.y; c[3][2] = c3.z; c[3][3] = c3.w;
+  // E (k = 0): c(q -> p) = W cap of the right neighbour, flow = own E flow
+  wq[0][0] = c1.y; wq[0][1] = c1.z; wq[0][2] = c1.w; wq[0][3] = cWr;
+  wfr[0][0] = f0.x; wfr[0][1] = f0.y; wfr[0][2] = f0.z; wfr[0][3] = f0.w;
+  // W (k = 1): c(q -> p) = E cap of the left neighbour, flow = its E flow
+  wq[1][0] = cEl; wq[1][1] = c0.x; wq[1][2] = c0.y; wq[1][3] = c0.z;
+  wfr[1][0] = f0l; wfr[1][1] = f0.x; wfr[1][2] = f0.y; wfr[1][3] = f0.z;
+  // S (k = 2): c(q -> p) = N cap of the pixel below, flow = own S flow
+  wq[2][0] = cNdn.x; wq[2][1] = cNdn.y; wq[2][2] = cNdn.z; wq[2][3] = cNdn.w;
+  wfr[2][0] = f1.x; wfr[2][1] = f1.y; wfr[2][2] = f1.z; wfr[2][3] = f1.w;
+  // N (k = 3): c(q -> p) = S cap of the pixel above, flow = its S flow
+  wq[3][0] = cSup.x; wq[3][1] = cSup.y; wq[3][2] = cSup.z; wq[3][3] = cSup.w;
+  wfr[3][0] = f1up.x; wfr[3][1] = f1up.y; wfr[3][2] = f1up.z; wfr[3][3] = f1up.w;
+}
+
 template <int K>
 __device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0, bool vec, int* smem,
                                           const Tmaps& tm, uint64_t* mbar, unsigned& tpar) {
@@ -1270,17 +1404,16 @@ __device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0
       if (P.fs) tile_init_regs<K, false, true>(d, io, gt0 + i, P, a, b, c, part + i);
       else tile_init_regs<K, false, false>(d, io, gt0 + i, P, a, b, c, part + i);
     }
-  } else if (K == 4 && vec && P.wf) {
-    // warm 4-neighbour frames, aligned rows: every neighbour cap / flow staged in shared memory
-    int* ws = reinterpret_cast<int*>(uni_s + INIT_GMAX);
+  } else if (K == 4 && vec && P.wf && ((uintptr_t)P.wf & 15) == 0) {
+    // warm 4-neighbour frames, aligned rows: every cap and flow the clamp needs in one batch of
+    // loads per tile (warm4_load; no staging, no barrier)
 #pragma unroll 1
     for (int i = 0; i < n; ++i) {
       const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
-      init_load<K>(d, P, ty, tx, vec, a, b, c);
-      if (i) __syncthreads();  // the previous tile's stage is consumed
-      warm_stage4(d, P, ty, tx, reinterpret_cast<const int(&)[4][4]>(c), ws);
-      if (P.fs) tile_init_regs<K, true, true>(d, io, gt0 + i, P, a, b, c, part + i, false, ws);
-      else tile_init_regs<K, true, false>(d, io, gt0 + i, P, a, b, c, part + i, false, ws);
+      int wq[4][4], wfr[4][4];
+      warm4_load(d, P, ty, tx, a, b, reinterpret_cast<int(&)[4][4]>(c), wq, wfr);
+      if (P.fs) tile_init_regs<K, true, true>(d, io, gt0 + i, P, a, b, c, part + i, false, nullptr, wq, wfr);
+      else tile_init_regs<K, true, false>(d, io, gt0 + i, P, a, b, c, part + i, false, nullptr, wq, wfr);
     }
   } else {
 #pragma unroll 1

@@ -692,6 +692,36 @@ __device__ __forceinline__ void task_export(const Dev& d, const IO& io, size_t g
   const size_t plane = (size_t)H * W;
   const size_t fr = (size_t)d.sfr[s];
   int32_t* fsp = d.sfs[s];
+  const int32_t* nbp = d.snb[s];
+  if (K == 4 && (W & 3) == 0 && (((uintptr_t)fsp | (uintptr_t)nbp) & 15) == 0) {
+    // aligned rows (a materialised tile, the only kind exported here): thread t takes row t/8,
+    // columns 4(t%8)..+3 -- every residual and cap of its forward arcs in 16-byte loads at once
+    const int iy = t >> 3, ix0 = (t & 7) * 4;
+    const int y = ty * TS + iy, x0 = tx * TS + ix0;
+    if (y < H && x0 < W) {
+      const size_t o = (size_t)y * W + x0;
+      int4 rv[K / 2], cv[K / 2];
+#pragma unroll
+      for (int kk = 0; kk < K / 2; ++kk) {
+        rv[kk] = *reinterpret_cast<const int4*>(Rp(d, K, gt, 2 * kk) + iy * TS + ix0);
+        cv[kk] = __ldg(reinterpret_cast<const int4*>(nbp + 2 * kk * plane + o));
+      }
+#pragma unroll
+      for (int kk = 0; kk < K / 2; ++kk) {
+        const int k = 2 * kk, y2 = y + DYk(k);
+        const int* rr = &rv[kk].x;
+        const int* cc = &cv[kk].x;
+        int f[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int x2 = x0 + i + DXk(k);
+          f[i] = (y2 >= 0 && y2 < H && x2 >= 0 && x2 < W) ? cc[i] - rr[i] : 0;
+        }
+        *reinterpret_cast<int4*>(fsp + kk * plane + o) = make_int4(f[0], f[1], f[2], f[3]);
+      }
+    }
+    return;
+  }
 #pragma unroll 1
   for (int j = 0; j < 4; ++j) {
     const int y = ty * TS + iy0 + 8 * j, x = tx * TS + ix;
