@@ -806,17 +806,11 @@ struct InitPart {
                             // bit 2: not a uniform source tile
 };
 
-// Warm init of a 4-neighbour tile from shared memory (warm_stage4): per plane a 34 x 34 block
-// (the tile and a one-pixel ring, hidx layout) of c_E, c_W, c_S, c_N and the forward flows
-// f_E, f_S, so that every clamp reads its neighbour's cap and flow without a global load.
-constexpr int WS_PLANES = 6;  // c0..c3, wf0, wf1
-constexpr size_t warm_stage_bytes() { return (size_t)WS_PLANES * HS * HS * 4; }
-
 template <int K, bool WARM, bool EXPORT>
 __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_t gt, const FramePtrs& P,
                                                const int (&a)[4], const int (&b)[4], const int (&c)[K][4],
-                                               InitPart* part, bool sym = false, const int* ws = nullptr,
-                                               const int (*wq)[4] = nullptr, const int (*wfr)[4] = nullptr) {
+                                               InitPart* part, bool sym = false, const int (*wq)[4] = nullptr,
+                                               const int (*wfr)[4] = nullptr) {
   const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
   const int ty = tile / d.TX, tx = tile - ty * d.TX;
   const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
@@ -865,18 +859,17 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
         if (WARM && on) {  // a1w: clamp the previous flow to the new capacities
           const int y2 = y + DYk(k), x2 = x + DXk(k);
           const size_t oq = (size_t)y2 * W + x2;
-          // energy caps are symmetric (c(q -> p) = c(p -> q)): the neighbour's may not be built yet
-          // (staged: the pixel's position in the 34 x 34 blocks and its neighbour's)
-          const int hp = (iy + 1) * HS + ix0 + i + 1, hq = hp + DYk(k) * HS + DXk(k);
-          const int cq = sym ? ck : (wq ? wq[k][i] : (ws ? ws[(k ^ 1) * HS * HS + hq] : __ldg(nb + (k ^ 1) * plane + oq)));
+          // energy caps are symmetric (c(q -> p) = c(p -> q)): the neighbour's may not be built yet;
+          // wq / wfr: the values warm4_load fetched
+          const int cq = sym ? ck : (wq ? wq[k][i] : __ldg(nb + (k ^ 1) * plane + oq));
           if ((k & 1) == 0) {
-            const int fraw = wfr ? wfr[k][i] : (ws ? ws[(4 + (k >> 1)) * HS * HS + hp] : __ldg(wf + (k >> 1) * plane + o0 + i));
+            const int fraw = wfr ? wfr[k][i] : __ldg(wf + (k >> 1) * plane + o0 + i);
             const int fv = max(-cq, min(ck, fraw));
             rk = ck - fv;
             ev -= fv;
             fw[k >> 1] = fv;
           } else {
-            const int fraw = wfr ? wfr[k][i] : (ws ? ws[(4 + ((k ^ 1) >> 1)) * HS * HS + hq] : __ldg(wf + ((k ^ 1) >> 1) * plane + oq));
+            const int fraw = wfr ? wfr[k][i] : __ldg(wf + ((k ^ 1) >> 1) * plane + oq);
             const int fv = max(-ck, min(cq, fraw));
             rk = ck + fv;
             ev += fv;
@@ -936,53 +929,6 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
     part->neg[t >> 5] = (long long)n_lo + ((long long)n_hi << 16);
     part->fl[t >> 5] = wfl;
   }
-}
-
-// Stage the 34 x 34 blocks of warm_stage_bytes for tile (ty, tx) of a 4-neighbour frame: the
-// thread's own 4 pixels from registers (caps) and 16-byte loads (flows), the ring by 132
-// threads (0 off the frame).  Block-wide; ends with a barrier.
-__device__ __forceinline__ void warm_stage4(const Dev& d, const FramePtrs& P, int ty, int tx, const int (&c)[4][4],
-                                            int* ws) {
-  const int t = threadIdx.x, iy = t >> 3, ix0 = (t & 7) * 4;
-  const int H = d.H, W = d.W;
-  const size_t plane = (size_t)H * W;
-  const int y = ty * TS + iy, x0 = tx * TS + ix0;
-  int4 f0 = make_int4(0, 0, 0, 0), f1 = f0;
-  if (y < H && x0 + 3 < W) {
-    f0 = __ldg(reinterpret_cast<const int4*>(P.wf + (size_t)y * W + x0));
-    f1 = __ldg(reinterpret_cast<const int4*>(P.wf + plane + (size_t)y * W + x0));
-  } else if (y < H) {
-    int* a0 = &f0.x;
-    int* a1 = &f1.x;
-    for (int i = 0; i < 4; ++i)
-      if (x0 + i < W) { a0[i] = __ldg(P.wf + (size_t)y * W + x0 + i); a1[i] = __ldg(P.wf + plane + (size_t)y * W + x0 + i); }
-  }
-  const int base = (iy + 1) * HS + ix0 + 1;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) ws[k * HS * HS + base + i] = c[k][i];
-  }
-  ws[4 * HS * HS + base + 0] = f0.x; ws[4 * HS * HS + base + 1] = f0.y;
-  ws[4 * HS * HS + base + 2] = f0.z; ws[4 * HS * HS + base + 3] = f0.w;
-  ws[5 * HS * HS + base + 0] = f1.x; ws[5 * HS * HS + base + 1] = f1.y;
-  ws[5 * HS * HS + base + 2] = f1.z; ws[5 * HS * HS + base + 3] = f1.w;
-  // the ring: every plane's value at the 4 x 32 border neighbours (+ corners unused by K = 4)
-  if (t < 128) {
-    const int side = t >> 5, i = t & 31;
-    int yy, xx, pos;
-    if (side == 0) { yy = ty * TS - 1; xx = tx * TS + i; pos = hidx(-1, i); }
-    else if (side == 1) { yy = ty * TS + 32; xx = tx * TS + i; pos = hidx(32, i); }
-    else if (side == 2) { yy = ty * TS + i; xx = tx * TS - 1; pos = hidx(i, -1); }
-    else { yy = ty * TS + i; xx = tx * TS + 32; pos = hidx(i, 32); }
-    const bool in = yy >= 0 && yy < H && xx >= 0 && xx < W;
-    const size_t o = in ? (size_t)yy * W + xx : 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) ws[k * HS * HS + pos] = in ? __ldg(P.nb + k * plane + o) : 0;
-    ws[4 * HS * HS + pos] = in ? __ldg(P.wf + o) : 0;
-    ws[5 * HS * HS + pos] = in ? __ldg(P.wf + plane + o) : 0;
-  }
-  __syncthreads();
 }
 
 // Per-tile results of an init group, after a barrier: tile words, frame sums, range flag,
@@ -1412,8 +1358,8 @@ __device__ __forceinline__ void task_init(const Dev& d, const IO& io, size_t gt0
       const int tile = tile0 + i, ty = tile / d.TX, tx = tile - ty * d.TX;
       int wq[4][4], wfr[4][4];
       warm4_load(d, P, ty, tx, a, b, reinterpret_cast<int(&)[4][4]>(c), wq, wfr);
-      if (P.fs) tile_init_regs<K, true, true>(d, io, gt0 + i, P, a, b, c, part + i, false, nullptr, wq, wfr);
-      else tile_init_regs<K, true, false>(d, io, gt0 + i, P, a, b, c, part + i, false, nullptr, wq, wfr);
+      if (P.fs) tile_init_regs<K, true, true>(d, io, gt0 + i, P, a, b, c, part + i, false, wq, wfr);
+      else tile_init_regs<K, true, false>(d, io, gt0 + i, P, a, b, c, part + i, false, wq, wfr);
     }
   } else {
 #pragma unroll 1

@@ -755,9 +755,7 @@ constexpr size_t push_smem_bytes() { return sizeof(int) * (2 * HS * HS + TPX + K
 // dynamic shared memory of k_solve: the largest task layout
 template <int K>
 constexpr size_t solve_smem_bytes() {
-  return push_smem_bytes<K>() > init_smem_bytes<K>() - (2 + K) * NTH * 16 + warm_stage_bytes()
-             ? push_smem_bytes<K>()
-             : init_smem_bytes<K>() - (2 + K) * NTH * 16 + warm_stage_bytes();
+  return push_smem_bytes<K>() > init_smem_bytes<K>() ? push_smem_bytes<K>() : init_smem_bytes<K>();
 }
 static_assert(init_smem_bytes<4>() <= push_smem_bytes<4>() && init_smem_bytes<8>() <= push_smem_bytes<8>(),
               "the init pass's prefetch buffer must fit the push tile's shared memory");
