@@ -38,6 +38,8 @@ CONFIGS = {
                frames=1024, seed_off=3),
     "c5": dict(workload="C5 3840x2160 serpentine adversarial, 4-nbr", kind="serpentine", H=2160, W=3840, K=4,
                frames=8, seed_off=4, oracle_hw=(540, 960)),
+    # NEXT-3 workload: single 4K frames, solved one per call with --frames 1
+    "c4k": dict(workload="3840x2160 blob frames, 8-nbr", kind="blob", H=2160, W=3840, K=8, frames=8, seed_off=14),
 }
 # algorithmic bytes per processed 32x32 tile and kernel class
 
@@ -609,6 +611,8 @@ def main():
     ap.add_argument("--saliency", action="store_true", help="NEXT-4: the saliency front-end (gc_saliency)")
     ap.add_argument("--warm", action="store_true",
                     help="sequence mode (C3): S sequences x L frames, frame t warm-started from t-1")
+    ap.add_argument("--parts", type=int, default=1,
+                    help="NEXT-3: band-partition every frame over N CTA groups (gc_set_partitions; 1: off)")
     ap.add_argument("--seqs", type=int, default=8)
     ap.add_argument("--seq-len", type=int, default=120)
     args = ap.parse_args()
@@ -657,6 +661,8 @@ def main():
     mask = torch.empty((n, H, W), dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     g = gc.GridCut(neighborhood=K, max_h=H, max_w=W)
+    if args.parts > 1:  # NEXT-3: band partition of each frame over CTA groups (gc_set_partitions)
+        g.set_partitions(args.parts)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -740,11 +746,13 @@ def main():
     g.set_profiling(True)
     g.profile(reset=True)
     g.kernel_ms(reset=True)
+    gc.debug_counters(g.ctx, reset=True)
     for _ in range(args.profile_steps):
         g.solve(cs, ct, nb, out=(flow, mask))
     torch.cuda.synchronize()
     prof = g.profile(reset=True)
     kms_prof = g.kernel_ms(reset=True)
+    cross_band = gc.debug_counters(g.ctx, reset=True)[19] / max(1, n * args.profile_steps)
     g.set_profiling(False)
     peak, peak_src = load_peak()
     nlp = max(prof["init"][0], 1)
@@ -835,7 +843,10 @@ def main():
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
                "data": "synthetic (seeded saliency-blob frames, synth/; generated on device before timing)",
                "config": {"workload": cfg["workload"], "H": H, "W": W, "K": K, "frames_per_rank": n,
-                          "frames_total": n * world, "parallelism": f"frame-sharded dp{world}",
+                          "frames_total": n * world, "parallelism": f"frame-sharded dp{world}" +
+                          (f", each frame band-partitioned over {args.parts} CTA groups (NEXT-3 emulation)"
+                           if args.parts > 1 else ""),
+                          "partitions": args.parts,
                           "l2": (f"inputs {in_bytes / 1e9:.2f} GB per rank: L2 (126 MB) flushed by a 252 MB write before "
                                  f"each separately timed step" if l2_flush else
                                  f"inputs {in_bytes / 1e9:.1f} GB per rank >> 126 MB L2 (no flush needed)")},
@@ -850,6 +861,7 @@ def main():
                "checksum": {"sum_F": int(stats[0].item()), "sum_mask": int(stats[1].item()),
                             "hash_xor": int(np.bitwise_xor.reduce(per_frame[:, 2].cpu().numpy()))},
                "cross_rank": cross,
+               "cross_band_handoffs_per_frame": round(cross_band, 1) if args.parts > 1 else None,
                "verify": verify,
                "paper_context": "graph-cut stage 1.47 / 6.65 / 1.41 Mpx/s on a GeForce 9800GT (P:757-762)"}
         print(json.dumps(out), flush=True)

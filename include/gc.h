@@ -260,6 +260,20 @@ gc_status gc_saliency_dims(int H, int W, int* h4, int* w4);
  * sigma 2, wavelength 6, aspect 0.5, mean removed (DESIGN.md c19).  Host only. */
 gc_status gc_gabor_kernels(float* out);
 
+/* NEXT-3 (per-pixel time vs resolution): band
+ * partition of every frame's tiles for the next solves on this context.  The tile rows of a
+ * frame are split into `parts` horizontal bands of ceil(tile rows / parts) rows; every task of
+ * band b (init group, relabel, push, closure) is queued on band b's own ring and run only by
+ * the persistent CTAs with blockIdx % parts == b, so band b's state is only ever written by its
+ * own CTAs except across the band border (border flow counters, requests, reach marks, halo
+ * reads) -- the owner-computes schedule of a parts-GPU domain decomposition of one frame,
+ * EMULATED in one kernel on one device (the bands share the device's memory; nothing here
+ * spans GPUs).  Results are identical for every `parts`; profiling counts the cross-band
+ * requests and task hand-offs (development counter 19).  parts = 1 (default) turns it off; 1 <= parts <=
+ * GC_PARTS_MAX, else GC_ERR_ARG.  Host only. */
+#define GC_PARTS_MAX 8
+gc_status gc_set_partitions(gc_ctx* ctx, int parts);
+
 /* Message for the last failing call on this context ("" if none).  Never NULL. */
 const char* gc_last_error(const gc_ctx* ctx);
 

@@ -18,7 +18,8 @@ import numpy as np
 __all__ = ["GridCut", "GcError", "gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_solve_sequences",
            "gc_solve_energy", "gc_gmm_prepare", "gc_gauss_taps", "gc_kalman_step", "gc_prior_update",
            "gc_saliency", "gc_saliency_dims", "gc_gabor_kernels",
-           "gc_frame_digest", "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "CAP_MAX",
+           "gc_frame_digest", "gc_last_error", "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms",
+           "gc_set_partitions", "CAP_MAX", "PARTS_MAX",
            "STATUS", "lib_path"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -121,6 +122,8 @@ _lib.gc_last_launches.argtypes = [ctypes.c_void_p]
 _lib.gc_last_launches.restype = ctypes.c_longlong
 _lib.gc_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int]
 _lib.gc_set_profiling.restype = None
+_lib.gc_set_partitions.argtypes = [ctypes.c_void_p, ctypes.c_int]
+_lib.gc_set_partitions.restype = ctypes.c_int
 _lib.gc_get_profile.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_longlong),
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]
 _lib.gc_get_profile.restype = None
@@ -135,7 +138,8 @@ _lib.gc_frame_digest.restype = ctypes.c_int
 EXPORTED = ("gc_create", "gc_destroy", "gc_solve_batch", "gc_solve_batch_host", "gc_last_error",
             "gc_last_launches", "gc_set_profiling", "gc_get_profile", "gc_get_kernel_ms", "gc_frame_digest",
             "gc_solve_sequences", "gc_solve_energy", "gc_gmm_prepare", "gc_gauss_taps", "gc_kalman_step",
-            "gc_prior_update", "gc_saliency", "gc_saliency_dims", "gc_gabor_kernels")
+            "gc_prior_update", "gc_saliency", "gc_saliency_dims", "gc_gabor_kernels", "gc_set_partitions")
+PARTS_MAX = 8  # GC_PARTS_MAX
 
 
 class GcError(RuntimeError):
@@ -250,6 +254,12 @@ def gc_last_error(ctx) -> str:
 
 def gc_last_launches(ctx) -> int:
     return int(_lib.gc_last_launches(ctx))
+
+
+def gc_set_partitions(ctx, parts: int) -> None:
+    st = _lib.gc_set_partitions(ctx, int(parts))
+    if st != 0:
+        raise GcError(st, "gc_set_partitions: parts must be in [1, PARTS_MAX]")
 
 
 def gc_set_profiling(ctx, enable: bool) -> None:
@@ -493,6 +503,10 @@ class GridCut:
 
     def launches(self) -> int:
         return gc_last_launches(self.ctx)
+
+    def set_partitions(self, parts: int):
+        """NEXT-3: band partition of every frame over `parts` CTA groups (gc.h gc_set_partitions)."""
+        gc_set_partitions(self.ctx, parts)
 
     def set_profiling(self, on):
         """False/True, or 2 for the development per-task trace as well."""

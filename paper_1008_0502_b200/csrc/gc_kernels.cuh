@@ -128,6 +128,12 @@ struct Dev {
   unsigned long long* qitail;
   int32_t* done;    // [0] every frame finished, [1] aborted
   unsigned long long* ntask;  // tasks executed (watchdog)
+  // NEXT-3 band partition (gc_set_partitions): a frame's tile rows split into nparts bands of
+  // prow rows; band b's tasks go to ring b (q / qi + b x capacity, head / tail pairs at
+  // qhead + 2b, qihead + 2b) and run only on CTAs with blockIdx % nparts == b -- the owner-
+  // computes schedule of an nparts-GPU domain decomposition, emulated in one kernel.  1: off.
+  int nparts;
+  int prow;
   const volatile int32_t* hostabort;  // mapped host word: the host asks the kernel to stop
   unsigned long long* ptiles;  // [6] tasks per class (profiling only, else NULL)
   unsigned long long* pns;     // [6] ns per class summed over CTAs (profiling only)

@@ -121,14 +121,24 @@ __device__ __forceinline__ int ld_acquire_s32(const int32_t* p) {
   return v;
 }
 
-__device__ __forceinline__ void q_put(const Dev& d, unsigned long long p, uint32_t v) {
-  volatile uint32_t* slot = d.q + (p & d.qmask);
+// Band (NEXT-3 partition) owning tile gt: 0 unless the call is partitioned.
+__device__ __forceinline__ int part_of(const Dev& d, size_t gt) {
+  if (d.nparts <= 1) return 0;
+  const int s = (int)((unsigned)gt / (unsigned)d.T), tile = (int)(gt - (size_t)s * d.T);
+  return min(tile / d.TX / d.prow, d.nparts - 1);
+}
+__device__ __forceinline__ void q_put(const Dev& d, int r, unsigned long long p, uint32_t v) {
+  volatile uint32_t* slot = d.q + (size_t)r * (d.qmask + 1) + (p & d.qmask);
   while (*slot != QEMPTY) __nanosleep(32);  // previous lap not consumed yet (capacity 2x: never in practice)
   *slot = v;
 }
-__device__ __forceinline__ void chain_put(const Dev& d, uint32_t v) { q_put(d, atomicAdd(d.qtail, 1ULL), v); }
-__device__ __forceinline__ void qi_put(const Dev& d, unsigned long long p, uint32_t v) {
-  volatile uint32_t* slot = d.qi + (p & d.qimask);
+// A task entry to the ring of the band owning its tile.
+__device__ __forceinline__ void chain_put(const Dev& d, uint32_t v) {
+  const int r = part_of(d, v & 0x00ffffffu);
+  q_put(d, r, atomicAdd(d.qtail + 2 * r, 1ULL), v);
+}
+__device__ __forceinline__ void qi_put(const Dev& d, int r, unsigned long long p, uint32_t v) {
+  volatile uint32_t* slot = d.qi + (size_t)r * (d.qimask + 1) + (p & d.qimask);
   while (*slot != QEMPTY) __nanosleep(32);
   *slot = v;
 }
@@ -1231,11 +1241,13 @@ __device__ __forceinline__ void transition(const Dev& d, const IO& io, int s, co
           kind = SET_NONE;
           {  // a slot goes idle: release the CTAs parked on the init ring (tickets beyond its
              // tail; in batch mode no init group will be queued any more), one no-op entry each
-            const unsigned long long ih = atomicAdd(d.qihead, 0ULL), it = atomicAdd(d.qitail, 0ULL);
-            const unsigned parked = ih > it ? (unsigned)min(ih - it, (unsigned long long)gridDim.x) : 0u;
-            if (parked) {
-              const unsigned long long p0 = atomicAdd(d.qitail, (unsigned long long)parked);
-              for (unsigned i = 0; i < parked; ++i) qi_put(d, p0 + i, QNOP);
+            for (int r = 0; r < d.nparts; ++r) {
+              const unsigned long long ih = atomicAdd(d.qihead + 2 * r, 0ULL), it = atomicAdd(d.qitail + 2 * r, 0ULL);
+              const unsigned parked = ih > it ? (unsigned)min(ih - it, (unsigned long long)gridDim.x) : 0u;
+              if (parked) {
+                const unsigned long long p0 = atomicAdd(d.qitail + 2 * r, (unsigned long long)parked);
+                for (unsigned i = 0; i < parked; ++i) qi_put(d, r, p0 + i, QNOP);
+              }
             }
           }
         }
@@ -1416,9 +1428,11 @@ __device__ __forceinline__ void transition(const Dev& d, const IO& io, int s, co
       }
       if (t == 0) {
         atomicAdd(&d.fout[s], total);
-        const unsigned long long p0 = atomicAdd(kind == SET_INITG ? d.qitail : d.qtail, (unsigned long long)total);
-        bc[6] = (int)(p0 & 0xffffffffu);
-        bc[7] = (int)(p0 >> 32);
+        if (d.nparts <= 1) {
+          const unsigned long long p0 = atomicAdd(kind == SET_INITG ? d.qitail : d.qtail, (unsigned long long)total);
+          bc[6] = (int)(p0 & 0xffffffffu);
+          bc[7] = (int)(p0 >> 32);
+        }
       }
       __syncthreads();
       if (tprof) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); atomicAdd(&d.pdbg[17], tp1 - tp0); tp0 = tp1; }
@@ -1430,8 +1444,16 @@ __device__ __forceinline__ void transition(const Dev& d, const IO& io, int s, co
         const int i = bb + c2 * NTH + t;
         const int gcnt = ((kind == SET_SEED || kind == SET_CSEED) && d.bulkg > 1) ? min(d.bulkg, d.T - i) : 1;
         const uint32_t ent = qent(bc[2], base_gt + i, gcnt);
-        if (kind == SET_INITG) qi_put(d, pos, ent);
-        else q_put(d, pos, ent);
+        if (d.nparts > 1) {  // partitioned: each entry to its band's CHAIN ring -- init groups
+          // too: the band's CTAs may all be parked on that ring (no other CTA serves the band)
+          const int r = part_of(d, base_gt + i);
+          if (d.pdbg && r != (int)(blockIdx.x % (unsigned)d.nparts)) atomicAdd(&d.pdbg[19], 1ULL);  // cross-band
+          q_put(d, r, atomicAdd(d.qtail + 2 * r, 1ULL), ent);
+        } else if (kind == SET_INITG) {
+          qi_put(d, 0, pos, ent);
+        } else {
+          q_put(d, 0, pos, ent);
+        }
         ++pos;
       }
       __syncthreads();
@@ -1470,6 +1492,7 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
   if (threadIdx.x == 0) next_s = QEMPTY;
   const int t = threadIdx.x;
   const bool prof = d.pns != nullptr;
+  const int myband = d.nparts > 1 ? (int)(blockIdx.x % (unsigned)d.nparts) : 0;
   unsigned long long t_idle = 0;
   unsigned ntask_local = 0;
   for (;;) {
@@ -1488,12 +1511,13 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
       volatile uint32_t* slot;
       {
         unsigned long long qh, qt, qih, qit;  // one 16-byte load per ring: head, tail
-        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qh), "=l"(qt) : "l"(d.qhead));
-        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qih), "=l"(qit) : "l"(d.qihead));
+        const int r = myband;                 // partitioned: this CTA's band's rings only
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qh), "=l"(qt) : "l"(d.qhead + 2 * r));
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(qih), "=l"(qit) : "l"(d.qihead + 2 * r));
         if (qt <= qh && qit > qih) {
-          slot = d.qi + (atomicAdd(d.qihead, 1ULL) & d.qimask);
+          slot = d.qi + (size_t)r * (d.qimask + 1) + (atomicAdd(d.qihead + 2 * r, 1ULL) & d.qimask);
         } else {
-          slot = d.q + (atomicAdd(d.qhead, 1ULL) & d.qmask);
+          slot = d.q + (size_t)r * (d.qmask + 1) + (atomicAdd(d.qhead + 2 * r, 1ULL) & d.qmask);
         }
       }
       // acquire: the task's producers wrote its state before they queued it
@@ -1615,7 +1639,9 @@ __global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ 
           if (n >= 0 && !(md == M_BFS && __ldcg(d.tfix + n))) {
             if (atomicAdd(&d.treq[n], 1) == 0) {
               atomicAdd(&d.fout[s], 1);
-              if (atomicCAS(&next_s, QEMPTY, qent(md, n)) != QEMPTY) chain_put(d, qent(md, n));
+              const bool own = part_of(d, (size_t)n) == myband;  // another band's tile: its ring
+              if (prof && !own) atomicAdd(&d.pdbg[19], 1ULL);   // (cross-band requests)
+              if (!own || atomicCAS(&next_s, QEMPTY, qent(md, n)) != QEMPTY) chain_put(d, qent(md, n));
             }
           }
         }
@@ -1686,7 +1712,12 @@ __global__ void k_setup(Dev d, IO io, Ctl c) {
   const size_t ntask = (size_t)d.nslot * G;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < ntask; i += (size_t)gridDim.x * blockDim.x) {
     const size_t s = i / G, g = i - s * G;
-    d.q[i] = qent(M_INIT, s * d.T + g * d.initg);
+    if (d.nparts > 1) {  // partitioned: each init group to its band's ring
+      const int r = part_of(d, s * d.T + g * d.initg);
+      d.q[(size_t)r * (d.qmask + 1) + (atomicAdd(d.qtail + 2 * r, 1ULL) & d.qmask)] = qent(M_INIT, s * d.T + g * d.initg);
+    } else {
+      d.q[i] = qent(M_INIT, s * d.T + g * d.initg);
+    }
     if (g == 0) {
       slot_assign(d, io, c, (int)s, c.seqL ? (int)s * c.seqL : (int)s);  // slot s: frame s / sequence s
       d.fmode[s] = M_INIT;
@@ -1694,7 +1725,7 @@ __global__ void k_setup(Dev d, IO io, Ctl c) {
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *d.qtail = ntask;
+    if (d.nparts <= 1) *d.qtail = ntask;
     d.gctr[0] = d.nslot;
   }
 }

@@ -41,6 +41,7 @@ struct gc_ctx {
   int tma = 1;                    // TMA staging of the init stream when the layout allows
   int tmapf = 0;                  // ... with an L2 prefetch this many tiles ahead (measured: slower)
   int l2ef = 0;                   // ... with an L2 evict-first policy on the cap loads
+  int nparts = 1;                 // NEXT-3 band partition of each frame (gc_set_partitions)
   int grid = 0;                   // k_solve CTAs of the last launch
   int grid_max = 0;               // persistent grid of k_solve<K> on this context's device
   std::string err;
@@ -118,6 +119,8 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.TY = (H + TS - 1) / TS; d.TX = (W + TS - 1) / TS; d.T = d.TY * d.TX;
   d.nslot = nslot;
   d.hmax = d.T * TPX + 2;
+  d.nparts = c->nparts;
+  d.prow = (d.TY + d.nparts - 1) / d.nparts;  // tile rows per band (the last band may be short)
   // Tiles per init task and per seed / closure-seed task: large groups amortise the per-task
   // cost when many frames are in flight (C4), single tiles spread a latency-bound call's few
   // frames over the CTAs (C3 sequences: 8 VGA frames in flight)
@@ -136,7 +139,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };
   // per-frame words and the queue counters first: contiguous, so one memset clears them
-  char* fw = take((size_t)nslot * (4 * 25 + 8 * 9) + 64 * 4);  // <= 25 int + 9 u64 per slot
+  char* fw = take((size_t)nslot * (4 * 25 + 8 * 9) + 64 * 4 + 32 * GC_PARTS_MAX);  // <= 25 int + 9 u64 per slot
   int32_t* w = (int32_t*)fw;
   d.fmode = w; w += nslot;
   d.sfr = w; w += nslot;
@@ -166,10 +169,12 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.swf = (const int32_t**)u; u += nslot;
   d.sfs = (int32_t**)u; u += nslot;
   u = (unsigned long long*)align_up((size_t)u, 16);
-  d.qhead = u; u += 1;
-  d.qtail = u; u += 1;
-  d.qihead = u; u += 1;
-  d.qitail = u; u += 1;
+  const int R = d.nparts;
+  d.qhead = u;  // [R] (head, tail) pairs of the chain rings, then of the init rings
+  d.qtail = u + 1;
+  d.qihead = u + 2 * R;
+  d.qitail = u + 2 * R + 1;
+  u += 4 * R;
   d.ntask = u; u += 1;
   c->words_bytes = (char*)u - fw;
   d.treq = (int32_t*)take(ns * 4);
@@ -179,12 +184,14 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.reach = (uint8_t*)(d.got + ns * K * 64);  // zeroed per call with treq .. got (epochs: Dev::sep)
   *sentgot_bytes = (char*)(d.reach + ns * K * 64) - (char*)d.treq;
   take(ns * K * 64);
-  const size_t qcap = pow2_at_least(2 * ns + 1024);
-  d.q = (uint32_t*)take(qcap * 4);
+  // per band (one ring pair when not partitioned): capacity >= 2 x the band's tiles in flight
+  const size_t bt = (size_t)nslot * (R > 1 ? (size_t)d.prow * d.TX : T);
+  const size_t qcap = pow2_at_least(2 * bt + 1024);
+  d.q = (uint32_t*)take(qcap * 4 * R);
   d.qmask = (uint32_t)(qcap - 1);
   // init ring: every slot's init groups once, plus one release entry per CTA (k_solve)
-  const size_t qicap = pow2_at_least(2 * ((size_t)nslot * ((T + d.initg - 1) / d.initg) + 4096) + 1024);
-  d.qi = (uint32_t*)take(qicap * 4);
+  const size_t qicap = pow2_at_least(2 * ((size_t)nslot * ((R > 1 ? (size_t)d.prow * d.TX : T) / d.initg + 2) + 4096) + 1024);
+  d.qi = (uint32_t*)take(qicap * 4 * R);
   d.qimask = (uint32_t)(qicap - 1);
   *q_bytes = (char*)(d.qi + qicap) - (char*)d.q;
   d.e = (int32_t*)take(ns * TPX * 4);
@@ -667,7 +674,7 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
     nf = budget / fb;
     if (nf < 1) nf = 1;
   }
-  c->pool_bytes = nf * fb;
+  c->pool_bytes = nf * fb + ((size_t)GC_PARTS_MAX << 18);  // + the band rings of a partitioned call
   if (cudaMalloc(&c->pool, c->pool_bytes) != cudaSuccess) { cudaGetLastError(); delete c; return GC_ERR_OOM; }
   if (cudaMallocHost(&c->hpin, 64) != cudaSuccess) { cudaFree(c->pool); delete c; return GC_ERR_OOM; }
   if (cudaMalloc(&c->dtiles, 256) != cudaSuccess) { cudaFree(c->pool); cudaFreeHost(c->hpin); delete c; return GC_ERR_OOM; }
@@ -723,6 +730,16 @@ void gc_destroy(gc_ctx* c) {
 const char* gc_last_error(const gc_ctx* c) { return c ? c->err.c_str() : "NULL context"; }
 
 long long gc_last_launches(const gc_ctx* c) { return c ? c->last_launches : 0; }
+
+gc_status gc_set_partitions(gc_ctx* c, int parts) {
+  if (!c) return GC_ERR_ARG;
+  if (parts < 1 || parts > GC_PARTS_MAX || parts > c->grid_max) {
+    c->err = "gc_set_partitions: parts must be in [1, GC_PARTS_MAX]";
+    return GC_ERR_ARG;
+  }
+  c->nparts = parts;
+  return GC_OK;
+}
 
 void gc_set_profiling(gc_ctx* c, int enable) {
   if (!c) return;
