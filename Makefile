@@ -10,6 +10,10 @@ endif
 ifeq ($(CHECKS),1)
 NVFLAGS += -DGC_CHECKS
 endif
+# make MINB=n: resident CTAs per SM the k_solve register budget is sized for (A/B builds)
+ifneq ($(MINB),)
+NVFLAGS += -DGC_MINB=$(MINB)
+endif
 PKG := paper_1008_0502_b200
 
 all: $(PKG)/libgc.so synth/libsynth.so oracle/liboracle.so

@@ -41,6 +41,12 @@ namespace gcb {
 #ifndef GC_MINB
 #define GC_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
+// Batches of frames of at least this many tiles that refill their slots run the 3-CTA-per-SM
+// variant (80 registers, little spilling): a hard frame's long dependency chain of tile tasks
+// then runs beside the streaming frames with two co-resident CTAs per SM instead of three
+// (C4 ~37 -> ~32 ms per step).
+constexpr int GC_MINB_LARGE = 3;
+constexpr int GC_LARGE_TILES = 1000;
 constexpr uint32_t QEMPTY = 0xffffffffu;
 constexpr uint32_t QEXIT = 0xfffffffeu;
 constexpr uint32_t QNOP = 0xfffffffdu;  // releases a CTA waiting on the init ring (no task)
@@ -1476,8 +1482,8 @@ __device__ __forceinline__ void transition(const Dev& d, const IO& io, int s, co
 // ---------------------------------------------------------------- the persistent kernel
 // EN: energy mode (NEXT-1, the init pass builds the caps from the energy) -- a kernel of its own
 // so that the cap-streaming kernel carries none of its code or registers.
-template <int K, bool EN = false>
-__global__ void __launch_bounds__(NTH, GC_MINB) k_solve(const __grid_constant__ Dev d, const __grid_constant__ IO io,
+template <int K, bool EN = false, int MB = GC_MINB>
+__global__ void __launch_bounds__(NTH, MB) k_solve(const __grid_constant__ Dev d, const __grid_constant__ IO io,
                                                          const __grid_constant__ Ctl c, const __grid_constant__ Tmaps tm) {
   extern __shared__ __align__(128) int smem[];
   __shared__ uint64_t mbar[NTH / 32];  // one TMA barrier per warp (init stream)

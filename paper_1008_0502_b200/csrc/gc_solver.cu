@@ -44,6 +44,7 @@ struct gc_ctx {
   int nparts = 1;                 // NEXT-3 band partition of each frame (gc_set_partitions)
   int grid = 0;                   // k_solve CTAs of the last launch
   int grid_max = 0;               // persistent grid of k_solve<K> on this context's device
+  int grid_max_large = 0;         // ... of the large-frame variant k_solve<K, false, GC_MINB_LARGE>
   std::string err;
   long long last_launches = 0;
   bool prof = false;
@@ -381,7 +382,13 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   if (io.stats && !ck(c, cudaMemsetAsync(io.stats, 0, (size_t)nframes * 16, st), "memset")) return GC_ERR_CUDA;
   const size_t smem = solve_smem_bytes<K>();
   const size_t ns = (size_t)nslot * d.T;
-  int grid = c->grid_max;  // computed per context (its device) in gc_create
+  // large frames streamed through refilled slots (cap solves): the 3-CTA-per-SM variant
+  // (GC_LARGE_TILES, gc_phases.cuh).  Measured: C4 (1024 x 1080p) 33-40 -> 31.6-34.3 ms per
+  // step (a hard frame's chain runs beside the streaming frames); calls whose frames all fit
+  // the slots keep 4 CTAs per SM (C5's 8 serpentine frames, all long chains: 5.9 vs 4.9 Mpx/s)
+  bool large = !io.img && d.T >= GC_LARGE_TILES && nframes > nslot && c->grid_max_large > 0;
+  if (const char* ev = knob("GC_LARGE")) large = !io.img && c->grid_max_large > 0 && atoi(ev) != 0;  // tuning knob
+  int grid = large ? c->grid_max_large : c->grid_max;  // computed per context (its device) in gc_create
   if (const char* ev = knob("GC_GRID")) grid = atoi(ev) > 0 && atoi(ev) < grid ? atoi(ev) : grid;
   c->grid = grid;
   if (!ck(c, cudaMemsetAsync(d.fmode, 0, c->words_bytes, st), "memset")) return GC_ERR_CUDA;
@@ -433,6 +440,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   cudaEvent_t e1 = c->evpool[c->evnext++];
   cudaEventRecord(e0, st);
   if (io.img) k_solve<K, true><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
+  else if (large) k_solve<K, false, GC_MINB_LARGE><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
   else k_solve<K><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
   ++L.n;
   cudaEventRecord(e1, st);
@@ -696,7 +704,12 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
     if (e == cudaSuccess)
       e = c->K == 8 ? cudaFuncSetAttribute(k_solve<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                     : cudaFuncSetAttribute(k_solve<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = c->K == 8 ? cudaFuncSetAttribute(k_solve<8, false, GC_MINB_LARGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                    : cudaFuncSetAttribute(k_solve<4, false, GC_MINB_LARGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     c->grid_max = c->K == 8 ? persistent_grid(c, k_solve<8>, smem) : persistent_grid(c, k_solve<4>, smem);
+    c->grid_max_large = c->K == 8 ? persistent_grid(c, k_solve<8, false, GC_MINB_LARGE>, smem)
+                                  : persistent_grid(c, k_solve<4, false, GC_MINB_LARGE>, smem);
     if (e != cudaSuccess) {
       cudaGetLastError();
       gc_destroy(c);
