@@ -520,8 +520,10 @@ def run_saliency(args, cfg):
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    launches = 0
     for _ in range(args.steps):
         g.saliency(cur, prev)
+        launches += g.launches()
     e1.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -551,7 +553,7 @@ def run_saliency(args, cfg):
                             "bytes_rule": f"{bpx} B/px compulsory (two RGB frames in, the prior code out); "
                                           "the pyramids and feature maps stay in HBM / L2", "traffic": None,
                             "peak_source": peak_src},
-               "cpu_baseline": cpu, "gpu_launches": None, "clocks": clocks}
+               "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(res), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -17,6 +17,10 @@
 
 #include "gc.h"
 
+// gc_solver.cu: the context's grow-only device scratch (library-internal)
+extern "C" void* gc_ctx_scratch(gc_ctx* c, int i, size_t bytes);
+extern "C" void gc_ctx_set_launches(gc_ctx* c, long long n);
+
 namespace {
 
 constexpr int NLEV = 9;      // pyramid levels 0..8
@@ -277,10 +281,10 @@ gc_status gc_saliency(gc_ctx* ctx, const gc_saliency_batch* b, void* stream) {
   const size_t nc = (size_t)n * hl[2] * wl[2];  // largest feature map
   // scratch: 4 feature pyramids + 4 orientation pyramids, feature map + temps, class sums
   const size_t fl = 8 * pyr + 3 * nc + 6 * n4 + 16;
-  float* buf = nullptr;
-  void* red = nullptr;
-  if (cudaMalloc(&buf, fl * sizeof(float)) != cudaSuccess) { cudaGetLastError(); return GC_ERR_OOM; }
-  if (cudaMalloc(&red, (size_t)n * 32) != cudaSuccess) { cudaFree(buf); cudaGetLastError(); return GC_ERR_OOM; }
+  // the context's grow-only scratch (no allocation per call once it has grown)
+  float* buf = static_cast<float*>(gc_ctx_scratch(ctx, 0, fl * sizeof(float)));
+  void* red = gc_ctx_scratch(ctx, 1, (size_t)n * 32);
+  if (!buf || !red) return GC_ERR_OOM;
   float* P[8];
   for (int c = 0; c < 8; ++c) P[c] = buf + c * pyr;  // I, RG, BY, M, O0..O3
   float* fm = buf + 8 * pyr;   // feature map
@@ -295,14 +299,15 @@ gc_status gc_saliency(gc_ctx* ctx, const gc_saliency_batch* b, void* stream) {
   unsigned long long* cnt = (unsigned long long*)(mx + n);  // 8n bytes in: aligned
   unsigned long long* sum = cnt + n;
   const size_t HW = (size_t)H * W;
-  k_features<<<nblk(n * HW), 256, 0, st>>>(n, (int)HW, b->image, b->prev, P[0], P[1], P[2], P[3]);
+  long long nl = 0;  // kernel launches of this call (gc_last_launches)
+  k_features<<<nblk(n * HW), 256, 0, st>>>(n, (int)HW, b->image, b->prev, P[0], P[1], P[2], P[3]); ++nl;
   for (int c = 0; c < 4; ++c)
     for (int l = 1; l < NLEV; ++l)
       k_down<<<nblk((size_t)n * hl[l] * wl[l]), 256, 0, st>>>(n, hl[l - 1], wl[l - 1], hl[l], wl[l], P[c] + off[l - 1],
-                                                              P[c] + off[l]);
+                                                              P[c] + off[l]); ++nl;
   for (int t = 0; t < NORI; ++t)
     for (int l = 2; l < NLEV; ++l)
-      k_gabor<<<nblk((size_t)n * hl[l] * wl[l]), 256, 0, st>>>(n, hl[l], wl[l], t, P[0] + off[l], P[4 + t] + off[l]);
+      k_gabor<<<nblk((size_t)n * hl[l] * wl[l]), 256, 0, st>>>(n, hl[l], wl[l], t, P[0] + off[l], P[4 + t] + off[l]); ++nl;
   cudaMemsetAsync(cls[0], 0, 4 * n4 * sizeof(float), st);
   // N(.) of a map at level l (in place), then added into `dst` at level 4
   auto normalize = [&](float* v, int l) {
@@ -310,20 +315,20 @@ gc_status gc_saliency(gc_ctx* ctx, const gc_saliency_batch* b, void* stream) {
     cudaMemsetAsync(mn, 0xff, (size_t)n * 4, st);  // > +inf bits: every value lowers it
     cudaMemsetAsync(mx, 0, (size_t)n * 4, st);
     cudaMemsetAsync(cnt, 0, (size_t)n * 16, st);
-    k_minmax<<<dim3(64, n), 256, 0, st>>>(n, (int)hw, v, mn, mx);
-    k_rescale<<<nblk(n * hw), 256, 0, st>>>(n, (int)hw, v, mn, mx);
-    k_rowmax<<<nblk(n * hw), 256, 0, st>>>(n, hl[l], wl[l], v, tmp);
-    k_colmax_localmax<<<nblk(n * hw), 256, 0, st>>>(n, hl[l], wl[l], v, tmp, cnt, sum);
-    k_nscale<<<nblk(n * hw), 256, 0, st>>>(n, (int)hw, v, cnt, sum, mx, mn);
+    k_minmax<<<dim3(64, n), 256, 0, st>>>(n, (int)hw, v, mn, mx); ++nl;
+    k_rescale<<<nblk(n * hw), 256, 0, st>>>(n, (int)hw, v, mn, mx); ++nl;
+    k_rowmax<<<nblk(n * hw), 256, 0, st>>>(n, hl[l], wl[l], v, tmp); ++nl;
+    k_colmax_localmax<<<nblk(n * hw), 256, 0, st>>>(n, hl[l], wl[l], v, tmp, cnt, sum); ++nl;
+    k_nscale<<<nblk(n * hw), 256, 0, st>>>(n, (int)hw, v, cnt, sum, mx, mn); ++nl;
   };
   auto add_at4 = [&](const float* v, int l, float* dst) {
     const float* cur = v;
     for (int k = l; k < 4; ++k) {  // blur-decimate down to level 4
       float* o = (k % 2 == l % 2) ? tmp : tmp2;
-      k_down<<<nblk((size_t)n * hl[k + 1] * wl[k + 1]), 256, 0, st>>>(n, hl[k], wl[k], hl[k + 1], wl[k + 1], cur, o);
+      k_down<<<nblk((size_t)n * hl[k + 1] * wl[k + 1]), 256, 0, st>>>(n, hl[k], wl[k], hl[k + 1], wl[k + 1], cur, o); ++nl;
       cur = o;
     }
-    k_accum<<<nblk(n4), 256, 0, st>>>(n4, cur, dst);
+    k_accum<<<nblk(n4), 256, 0, st>>>(n4, cur, dst); ++nl;
   };
   // classes: 0 intensity, 1 colour (RG and BY), 2 orientation, 3 motion
   const int chan_class[8] = {0, 1, 1, 3, 2, 2, 2, 2};
@@ -337,24 +342,23 @@ gc_status gc_saliency(gc_ctx* ctx, const gc_saliency_batch* b, void* stream) {
       for (int di = 0; di < 2; ++di) {
         const int c = CENTERS[ci], s = c + DELTAS[di];
         k_cs<<<nblk((size_t)n * hl[c] * wl[c]), 256, 0, st>>>(n, hl[c], wl[c], hl[s], wl[s], P[ch] + off[c],
-                                                              P[ch] + off[s], fm);
+                                                              P[ch] + off[s], fm); ++nl;
         normalize(fm, c);
         add_at4(fm, c, dst);
       }
     if (ch >= 4) {
       normalize(acc, 4);
-      k_accum<<<nblk(n4), 256, 0, st>>>(n4, acc, cls[2]);
+      k_accum<<<nblk(n4), 256, 0, st>>>(n4, acc, cls[2]); ++nl;
     }
   }
   for (int c = 0; c < 4; ++c) normalize(cls[c], 4);
-  k_final<<<nblk(n4), 256, 0, st>>>(n4, cls[0], cls[1], cls[2], cls[3], sal);
+  k_final<<<nblk(n4), 256, 0, st>>>(n4, cls[0], cls[1], cls[2], cls[3], sal); ++nl;
   normalize(sal, 4);  // rescaled to [0, 1] (and the same N(.) as every stage)
   if (b->sal_out) cudaMemcpyAsync(b->sal_out, sal, n4 * sizeof(float), cudaMemcpyDeviceToDevice, st);
-  if (b->q_out) k_upcode<<<nblk((size_t)n * HW), 256, 0, st>>>(n, H, W, hl[4], wl[4], sal, b->q_out);
+  if (b->q_out) k_upcode<<<nblk((size_t)n * HW), 256, 0, st>>>(n, H, W, hl[4], wl[4], sal, b->q_out); ++nl;
   const cudaError_t e = cudaGetLastError();
   const cudaError_t e2 = cudaStreamSynchronize(st);
-  cudaFree(buf);
-  cudaFree(red);
+  gc_ctx_set_launches(ctx, nl);
   return (e != cudaSuccess || e2 != cudaSuccess) ? GC_ERR_CUDA : GC_OK;
 }
 

@@ -72,7 +72,23 @@ struct gc_ctx {
   int32_t* capbuf = nullptr;  // energy mode: the slots' cap buffers
   size_t capbuf_bytes = 0;
   int32_t* elut = nullptr;    // energy mode: n-link LUT [2][256]
+  void* scratch[2] = {nullptr, nullptr};  // gc_saliency's pyramids / reductions (grow-only)
+  size_t scratch_bytes[2] = {0, 0};
 };
+
+// Grow-only device scratch of the context for the other translation units of the library
+// (gc_saliency.cu); not part of gc.h.  NULL if the allocation fails.
+extern "C" __attribute__((visibility("hidden"))) void* gc_ctx_scratch(gc_ctx* c, int i, size_t bytes) {
+  if (bytes > c->scratch_bytes[i]) {
+    if (c->scratch[i]) cudaFree(c->scratch[i]);
+    c->scratch[i] = nullptr;
+    c->scratch_bytes[i] = 0;
+    if (cudaMalloc(&c->scratch[i], bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    c->scratch_bytes[i] = bytes;
+  }
+  return c->scratch[i];
+}
+extern "C" __attribute__((visibility("hidden"))) void gc_ctx_set_launches(gc_ctx* c, long long n) { c->last_launches = n; }
 
 namespace {
 
@@ -733,6 +749,8 @@ void gc_destroy(gc_ctx* c) {
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->habort) cudaFreeHost(c->habort);
   if (c->dtiles) cudaFree(c->dtiles);
+  for (int i = 0; i < 2; ++i)
+    if (c->scratch[i]) cudaFree(c->scratch[i]);
   if (c->trace) cudaFree(c->trace);
   if (c->fbuf) cudaFree(c->fbuf);
   if (c->capbuf) cudaFree(c->capbuf);
