@@ -14,7 +14,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 H, W = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (2160, 3840)
 synth.set_serpentine_params(lane=64, big=1 << 20)
 cs, ct, nb = synth.gen_torch("serpentine", synth.BASE_SEED + 4, 0, n, H, W, 4)
-g = gc.GridCut(neighborhood=4, max_h=H, max_w=W)
+g = gc.GridCut(neighborhood=4, max_h=H, max_w=W, rounds_per_launch=int(os.environ.get("C5_ROUNDS", "0")))
 g.set_profiling(True)
 g.profile(reset=True)
 g.kernel_ms(reset=True)
