@@ -1,5 +1,6 @@
-python bench.py --config c3 --warm --no-cpu-baseline --no-e2e --steps 3 --warmup 3 > gpurun_out/bench_c3w_t5.log 2>&1; tail -1 gpurun_out/bench_c3w_t5.log | cut -c1-200; grep -o '"cold_same_schedule[^}]*}' gpurun_out/bench_c3w_t5.log
-python bench.py --config c3 --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/bench_c3_t5.log 2>&1; python tools/tsum.py c3_t5 2>/dev/null | head -1
-python bench.py --config c2 --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/bench_c2_t5.log 2>&1; python tools/tsum.py c2_t5 2>/dev/null | head -1
-python bench.py --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/bench_c4_t5.log 2>&1; python tools/tsum.py c4_t5 2>/dev/null | head -1
-python -m pytest tests -m gpu -x -q > gpurun_out/pytest_t5.log 2>&1; tail -3 gpurun_out/pytest_t5.log
+rm -f paper_1008_0502_b200/libgc.so; make -s DEV=1 all > /dev/null 2>&1
+for v in 0 1; do echo "LREL=$v c5 $(GC_LRELABEL=$v timeout 600 python tools/c5_probe.py 1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["kernel_ms"], d["stats"][0][:3])')"; done
+for v in 0 1; do echo "LREL=$v f0 $(GC_LRELABEL=$v timeout 600 python tools/f0_counters.py 0 | cut -c1-120)"; done
+GC_LRELABEL=1 timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+bash tools/ab_knob.sh GC_LRELABEL "0 1" 2
+bash tools/ab_rest.sh GC_LRELABEL "0 1" 1

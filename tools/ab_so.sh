@@ -19,7 +19,7 @@ for _ in range(4):
 print(json.dumps(ms))
 PY
 for r in $(seq $REPS); do
-  for v in A C B; do
+  for v in A B; do
     cp $P/libgc_$v.so $P/libgc.so
     echo "$v rest $(timeout 300 python /tmp/abso.py 1 2>&1 | tail -1)  all $(timeout 300 python /tmp/abso.py 0 2>&1 | tail -1)"
   done
