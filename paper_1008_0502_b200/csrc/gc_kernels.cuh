@@ -836,6 +836,26 @@ __device__ __forceinline__ void tile_init_regs(const Dev& d, const IO& io, size_
   int fwv[K / 2][4];  // exported forward flows of the 4 pixels (EXPORT)
   // 16-byte export stores: the 4 pixels in the frame and the rows aligned
   const bool ev4 = EXPORT && K == 4 && y < H && x0 + 3 < W && (((uintptr_t)(P.fs + o0)) & 15) == 0 && ((plane & 3) == 0);
+  if (!WARM && !EXPORT && inner) {
+    // cold tile away from the frame border (most tiles): every arc in the grid, no clamp
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int f = 0, ca = a[i] | b[i];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ca |= c[k][i];
+        f |= (c[k][i] > 0) << k;
+      }
+      acc |= ca;
+      const int ev = a[i] - b[i];  // a1: pre-cancel min(cs,ct) straight s -> v -> t
+      sct += b[i];
+      f |= (ev > 0 ? FL_POS : 0) | (ev < 0 ? FL_NEG : 0);
+      neg += ev < 0 ? -(long long)ev : 0;
+      uni &= ev < 0;
+      src &= ev > 0;
+      fl4[i] = f;
+    }
+  } else
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int x = x0 + i;
