@@ -143,7 +143,8 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   // frames over the CTAs (C3 sequences: 8 VGA frames in flight)
   {
     const long long inflight = (long long)nslot * d.T, ctas = c->grid_max > 0 ? c->grid_max : 592;
-    long long g = d.T / 32;
+    long long g = d.T / 20;  // (T / 32 capped QVGA batches at 2 tiles per task: C2 47-49 -> 53 Gpx/s
+                             //  at 4-8; VGA batches: 8-16 best, 20 slower)
     const long long g2 = inflight / (4 * ctas);
     if (g2 < g) g = g2;
     d.initg = (int)(g < 1 ? 1 : (g > 32 ? 32 : g));
