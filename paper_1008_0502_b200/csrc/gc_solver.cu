@@ -152,7 +152,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
     d.bulkg = b >= 8 ? 8 : (b >= 4 ? 4 : (b >= 2 ? 2 : 1));
   }
   if (const char* ev = knob("GC_INITG")) d.initg = atoi(ev) > 0 && atoi(ev) <= INIT_GMAX ? atoi(ev) : d.initg;
-  if (const char* ev = knob("GC_BULKG")) d.bulkg = atoi(ev) == 1 || atoi(ev) == 2 || atoi(ev) == 4 || atoi(ev) == 8 ? atoi(ev) : d.bulkg;
+  if (const char* ev = knob("GC_BULKG")) d.bulkg = atoi(ev) == 1 || atoi(ev) == 2 || atoi(ev) == 4 || atoi(ev) == 8 || atoi(ev) == 16 ? atoi(ev) : d.bulkg;
   const size_t T = d.T, ns = (size_t)nslot * T, K = c->K;
   char* p = c->pool;
   auto take = [&](size_t bytes) { char* q = p; p += align_up(bytes, 256); return q; };

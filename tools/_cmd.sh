@@ -1,1 +1,2 @@
-for i in 1 2; do for c in c2 c3; do python bench.py --config $c --no-cpu-baseline --no-e2e --steps 5 --warmup 3 > gpurun_out/bench_${c}_ig$i.log 2>&1; echo "$c $(python tools/tsum.py ${c}_ig$i 2>/dev/null | head -1)"; done; done
+bash tools/ab_knob.sh GC_BULKG "2 4 8" 2 "--config c2" 2>&1 | grep GC_BULKG
+bash tools/ab_rest.sh GC_BULKG "4 8 16" 2 2>&1 | grep GC_BULKG
