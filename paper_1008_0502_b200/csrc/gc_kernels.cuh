@@ -111,6 +111,7 @@ struct Dev {
   int32_t* sep;     // [nslot] closure attempts of the slot in this call (all its frames): the
                     //         reach-mark epoch is sep % 255 + 1; the slot's marks are cleared
                     //         when it wraps, so a mark never aliases an earlier attempt's
+  int32_t* fflag;   // [nslot] a task of the running phase flagged a tile for the next one
   int32_t* fstat;   // [nslot][4] push tasks, global relabels, BFS relax tasks, -
   unsigned long long* frel;   // [nslot] relabel operations in the current push phase
   unsigned long long* sumct;  // [nslot]

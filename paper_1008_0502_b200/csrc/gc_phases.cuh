@@ -176,7 +176,10 @@ __device__ __forceinline__ void flag_sides(const Dev& d, size_t gt, int bits, in
   const int t = threadIdx.x;
   if (t < 8 && ((bits >> t) & 1) && !(t >= 4 && K == 4)) {
     const long long n = side_tile(d, gt, t);
-    if (n >= 0) d.flag[n] = 1;
+    if (n >= 0) {
+      d.flag[n] = 1;
+      d.fflag[(unsigned)gt / (unsigned)d.T] = 1;  // the phase has a follow-up task set
+    }
   }
 }
 
@@ -1122,9 +1125,9 @@ __device__ __forceinline__ void transition(const Dev& d, const IO& io, int s, co
     if (t == 0) {
       const int a0 = __ldcg(d.fmode + s), a1 = __ldcg(d.ferr + s), a2 = __ldcg(d.cep + s), a3 = __ldcg(d.cfail + s);
       const int a4 = __ldcg(d.fbnd + s), a5 = __ldcg(d.fbe + s), a6 = __ldcg(d.fph + s), a7 = __ldcg(d.sep + s);
-      const int a8 = __ldcg(d.fstat + s * 4 + 1), a9 = __ldcg(d.sfr + s);
+      const int a8 = __ldcg(d.fstat + s * 4 + 1), a9 = __ldcg(d.sfr + s), a10 = __ldcg(d.fflag + s);
       sw[0] = a0; sw[1] = a1; sw[2] = a2; sw[3] = a3; sw[4] = a4;
-      sw[5] = a5; sw[6] = a6; sw[7] = a7; sw[8] = a8; sw[9] = a9;
+      sw[5] = a5; sw[6] = a6; sw[7] = a7; sw[8] = a8; sw[9] = a9; sw[10] = a10;
     }
     __syncthreads();
     const int md = sw[0];
@@ -1209,10 +1212,10 @@ __device__ __forceinline__ void transition(const Dev& d, const IO& io, int s, co
           d.cep[s] = sw[2];
           nm = M_SEED;
           kind = SET_SEED;
-        } else if (md == M_CSEED) {
+        } else if (md == M_CSEED && sw[10]) {
           nm = M_CLOS;
           kind = SET_FLAG;
-        } else {  // certified: the mask is written
+        } else {  // certified (no closure relax needed, or done): the mask is written
           d.cfail[s] = 0;
           finished = true;  // (flow_state_out is written by the init pass and the closure seeds)
         }
@@ -1266,6 +1269,7 @@ __device__ __forceinline__ void transition(const Dev& d, const IO& io, int s, co
       }
       bc[1] = 0;
       if (nm == M_CSEED) {  // a new closure attempt: the next reach-mark epoch of the slot
+        d.fflag[s] = 0;     // (set again by a closure seed that flags a tile for closure relax)
         const int se = sw[7] + 1;
         d.sep[s] = se;
         bc[1] = (se % 255) == 0;  // wrapped: clear the slot's marks first

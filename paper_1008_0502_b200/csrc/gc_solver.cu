@@ -174,6 +174,7 @@ Dev carve(gc_ctx* c, int nslot, int H, int W, size_t* sentgot_bytes, size_t* q_b
   d.fcap = w; w += nslot;
   d.fbnd = w; w += nslot;
   d.sep = w; w += nslot;
+  d.fflag = w; w += nslot;
   d.fstat = w; w += 4 * nslot;
   d.gctr = w; w += 4;
   d.done = w; w += 4;
