@@ -67,6 +67,11 @@ struct gc_ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr};       // staging buffer b filled
   cudaEvent_t ev_free[2] = {nullptr, nullptr};     // staging buffer b solved and read back
   size_t words_bytes = 0;
+  // the border-flow counters (sent, got) of the last call's layout are balanced (every frame
+  // finished, so all its border flow was absorbed: sent == got, the invariant a refilled slot
+  // already relies on); a call with the same layout then skips zeroing them
+  bool sg_clean = false;
+  int sg_key[5] = {0, 0, 0, 0, 0};
   int32_t* fbuf = nullptr;  // sequence mode: ping-pong flow buffers of the slots
   size_t fbuf_bytes = 0;
   int32_t* capbuf = nullptr;  // energy mode: the slots' cap buffers
@@ -410,7 +415,19 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   if (const char* ev = knob("GC_GRID")) grid = atoi(ev) > 0 && atoi(ev) < grid ? atoi(ev) : grid;
   c->grid = grid;
   if (!ck(c, cudaMemsetAsync(d.fmode, 0, c->words_bytes, st), "memset")) return GC_ERR_CUDA;
-  if (!ck(c, cudaMemsetAsync(d.treq, 0, sg_bytes, st), "memset")) return GC_ERR_CUDA;
+  {
+    const int key[5] = {nslot, H, W, K, d.nparts};
+    const bool reuse = c->sg_clean && memcmp(key, c->sg_key, sizeof(key)) == 0;
+    c->sg_clean = false;  // until this call completes
+    memcpy(c->sg_key, key, sizeof(key));
+    if (!reuse) {
+      if (!ck(c, cudaMemsetAsync(d.treq, 0, sg_bytes, st), "memset")) return GC_ERR_CUDA;
+    } else {  // requests and flags, and the reach marks (their epochs restart per call)
+      if (!ck(c, cudaMemsetAsync(d.treq, 0, (char*)d.sent - (char*)d.treq, st), "memset")) return GC_ERR_CUDA;
+      if (!ck(c, cudaMemsetAsync(d.reach, 0, (char*)d.treq + sg_bytes - (char*)d.reach, st), "memset"))
+        return GC_ERR_CUDA;
+    }
+  }
   if (!ck(c, cudaMemsetAsync(d.q, 0xff, q_bytes, st), "memset")) return GC_ERR_CUDA;
   Ctl ctl;
   ctl.relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
@@ -509,6 +526,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
     if (*c->habort) c->err = "solve timed out (host watchdog)";
     return GC_ERR_NOCONV;
   }
+  c->sg_clean = true;  // every frame finished: the border-flow counters are balanced
   if (c->hpin[2]) return GC_ERR_RANGE;
   return GC_OK;
 }
