@@ -272,6 +272,29 @@ def test_noconv(torch, gc):
     g.close()
 
 
+def test_same_layout_calls_after_abort(torch, gc):
+    """Calls with the previous call's slot layout reuse its balanced border-flow counters
+    (no zeroing); a call the watchdog stopped leaves them unbalanced, so the next call zeroes
+    them again.  Every solved call stays bit-exact against the oracle."""
+    synth.set_serpentine_params(lane=4, big=1 << 20)
+    try:
+        hard = synth.gen_host("serpentine", 5, 0, 1, 128, 128, 4)
+    finally:
+        synth.set_serpentine_params()
+    g = gc.GridCut(neighborhood=4, max_h=128, max_w=128, max_batch=2, max_launches=3)
+    for seed in (31, 32, 33):  # 3 calls, same layout (2 slots of 128 x 128, refilled)
+        caps = synth.gen_host("blob", seed, 0, 5, 128, 128, 4)
+        F, m = g.solve(*to_dev(torch, *caps))
+        check_against_oracle(*caps, F.cpu().numpy(), m.cpu().numpy())
+    hard2 = tuple(np.concatenate([h, h]) for h in hard)  # 2 frames: the same layout
+    F, m = g.solve(*to_dev(torch, *hard2), allow=(5,))
+    assert g.last_status == 5
+    caps = synth.gen_host("blob", 34, 0, 5, 128, 128, 4)
+    F, m = g.solve(*to_dev(torch, *caps))
+    check_against_oracle(*caps, F.cpu().numpy(), m.cpu().numpy())
+    g.close()
+
+
 def test_two_contexts_interleaved(torch, gc):
     a = gc.GridCut(neighborhood=4, max_h=100, max_w=100)
     b = gc.GridCut(neighborhood=8, max_h=100, max_w=100)
