@@ -278,8 +278,8 @@ gc_status gc_set_partitions(gc_ctx* ctx, int parts);
 const char* gc_last_error(const gc_ctx* ctx);
 
 /* Number of kernel launches the last call issued (for the bench's gpu_launches): a solve
- * issues a setup kernel and one persistent k_solve per chunk of frames (+ k_abort after a
- * watchdog stop); gc_saliency its ~500 stage kernels. */
+ * issues a clear kernel (the call's initial state), a setup kernel and one persistent k_solve
+ * per chunk of frames (+ k_abort after a watchdog stop); gc_saliency its ~440 stage kernels. */
 long long gc_last_launches(const gc_ctx* ctx);
 
 /* Profiling: when enabled, the persistent kernel times every tile task (globaltimer) and

@@ -364,6 +364,34 @@ double now_s() {
 // on the device as frames finish (continuous batching).
 // Sequence mode (seqL > 0, gc_solve_sequences): nframes = seqS x seqL frames, frame t of a
 // sequence solved after frame t-1 in the same slot (warm-started from its flows if seqWarm).
+// The per-call initial state of a solve in one launch instead of one memset per region: up to
+// 8 segments of 32-bit words, each filled with its value (grid-stride).
+struct ClearSeg {
+  uint32_t* p;
+  size_t n;  // words
+  uint32_t v;
+};
+struct ClearList {
+  ClearSeg seg[8];
+  int cnt;
+};
+__global__ void k_clear(const __grid_constant__ ClearList L) {
+  const size_t i0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+  for (int j = 0; j < L.cnt; ++j) {
+    uint32_t* p = L.seg[j].p;
+    const size_t n = L.seg[j].n;
+    const uint32_t v = L.seg[j].v;
+    if ((((uintptr_t)p) & 15) == 0) {  // 16-byte stores for the aligned part
+      uint4* q = reinterpret_cast<uint4*>(p);
+      const uint4 vv = make_uint4(v, v, v, v);
+      for (size_t i = i0; i < n / 4; i += stride) q[i] = vv;
+      for (size_t i = (n / 4) * 4 + i0; i < n; i += stride) p[i] = v;
+    } else {
+      for (size_t i = i0; i < n; i += stride) p[i] = v;
+    }
+  }
+}
+
 template <int K>
 gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaStream_t st, Launcher& L, int seqS = 0,
                       int seqL = 0, int seqWarm = 0, int32_t* caps_out = nullptr) {
@@ -400,9 +428,14 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
     if (caps_out && !ck(c, cudaMemsetAsync(caps_out, 0, (size_t)nframes * (2 + K) * H * W * 4, st), "memset"))
       return GC_ERR_CUDA;  // off-grid entries stay 0
   }
-  // unfinished frames read F = -1 and status 0 until the kernel writes them (k_abort relies on it)
-  if (!ck(c, cudaMemsetAsync(io.flow, 0xff, (size_t)nframes * 8, st), "memset")) return GC_ERR_CUDA;
-  if (io.stats && !ck(c, cudaMemsetAsync(io.stats, 0, (size_t)nframes * 16, st), "memset")) return GC_ERR_CUDA;
+  // the call's initial state, one k_clear launch: unfinished frames read F = -1 and status 0
+  // until the kernel writes them (k_abort relies on it); slot words; requests, flags, reach
+  // marks (and the border-flow counters unless balanced, below); the rings (empty = all ones)
+  ClearList cl;
+  memset(&cl, 0, sizeof(cl));
+  auto seg = [&](void* p, size_t bytes, uint32_t v) { cl.seg[cl.cnt++] = ClearSeg{(uint32_t*)p, bytes / 4, v}; };
+  seg(io.flow, (size_t)nframes * 8, 0xffffffffu);
+  if (io.stats) seg(io.stats, (size_t)nframes * 16, 0u);
   const size_t smem = solve_smem_bytes<K>();
   const size_t ns = (size_t)nslot * d.T;
   // large frames streamed through refilled slots (cap solves): the 3-CTA-per-SM variant
@@ -414,21 +447,28 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   int grid = large ? c->grid_max_large : c->grid_max;  // computed per context (its device) in gc_create
   if (const char* ev = knob("GC_GRID")) grid = atoi(ev) > 0 && atoi(ev) < grid ? atoi(ev) : grid;
   c->grid = grid;
-  if (!ck(c, cudaMemsetAsync(d.fmode, 0, c->words_bytes, st), "memset")) return GC_ERR_CUDA;
+  seg(d.fmode, c->words_bytes, 0u);
   {
     const int key[5] = {nslot, H, W, K, d.nparts};
     const bool reuse = c->sg_clean && memcmp(key, c->sg_key, sizeof(key)) == 0;
     c->sg_clean = false;  // until this call completes
     memcpy(c->sg_key, key, sizeof(key));
     if (!reuse) {
-      if (!ck(c, cudaMemsetAsync(d.treq, 0, sg_bytes, st), "memset")) return GC_ERR_CUDA;
+      seg(d.treq, sg_bytes, 0u);
     } else {  // requests and flags, and the reach marks (their epochs restart per call)
-      if (!ck(c, cudaMemsetAsync(d.treq, 0, (char*)d.sent - (char*)d.treq, st), "memset")) return GC_ERR_CUDA;
-      if (!ck(c, cudaMemsetAsync(d.reach, 0, (char*)d.treq + sg_bytes - (char*)d.reach, st), "memset"))
-        return GC_ERR_CUDA;
+      seg(d.treq, (char*)d.sent - (char*)d.treq, 0u);
+      seg(d.reach, (char*)d.treq + sg_bytes - (char*)d.reach, 0u);
     }
   }
-  if (!ck(c, cudaMemsetAsync(d.q, 0xff, q_bytes, st), "memset")) return GC_ERR_CUDA;
+  seg(d.q, q_bytes, 0xffffffffu);
+  {
+    size_t words = 0;
+    for (int j = 0; j < cl.cnt; ++j) words += cl.seg[j].n;
+    const size_t blocks = (words / 4 + 255) / 256;
+    k_clear<<<(unsigned)(blocks < 1 ? 1 : (blocks > 1184 ? 1184 : blocks)), 256, 0, st>>>(cl);
+    ++L.n;
+    if (!ck(c, cudaGetLastError(), "k_clear launch")) return GC_ERR_CUDA;
+  }
   Ctl ctl;
   ctl.relabel_budget = (long long)(c->alpha * (double)d.T * TPX);
   ctl.vis_budget = c->vis_mult * d.T;
