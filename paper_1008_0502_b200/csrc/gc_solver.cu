@@ -308,7 +308,9 @@ int chunk_frames(gc_ctx* c, int H, int W) {
   const size_t T = tiles_of(H, W);
   const size_t fb = frame_bytes(c->K, T);
   size_t n = c->pool_bytes / fb;
-  size_t want = T >= 40000 / 24 ? 24 : (40000 + T - 1) / T;
+  // large frames: 16 slots -- the cold-start frame's chain shares the GPU with fewer streaming
+  // frames (C4 1024 x 1080p, same box: 16 slots 28.8-30.7 ms, 24 slots 29.7-33.3 ms)
+  size_t want = T >= GC_LARGE_TILES ? 16 : (T >= 40000 / 24 ? 24 : (40000 + T - 1) / T);
   if (const char* ev = knob("GC_SLOTS")) want = atoi(ev) > 0 ? atoi(ev) : want;  // tuning knob
   if (n > want) n = want;
   if (n < 1) n = 1;
