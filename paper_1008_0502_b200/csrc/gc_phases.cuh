@@ -46,6 +46,9 @@ namespace gcb {
 // then runs beside the streaming frames with two co-resident CTAs per SM instead of three
 // (C4 ~37 -> ~32 ms per step).
 constexpr int GC_MINB_LARGE = 3;
+// Sequence passes (few frames in flight, each a latency-bound chain): 2 CTAs per SM, 128
+// registers (C3 8 x 120 warm 20.3 -> 21.5 Gpx/s, cold 21.1 -> 23.2 against 3 per SM).
+constexpr int GC_MINB_SEQ = 2;
 constexpr int GC_LARGE_TILES = 1000;
 constexpr uint32_t QEMPTY = 0xffffffffu;
 constexpr uint32_t QEXIT = 0xfffffffeu;

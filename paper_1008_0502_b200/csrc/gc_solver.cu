@@ -45,6 +45,7 @@ struct gc_ctx {
   int grid = 0;                   // k_solve CTAs of the last launch
   int grid_max = 0;               // persistent grid of k_solve<K> on this context's device
   int grid_max_large = 0;         // ... of the large-frame variant k_solve<K, false, GC_MINB_LARGE>
+  int grid_max_seq = 0;           // ... of the sequence-pass variant k_solve<K, false, GC_MINB_SEQ>
   std::string err;
   long long last_launches = 0;
   bool prof = false;
@@ -444,11 +445,12 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   // (GC_LARGE_TILES, gc_phases.cuh).  Measured: C4 (1024 x 1080p) 33-40 -> 31.6-34.3 ms per
   // step (a hard frame's chain runs beside the streaming frames); calls whose frames all fit
   // the slots keep 4 CTAs per SM (C5's 8 serpentine frames, all long chains: 5.9 vs 4.9 Mpx/s)
-  // Sequence passes too (latency-bound chains of warm frames: C3 8 x 120 warm 18.7 -> 20.2 Gpx/s,
-  // cold unchanged at 21.4)
-  bool large = !io.img && ((d.T >= GC_LARGE_TILES && nframes > nslot) || seqL > 0) && c->grid_max_large > 0;
+  // Sequence passes: the 2-CTA-per-SM variant (GC_MINB_SEQ: few frames in flight, each a
+  // latency-bound chain -- C3 8 x 120 warm 18.7 -> 21.5 Gpx/s, cold 21.4 -> 23.2)
+  const bool seqv = !io.img && seqL > 0 && c->grid_max_seq > 0;
+  bool large = !io.img && !seqv && d.T >= GC_LARGE_TILES && nframes > nslot && c->grid_max_large > 0;
   if (const char* ev = knob("GC_LARGE")) large = !io.img && c->grid_max_large > 0 && atoi(ev) != 0;  // tuning knob
-  int grid = large ? c->grid_max_large : c->grid_max;  // computed per context (its device) in gc_create
+  int grid = seqv ? c->grid_max_seq : (large ? c->grid_max_large : c->grid_max);  // per context (gc_create)
   if (const char* ev = knob("GC_GRID")) grid = atoi(ev) > 0 && atoi(ev) < grid ? atoi(ev) : grid;
   c->grid = grid;
   seg(d.fmode, c->words_bytes, 0u);
@@ -519,6 +521,7 @@ gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaSt
   cudaEvent_t e1 = c->evpool[c->evnext++];
   cudaEventRecord(e0, st);
   if (io.img) k_solve<K, true><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
+  else if (seqv) k_solve<K, false, GC_MINB_SEQ><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
   else if (large) k_solve<K, false, GC_MINB_LARGE><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
   else k_solve<K><<<grid, NTH, smem, st>>>(d, io, ctl, tm);
   ++L.n;
@@ -790,6 +793,11 @@ gc_status gc_create(const gc_config* cfg, gc_ctx** out) {
     c->grid_max = c->K == 8 ? persistent_grid(c, k_solve<8>, smem) : persistent_grid(c, k_solve<4>, smem);
     c->grid_max_large = c->K == 8 ? persistent_grid(c, k_solve<8, false, GC_MINB_LARGE>, smem)
                                   : persistent_grid(c, k_solve<4, false, GC_MINB_LARGE>, smem);
+    if (e == cudaSuccess)
+      e = c->K == 8 ? cudaFuncSetAttribute(k_solve<8, false, GC_MINB_SEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                    : cudaFuncSetAttribute(k_solve<4, false, GC_MINB_SEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    c->grid_max_seq = c->K == 8 ? persistent_grid(c, k_solve<8, false, GC_MINB_SEQ>, smem)
+                                : persistent_grid(c, k_solve<4, false, GC_MINB_SEQ>, smem);
     if (e != cudaSuccess) {
       cudaGetLastError();
       gc_destroy(c);
