@@ -305,13 +305,15 @@ int persistent_grid(gc_ctx* c, F kernel, size_t dyn_smem = 0) {
 // GPU busy -- about 40k tiles in flight, at least 24 frames.  More slots only lengthen the
 // task queue, i.e. the latency of every dependency-chain step (measured: 1080p 8-nbr runs
 // fastest with 15-40 slots, QVGA / VGA level off at 8k-16k tiles in flight).
-int chunk_frames(gc_ctx* c, int H, int W) {
+int chunk_frames(gc_ctx* c, int H, int W, bool energy = false) {
   const size_t T = tiles_of(H, W);
   const size_t fb = frame_bytes(c->K, T);
   size_t n = c->pool_bytes / fb;
   // large frames: 16 slots -- the cold-start frame's chain shares the GPU with fewer streaming
   // frames (C4 1024 x 1080p, same box: 16 slots 28.8-30.7 ms, 24 slots 29.7-33.3 ms)
-  size_t want = T >= GC_LARGE_TILES ? 16 : (T >= 40000 / 24 ? 24 : (40000 + T - 1) / T);
+  // (energy solves keep 24: their init pass is float64-heavy and wants the parallelism -- 16
+  // slots measured 234 vs 175 ms per 1024 frames)
+  size_t want = (T >= GC_LARGE_TILES && !energy) ? 16 : (T >= 40000 / 24 ? 24 : (40000 + T - 1) / T);
   if (const char* ev = knob("GC_SLOTS")) want = atoi(ev) > 0 ? atoi(ev) : want;  // tuning knob
   if (n > want) n = want;
   if (n < 1) n = 1;
@@ -399,7 +401,8 @@ template <int K>
 gc_status solve_chunk(gc_ctx* c, const IO& io, int nframes, int H, int W, cudaStream_t st, Launcher& L, int seqS = 0,
                       int seqL = 0, int seqWarm = 0, int32_t* caps_out = nullptr) {
   const int units = seqL ? seqS : nframes;  // slots serve frames, or whole sequences
-  const int nslot = chunk_frames(c, H, W) < units ? chunk_frames(c, H, W) : units;
+  const int cf = chunk_frames(c, H, W, io.img != nullptr);
+  const int nslot = cf < units ? cf : units;
   size_t sg_bytes = 0, q_bytes = 0;
   Dev d = carve(c, nslot, H, W, &sg_bytes, &q_bytes);
   if (seqL && seqWarm) {  // ping-pong flow buffers, two per slot
