@@ -78,3 +78,14 @@ def test_oracle_not_imported_by_product():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.cpp" not in txt, f
+
+
+def test_binding_constants_match_header():
+    """The binding's copies of the header's limits (no GPU needed)."""
+    import paper_1008_0502_b200 as gc
+    src = open(os.path.join(ROOT, "include", "gc.h")).read()
+    defs = dict(re.findall(r"#define (GC_[A-Z_]+) (.+)", src))
+    assert gc.PARTS_MAX == int(defs["GC_PARTS_MAX"])
+    assert gc.GMM_MAX == int(defs["GC_GMM_MAX"])
+    assert gc.PRIOR_RMAX == int(defs["GC_PRIOR_RMAX"])
+    assert defs["GC_CAP_MAX"].strip() == "((1 << 26) - 1)" and gc.CAP_MAX == (1 << 26) - 1
